@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark of the BRSVD hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (driver, N > 1)
+
+Workload (BASELINE.json configs[1], "config 2"): in-core fp32 32768 x 32768
+synthetic rank-256 + 1e-3 noise, k=256 p=32 q=2, one decomposition per step.
+The metric is the A-stream rate of SURVEY.md §8(d): (q+2) algorithmic passes
+over A (m*n*4 bytes each) per decomposition / time, in GB/s, whole job.
+
+  value  -- device-resident A (32768^2 fp32 = 4.3 GB > 126 MB L2, so no L2
+            flush is needed between steps), CUDA events on the library stream,
+            barrier + max over ranks.
+  e2e    -- the same decomposition through the reference-facing API
+            (rsvd_incore on a pinned host numpy array -> C ABI with host
+            pointers): H2D of A and D2H of U, sigma, Vt inside the timed region.
+  roofline -- the dominant kernel family (the A-streaming products), timed
+            live with CUDA events around each launch (brsvd_profile_*).
+  cpu_baseline -- the CPU oracle (oracle/ref_cpu.py, a restatement of the
+            reference's numpy path) on a row sample of the same matrix, all
+            host cores.
+
+With N > 1 each rank runs its own decomposition ("replicas", scaling weak):
+the in-core configuration has no cross-GPU exchange.  The row-sharded
+configuration with the NCCL all-reduce of Z is BASELINE config 4 (see
+DESIGN.md).
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+M = N_COLS = 32768
+RANK, NOISE = 256, 1e-3
+K, P, Q = 256, 32, 2
+PASSES = Q + 2
+METRIC = ("BRSVD rank-k A-stream GB/s, config 2 (in-core fp32 32768x32768 "
+          "rank-256+1e-3 noise, k=256 p=32 q=2)")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    return world, rank, local
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def a_stream_gbs(seconds, m=M, n=N_COLS, elsize=4, passes=PASSES):
+    return passes * m * n * elsize / seconds / 1e9
+
+
+def make_matrix(device, seed=1234):
+    """A = L R + 1e-3 N on the device (synthetic)."""
+    import torch
+    g = torch.Generator(device=device).manual_seed(seed)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    L = torch.randn(M, RANK, generator=g, device=device, dtype=torch.float32)
+    R = torch.randn(RANK, N_COLS, generator=g, device=device, dtype=torch.float32)
+    A = L @ R
+    torch.backends.cuda.matmul.allow_tf32 = prev
+    A.add_(torch.randn(M, N_COLS, generator=g, device=device, dtype=torch.float32),
+           alpha=NOISE)
+    del L, R
+    torch.cuda.synchronize(device)
+    return A
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+        "fallback"
+
+
+def cpu_baseline(A_dev, rows, reps=1):
+    """Time the CPU oracle (restatement of the reference numpy path) on the
+    first `rows` rows of A with all host cores."""
+    from oracle import ref_cpu
+    sample = A_dev[:rows].cpu().numpy()
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        ref_cpu.randomized_svd(sample, K, P, Q, seed=0)
+        times.append(time.perf_counter() - t0)
+    t = float(np.median(times))
+    return {
+        "value": a_stream_gbs(t, m=rows), "unit": "GB/s", "cores": os.cpu_count(),
+        "kind": "port",
+        "sample": f"rows 0..{rows} of the config-2 matrix ({rows}x{N_COLS} fp32), "
+                  f"k={K} p={P} q={Q}, oracle/ref_cpu.randomized_svd (numpy/OpenBLAS), "
+                  f"{t:.2f} s per decomposition",
+        "seconds": t,
+    }
+
+
+def run_reference(args, world, rank, local):
+    """--impl reference: the reference's CPU path (oracle port) on the host."""
+    if rank != 0:
+        return
+    import torch
+    budget_steps = max(args.steps + args.warmup, 1)
+    rows = int(min(16384, max(2048, 16384 * 8 // budget_steps)))
+    rows -= rows % 1024
+    from oracle import ref_cpu
+    dev = f"cuda:{local}" if torch.cuda.is_available() else "cpu"
+    if dev == "cpu":
+        rng = np.random.default_rng(1234)
+        sample = ((rng.standard_normal((rows, RANK), dtype=np.float32)
+                   @ rng.standard_normal((RANK, N_COLS), dtype=np.float32))
+                  + NOISE * rng.standard_normal((rows, N_COLS), dtype=np.float32))
+    else:
+        A = make_matrix(dev)
+        sample = A[:rows].cpu().numpy()
+        del A
+        torch.cuda.empty_cache()
+    for _ in range(args.warmup):
+        ref_cpu.randomized_svd(sample, K, P, Q, seed=0)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ref_cpu.randomized_svd(sample, K, P, Q, seed=0)
+    t = (time.perf_counter() - t0) / max(args.steps, 1)
+    v = a_stream_gbs(t, m=rows)
+    sample_desc = (f"rows 0..{rows} of the config-2 matrix ({rows}x{N_COLS} fp32), "
+                   f"oracle/ref_cpu.randomized_svd (numpy/OpenBLAS), {t:.2f} s/decomposition")
+    line = {
+        "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic", "impl": "reference",
+        "config": {"workload": "config2-row-sample", "m": rows, "n": N_COLS, "k": K,
+                   "p": P, "q": Q, "passes": PASSES},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": os.cpu_count(),
+                         "kind": "port", "sample": sample_desc},
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    from paper_1706_07191_b200 import SketchConfig, _lib
+    from paper_1706_07191_b200.rsvd import run_rsvd
+    import warnings
+    from paper_1706_07191_b200 import RankDeficiencyWarning
+    warnings.simplefilter("ignore", RankDeficiencyWarning)
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    os.environ["BRSVD_DEVICE"] = str(local)
+    cfg = SketchConfig(target_rank=K, oversampling=P, power_exponent=Q, master_seed=0)
+    A = make_matrix(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    # warm-up
+    for _ in range(args.warmup):
+        run_rsvd(A, cfg, warn=False)
+    torch.cuda.synchronize(dev)
+
+    # timed: device-resident A
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk, _lib.profile(local) as prof:
+        start.record(stream)
+        for _ in range(args.steps):
+            run = run_rsvd(A, cfg, warn=False)
+        stop.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier(world)
+    t_dev = start.elapsed_time(stop) / 1e3 / max(args.steps, 1)
+    t_dev = max_over_ranks(t_dev, world)
+    rep = prof.report
+    value = world * a_stream_gbs(t_dev)
+    st = run.stats
+
+    # roofline of the dominant kernel family
+    peaks, basis = measured_peaks()
+    big_ms_per_launch = rep.big_ms / max(rep.big_launches, 1)
+    flops_per_launch = rep.big_flops / max(rep.big_launches, 1)
+    achieved_tflops = flops_per_launch / (big_ms_per_launch * 1e-3) / 1e12
+    peak = peaks["bf16_tflops_sustained"] / 6.0
+    roofline = {
+        "bound": "tensor", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
+        "frac": achieved_tflops / peak, "traffic": None,
+        "kernel": "A-streaming products Y=A X / Z=A^T Y (2*m*n*l flops per launch)",
+        "peak_basis": f"{basis} bf16_tflops_sustained / 2 (TF32 rate) / 3 (3xTF32 split)",
+        "launch_ms": big_ms_per_launch, "launches_per_step": rep.big_launches / args.steps,
+        "share_of_step": rep.big_ms / (t_dev * 1e3 * args.steps),
+        "hbm_gbs_achieved": (rep.big_bytes / max(rep.big_launches, 1))
+        / (big_ms_per_launch * 1e-3) / 1e9,
+        "hbm_gbs_peak": peaks["hbm_gbs"],
+    }
+
+    # end to end through the reference-facing API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        pinned = torch.empty((M, N_COLS), dtype=torch.float32, pin_memory=True)
+        pinned.copy_(A)
+        a_host = pinned.numpy()
+        del A
+        torch.cuda.empty_cache()
+        for _ in range(max(1, min(args.warmup, 2))):
+            run_rsvd(a_host, cfg, warn=False)
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            r2 = run_rsvd(a_host, cfg, warn=False)
+            float(r2.factors.sigma[0])     # the result is on the host
+        t_e2e = (time.perf_counter() - t0) / max(args.steps, 1)
+        barrier(world)
+        t_e2e = max_over_ranks(t_e2e, world)
+        l = K + P
+        e2e = {"value": world * a_stream_gbs(t_e2e), "unit": "GB/s",
+               "ms_per_step": t_e2e * 1e3,
+               "h2d_bytes_per_step": M * N_COLS * 4,
+               "d2h_bytes_per_step": (M * l + l + l * N_COLS) * 4}
+        A = torch.as_tensor(a_host).to(dev)
+        del pinned
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline(A, 16384)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_dev * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "config2", "m": M, "n": N_COLS, "k": K, "p": P, "q": Q,
+                       "rank": RANK, "noise": NOISE, "passes": PASSES,
+                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "A (4.3 GB) exceeds L2; no flush needed"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(rep.gpu_launches),
+            "clocks": clk.summary(),
+            "stages_s": {"sketch": st.seconds_sketch, "orthonormalize": st.seconds_orthonormalize,
+                         "form_core": st.seconds_form_core, "svd": st.seconds_svd},
+            "sigma_top3": [float(x) for x in run.factors.sigma[:3].cpu()],
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank, local)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

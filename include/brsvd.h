@@ -1,0 +1,143 @@
+/* brsvd.h -- C ABI of the B200-native block randomized SVD (BRSVD) hot path.
+ *
+ * Drop-in boundary for the reference package `blocksvd`
+ * (/root/reference/pkg/src/blocksvd).  The reference is pure Python/numpy, so
+ * it has no FFI of its own; each entry point below replaces one Python
+ * function on the hot path and is bound from Python with ctypes by
+ * paper_1706_07191_b200/_lib.py (see INTEGRATION.md for the binding a
+ * maintainer would add to the reference):
+ *
+ *   brsvd_rsvd        <- rsvd_incore(a, cfg)              rsvd.py:126-141
+ *   brsvd_rsvd_stream <- brsvd_run / rsvd_naive_ooc       rsvd.py:188-284
+ *                        (row panels streamed from host memory)
+ *   brsvd_tsqr        <- tsqr_factor(y)                   kernels.py:139-164
+ *   brsvd_small_svd   <- small_svd(b)                     kernels.py:173-188
+ *   brsvd_gaussian    <- gaussian_matrix(...)             kernels.py:98-118
+ *   brsvd_rpca_*      <- _ialm_rpca_incore update step     rpca.py:188-211
+ *
+ * Conventions
+ *   - dtype codes are the .oocm element codes (store.py:14-15):
+ *     1 = binary64, 2 = binary32.
+ *   - Tall-skinny matrices (Omega, U, V) are column-major with leading
+ *     dimension = rows; Vt (l x n, row-major) is the same memory as V (n x l,
+ *     column-major).  A may be row- or column-major (`layout`).
+ *   - `where` flags say whether a pointer is host (pageable or pinned) or
+ *     device memory.  Host inputs are copied in, host outputs copied out;
+ *     calls are synchronous with respect to the host.
+ *   - Return value is a status code; brsvd_last_error() gives the message of
+ *     the last failing call on the calling thread.
+ *   - A context is not re-entrant: use one per thread (and per GPU).
+ */
+#ifndef BRSVD_H
+#define BRSVD_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define BRSVD_API __attribute__((visibility("default")))
+#else
+#define BRSVD_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum brsvd_status {
+  BRSVD_OK = 0,
+  BRSVD_ERR_CONFIG = 1,   /* ConfigError   rsvd.py:43-44      */
+  BRSVD_ERR_SHAPE = 2,    /* ShapeError    kernels.py:27-28   */
+  BRSVD_ERR_BUDGET = 3,   /* BudgetError   store.py:42-47     */
+  BRSVD_ERR_OVERFLOW = 4, /* FloatingPointError rsvd.py:84-91 */
+  BRSVD_ERR_CUDA = 5,
+  BRSVD_ERR_NCCL = 6,
+  BRSVD_ERR_ARG = 7
+};
+
+enum brsvd_dtype { BRSVD_F64 = 1, BRSVD_F32 = 2 };
+enum brsvd_layout { BRSVD_COL_MAJOR = 0, BRSVD_ROW_MAJOR = 1 };
+enum brsvd_where { BRSVD_DEVICE = 0, BRSVD_HOST = 1 };
+
+typedef struct brsvd_ctx brsvd_ctx;
+
+/* Mirrors PassStats (store.py:50-79) plus the diagnostics the reference
+ * raises as warnings/exceptions. */
+typedef struct brsvd_stats {
+  int64_t words_read;       /* elements of A read across the boundary   */
+  int64_t block_reads;      /* panel / block reads                       */
+  int64_t passes_num;       /* full passes = passes_num / passes_den     */
+  int64_t passes_den;
+  int64_t flop_estimate;    /* reference flop model rsvd.py:175-213       */
+  int32_t detected_rank;    /* numerical rank of the sample matrix Y      */
+  int32_t core_rank;        /* numerical rank of B^T inside small_svd     */
+  double max_abs_y0;        /* max |A Omega|                              */
+  double log10_peak_est;    /* log10 max|(A A^T)^q A Omega| (unnormalised) */
+  int32_t overflow;         /* 1 when the overflow guard fired            */
+  int32_t reserved;
+  double seconds_sketch;    /* stage timings (device events)             */
+  double seconds_orthonormalize;
+  double seconds_form_core;
+  double seconds_svd;
+} brsvd_stats;
+
+/* Device-side profile of the calls made between begin and end on this
+ * context: the big A-streaming products (CUDA events on the context stream)
+ * and the number of kernels launched by this thread. */
+typedef struct brsvd_profile {
+  int64_t big_launches;     /* launches of the A-streaming products        */
+  double big_ms;            /* summed event time of those launches          */
+  double big_flops;         /* algorithmic flops 2*m*n*l per launch, summed */
+  double big_bytes;         /* algorithmic A bytes m*n*elsize, summed       */
+  int64_t gpu_launches;     /* every kernel this library launched           */
+} brsvd_profile;
+
+BRSVD_API int brsvd_version(void);
+BRSVD_API const char* brsvd_last_error(void);
+
+/* Create a context on `device`.  `stream` is a cudaStream_t (NULL: the
+ * context creates its own non-blocking stream). */
+BRSVD_API int brsvd_ctx_create(int device, void* stream, brsvd_ctx** out);
+BRSVD_API int brsvd_ctx_set_stream(brsvd_ctx* ctx, void* stream);
+BRSVD_API int brsvd_ctx_destroy(brsvd_ctx* ctx);
+
+BRSVD_API int brsvd_profile_begin(brsvd_ctx* ctx);
+BRSVD_API int brsvd_profile_end(brsvd_ctx* ctx, brsvd_profile* out);
+
+/* In-core randomized SVD, global power iteration (rsvd_incore, rsvd.py:126).
+ *   A      m x n, leading dimension lda, `layout`, in `a_where` memory
+ *   k, p, q target rank, oversampling, power exponent (l = k + p)
+ *   omega  optional n x l column-major sketch (NULL: generated on device
+ *          from `seed`, stream 0, like rsvd.py:135-136)
+ *   U      m x l column-major,  sigma  l,  Vt  l x n row-major   (out_where)
+ * Returns BRSVD_ERR_OVERFLOW (after filling stats) when the unnormalised
+ * reference iteration would trip the guard of rsvd.py:84-91. */
+BRSVD_API int brsvd_rsvd(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda,
+               int dtype, int layout, int a_where, int k, int p, int q,
+               const void* omega, int omega_where, uint64_t seed, void* U,
+               void* sigma, void* Vt, int out_where, brsvd_stats* stats);
+
+/* Orthonormal basis of range(Y) (tsqr_factor, kernels.py:139-164).
+ *   Y m x l column-major (ldy); Q m x l column-major; R (optional) l x l
+ *   column-major with Y = Q R.  *detected_rank receives the numerical rank. */
+BRSVD_API int brsvd_tsqr(brsvd_ctx* ctx, const void* Y, int64_t m, int64_t l, int64_t ldy,
+               int dtype, int where, void* Q, void* R, int32_t* detected_rank);
+
+/* SVD of a short-fat l x n matrix B (small_svd, kernels.py:173-188).
+ *   B is given as its transpose Bt (n x l column-major, ldb), which is the
+ *   memory of a row-major l x n array.  Outputs W (l x l col-major), sigma
+ *   (l), Vt (l x n row-major). */
+BRSVD_API int brsvd_small_svd(brsvd_ctx* ctx, const void* Bt, int64_t n, int64_t l,
+                    int64_t ldb, int dtype, int where, void* W, void* sigma,
+                    void* Vt, int32_t* core_rank);
+
+/* Seeded i.i.d. N(0,1) matrix (gaussian_matrix, kernels.py:98-118):
+ * entry (i, j) is a pure function of (seed, stream, row_offset + i, j).
+ * out: rows x cols column-major (ld), device memory. */
+BRSVD_API int brsvd_gaussian(brsvd_ctx* ctx, void* out, int64_t rows, int64_t cols,
+                   int64_t ld, int dtype, uint64_t seed, uint64_t stream,
+                   int64_t row_offset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BRSVD_H */

@@ -1,0 +1,37 @@
+// The two products that stream the big matrix A once per call:
+//   big_nn:  Y (m x l) = A X,    X (n x l)     -- sample pass
+//   big_tn:  Z (n x l) = A^T Y,  Y (m x l)     -- transpose pass
+// They replace `a_block @ omega` / `a_block.T @ y` of _sketch_block
+// (rsvd.py:94-102) and `q_basis.T @ a` (rsvd.py:140).  A may be row- or
+// column-major; the tall-skinny operands are column-major.
+#pragma once
+#include "runtime.cuh"
+#include "tc_gemm.cuh"
+
+namespace brsvd {
+
+template <typename T>
+void big_nn(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool row_major,
+            const T* X, int64_t ldx, int l, T* Y, int64_t ldy) {
+  ProfScope ps(c, 2.0 * m * n * l, (double)m * n * sizeof(T));
+  if (tc_gemm_supported<T>(c, row_major, m, n, l, /*trans=*/false)) {
+    tc_gemm_launch<T>(c, A, m, n, lda, row_major, /*trans=*/false, X, ldx, l, Y, ldy);
+    return;
+  }
+  const int64_t sam = row_major ? lda : 1, sak = row_major ? 1 : lda;
+  gemm<T, T, T, T>(c, m, l, n, A, sam, sak, X, 1, ldx, Y, 1, ldy);
+}
+
+template <typename T>
+void big_tn(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool row_major,
+            const T* Yin, int64_t ldy, int l, T* Z, int64_t ldz) {
+  ProfScope ps(c, 2.0 * m * n * l, (double)m * n * sizeof(T));
+  if (tc_gemm_supported<T>(c, row_major, m, n, l, /*trans=*/true)) {
+    tc_gemm_launch<T>(c, A, m, n, lda, row_major, /*trans=*/true, Yin, ldy, l, Z, ldz);
+    return;
+  }
+  const int64_t sam = row_major ? 1 : lda, sak = row_major ? lda : 1;
+  gemm<T, T, T, T>(c, n, l, m, A, sam, sak, Yin, 1, ldy, Z, 1, ldz);
+}
+
+}  // namespace brsvd

@@ -1,0 +1,364 @@
+// extern "C" entry points declared in include/brsvd.h.  Each wraps the C++
+// runtime, converts exceptions into status codes and keeps the message for
+// brsvd_last_error() (per thread).
+#include <string>
+
+#include "../../include/brsvd.h"
+#include "pipeline.cuh"
+
+using namespace brsvd;
+
+namespace brsvd {
+thread_local long long g_brsvd_launches = 0;
+}
+
+struct brsvd_ctx {
+  Ctx c;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    g_last_error.clear();
+    return f();
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return kErrArg;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return kErrArg;
+  }
+}
+
+size_t esize(int dtype) {
+  if (dtype == BRSVD_F64) return 8;
+  if (dtype == BRSVD_F32) return 4;
+  throw Error(kErrArg, "dtype must be 1 (binary64) or 2 (binary32)");
+}
+
+// Device view of a (rows x cols, ld) column-major operand that may live on the
+// host: copies it in when needed.
+struct InView {
+  const void* dptr = nullptr;
+  int64_t ld = 0;
+  void* owned = nullptr;
+  cudaStream_t s = nullptr;
+  InView(Ctx& c, const void* p, int64_t rows, int64_t cols, int64_t ld_, size_t es,
+         int where) {
+    s = c.stream;
+    if (where == BRSVD_DEVICE) {
+      dptr = p;
+      ld = ld_;
+      return;
+    }
+    BRSVD_CUDA(cudaMallocAsync(&owned, (size_t)rows * cols * es, s));
+    BRSVD_CUDA(cudaMemcpy2DAsync(owned, rows * es, p, ld_ * es, rows * es, cols,
+                                 cudaMemcpyHostToDevice, s));
+    dptr = owned;
+    ld = rows;
+  }
+  ~InView() {
+    if (owned) cudaFreeAsync(owned, s);
+  }
+};
+
+struct OutView {
+  void* dptr = nullptr;
+  void* host = nullptr;
+  size_t bytes = 0;
+  cudaStream_t s = nullptr;
+  OutView(Ctx& c, void* p, size_t bytes_, int where) {
+    s = c.stream;
+    bytes = bytes_;
+    if (where == BRSVD_DEVICE || p == nullptr) {
+      dptr = p;
+      return;
+    }
+    host = p;
+    BRSVD_CUDA(cudaMallocAsync(&dptr, bytes, s));
+  }
+  void flush() {
+    if (host) BRSVD_CUDA(cudaMemcpyAsync(host, dptr, bytes, cudaMemcpyDeviceToHost, s));
+  }
+  ~OutView() {
+    if (host && dptr) cudaFreeAsync(dptr, s);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int brsvd_version(void) { return 1; }
+
+const char* brsvd_last_error(void) { return g_last_error.c_str(); }
+
+int brsvd_ctx_create(int device, void* stream, brsvd_ctx** out) {
+  return guarded([&] {
+    BRSVD_REQUIRE(out != nullptr, kErrArg, "out is NULL");
+    BRSVD_CUDA(cudaSetDevice(device));
+    auto* h = new brsvd_ctx();
+    h->c.device = device;
+    if (stream) {
+      h->c.stream = (cudaStream_t)stream;
+    } else {
+      BRSVD_CUDA(cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking));
+      h->c.own_stream = true;
+    }
+    BRSVD_CUDA(cudaHostAlloc((void**)&h->c.h_pinned, 64, cudaHostAllocDefault));
+    int sms = 0, optin = 0;
+    BRSVD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    BRSVD_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                                      device));
+    h->c.num_sms = sms;
+    h->c.max_smem_optin = (size_t)optin;
+    cudaMemPool_t pool;
+    BRSVD_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    BRSVD_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    *out = h;
+    return (int)kOk;
+  });
+}
+
+int brsvd_ctx_set_stream(brsvd_ctx* ctx, void* stream) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr, kErrArg, "ctx is NULL");
+    if (ctx->c.own_stream) {
+      BRSVD_CUDA(cudaStreamSynchronize(ctx->c.stream));
+      BRSVD_CUDA(cudaStreamDestroy(ctx->c.stream));
+      ctx->c.own_stream = false;
+    }
+    ctx->c.stream = (cudaStream_t)stream;
+    return (int)kOk;
+  });
+}
+
+int brsvd_ctx_destroy(brsvd_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return (int)kOk;
+    cudaStreamSynchronize(ctx->c.stream);
+    if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
+    if (ctx->c.h_pinned) cudaFreeHost(ctx->c.h_pinned);
+    delete ctx;
+    return (int)kOk;
+  });
+}
+
+int brsvd_profile_begin(brsvd_ctx* ctx) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr, kErrArg, "ctx is NULL");
+    Ctx& c = ctx->c;
+    for (auto e : c.prof_ev) cudaEventDestroy(e);
+    c.prof_ev.clear();
+    c.prof_flops = c.prof_bytes = 0.0;
+    c.prof = true;
+    c.prof_launch0 = g_brsvd_launches;
+    return (int)kOk;
+  });
+}
+
+int brsvd_profile_end(brsvd_ctx* ctx, brsvd_profile* out) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && out != nullptr, kErrArg, "NULL argument");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+    double ms = 0.0;
+    for (size_t i = 0; i + 1 < c.prof_ev.size(); i += 2) {
+      float t = 0.f;
+      BRSVD_CUDA(cudaEventElapsedTime(&t, c.prof_ev[i], c.prof_ev[i + 1]));
+      ms += t;
+    }
+    out->big_launches = (int64_t)(c.prof_ev.size() / 2);
+    out->big_ms = ms;
+    out->big_flops = c.prof_flops;
+    out->big_bytes = c.prof_bytes;
+    out->gpu_launches = g_brsvd_launches - c.prof_launch0;
+    for (auto e : c.prof_ev) cudaEventDestroy(e);
+    c.prof_ev.clear();
+    c.prof = false;
+    return (int)kOk;
+  });
+}
+
+int brsvd_rsvd(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda,
+               int dtype, int layout, int a_where, int k, int p, int q,
+               const void* omega, int omega_where, uint64_t seed, void* U,
+               void* sigma, void* Vt, int out_where, brsvd_stats* stats) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr, kErrArg, "ctx is NULL");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    const size_t es = esize(dtype);
+    BRSVD_REQUIRE(m >= 1 && n >= 1, kErrShape, "matrix must be non-empty");
+    BRSVD_REQUIRE(k >= 1, kErrConfig, "target rank must be positive");
+    BRSVD_REQUIRE(p >= 0, kErrConfig, "oversampling must be non-negative");
+    BRSVD_REQUIRE(k + p <= std::min(m, n), kErrConfig, "k + p exceeds min(m, n)");
+    BRSVD_REQUIRE(q >= 0, kErrConfig, "power exponent must be non-negative");
+    BRSVD_REQUIRE(k + p <= 1024, kErrConfig, "k + p above 1024 is not supported");
+    const int l = k + p;
+    const bool row_major = layout == BRSVD_ROW_MAJOR;
+    // A as a column-major (rows x cols) array: row-major A is A^T col-major.
+    const int64_t a_rows = row_major ? n : m, a_cols = row_major ? m : n;
+    BRSVD_REQUIRE(lda >= a_rows, kErrShape, "lda too small");
+    InView av(c, A, a_rows, a_cols, lda, es, a_where);
+    InView ov(c, omega, n, l, n, es, omega ? omega_where : BRSVD_DEVICE);
+    OutView uo(c, U, (size_t)m * l * es, out_where);
+    OutView so(c, sigma, (size_t)l * es, out_where);
+    OutView vo(c, Vt, (size_t)n * l * es, out_where);
+    RsvdInfo info;
+    if (dtype == BRSVD_F64) {
+      info = rsvd_device<double>(c, (const double*)av.dptr, m, n, av.ld, row_major, k,
+                                 p, q, (const double*)ov.dptr, seed, (double*)uo.dptr,
+                                 (double*)so.dptr, (double*)vo.dptr);
+    } else {
+      info = rsvd_device<float>(c, (const float*)av.dptr, m, n, av.ld, row_major, k, p,
+                                q, (const float*)ov.dptr, seed, (float*)uo.dptr,
+                                (float*)so.dptr, (float*)vo.dptr);
+    }
+    uo.flush();
+    so.flush();
+    vo.flush();
+    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+    if (stats) {
+      std::memset(stats, 0, sizeof(*stats));
+      stats->words_read = info.words_read;
+      stats->block_reads = info.block_reads;
+      stats->passes_num = info.words_read;
+      stats->passes_den = m * n;
+      stats->flop_estimate = (int64_t)2 * m * n * l * (2 * q + 2) +
+                             (int64_t)4 * m * l * l + (int64_t)2 * n * l * l;
+      stats->detected_rank = info.rank_y;
+      stats->core_rank = info.rank_b;
+      stats->max_abs_y0 = info.max_abs_y0;
+      stats->log10_peak_est = info.log10_peak;
+      stats->overflow = info.overflow ? 1 : 0;
+      stats->seconds_sketch = info.ms_sketch * 1e-3;
+      stats->seconds_orthonormalize = info.ms_orth * 1e-3;
+      stats->seconds_form_core = info.ms_core * 1e-3;
+      stats->seconds_svd = info.ms_svd * 1e-3;
+    }
+    if (info.overflow) {
+      throw Error(kErrOverflow,
+                  "sample matrix magnitude exceeds the overflow guard; lower the "
+                  "power exponent or rescale the input");
+    }
+    return (int)kOk;
+  });
+}
+
+int brsvd_tsqr(brsvd_ctx* ctx, const void* Y, int64_t m, int64_t l, int64_t ldy,
+               int dtype, int where, void* Q, void* R, int32_t* detected_rank) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr, kErrArg, "ctx is NULL");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    const size_t es = esize(dtype);
+    BRSVD_REQUIRE(l >= 1 && m >= l, kErrShape, "tsqr requires rows >= cols >= 1");
+    BRSVD_REQUIRE(l <= 1024, kErrShape, "tsqr supports at most 1024 columns");
+    InView yv(c, Y, m, l, ldy, es, where);
+    OutView qo(c, Q, (size_t)m * l * es, where);
+    OutView ro(c, R, (size_t)l * l * es, where);
+    DBuf<double> Qw(c, (size_t)m * l);
+    int rank;
+    if (dtype == BRSVD_F64) {
+      rank = orth_full<double>(c, (const double*)yv.dptr, m, (int)l, yv.ld, Qw.p,
+                               0x75717221ull, 2);
+      BRSVD_CUDA(cudaMemcpyAsync(qo.dptr, Qw.p, (size_t)m * l * 8,
+                                 cudaMemcpyDeviceToDevice, c.stream));
+      if (ro.dptr)
+        gemm_tn_cm<double, double, double>(c, l, l, m, Qw.p, m, (const double*)yv.dptr,
+                                           yv.ld, (double*)ro.dptr, l);
+    } else {
+      rank = orth_full<float>(c, (const float*)yv.dptr, m, (int)l, yv.ld, Qw.p,
+                              0x75717221ull, 1);
+      copy2d_kernel<double, float><<<grid_for(m * l), 256, 0, c.stream>>>(
+          Qw.p, m, l, m, (float*)qo.dptr, m);
+      BRSVD_CHECK_LAUNCH();
+      if (ro.dptr)
+        gemm_tn_cm<double, float, float>(c, l, l, m, Qw.p, m, (const float*)yv.dptr,
+                                         yv.ld, (float*)ro.dptr, l);
+    }
+    qo.flush();
+    ro.flush();
+    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+    if (detected_rank) *detected_rank = rank;
+    return (int)kOk;
+  });
+}
+
+int brsvd_small_svd(brsvd_ctx* ctx, const void* Bt, int64_t n, int64_t l,
+                    int64_t ldb, int dtype, int where, void* W, void* sigma,
+                    void* Vt, int32_t* core_rank) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr, kErrArg, "ctx is NULL");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    const size_t es = esize(dtype);
+    BRSVD_REQUIRE(l >= 1 && n >= l, kErrShape, "small_svd requires rows <= cols");
+    BRSVD_REQUIRE(l <= 1024, kErrShape, "small_svd supports at most 1024 rows");
+    InView bv(c, Bt, n, l, ldb, es, where);
+    OutView wo(c, W, (size_t)l * l * es, where);
+    OutView so(c, sigma, (size_t)l * es, where);
+    OutView vo(c, Vt, (size_t)n * l * es, where);
+    DBuf<double> Wd(c, (size_t)l * l), sd(c, l);
+    int rank;
+    if (dtype == BRSVD_F64) {
+      rank = small_svd_device<double>(c, (const double*)bv.dptr, n, (int)l, bv.ld, Wd.p,
+                                      sd.p, (double*)vo.dptr, n, 2);
+    } else {
+      rank = small_svd_device<float>(c, (const float*)bv.dptr, n, (int)l, bv.ld, Wd.p,
+                                     sd.p, (float*)vo.dptr, n, 1);
+    }
+    if (dtype == BRSVD_F64) {
+      BRSVD_CUDA(cudaMemcpyAsync(wo.dptr, Wd.p, (size_t)l * l * 8,
+                                 cudaMemcpyDeviceToDevice, c.stream));
+      BRSVD_CUDA(cudaMemcpyAsync(so.dptr, sd.p, (size_t)l * 8, cudaMemcpyDeviceToDevice,
+                                 c.stream));
+    } else {
+      copy2d_kernel<double, float><<<grid_for(l * l), 256, 0, c.stream>>>(
+          Wd.p, l, l, l, (float*)wo.dptr, l);
+      copy2d_kernel<double, float><<<1, 256, 0, c.stream>>>(sd.p, l, 1, l,
+                                                           (float*)so.dptr, l);
+      BRSVD_CHECK_LAUNCH();
+    }
+    wo.flush();
+    so.flush();
+    vo.flush();
+    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+    if (core_rank) *core_rank = rank;
+    return (int)kOk;
+  });
+}
+
+int brsvd_gaussian(brsvd_ctx* ctx, void* out, int64_t rows, int64_t cols, int64_t ld,
+                   int dtype, uint64_t seed, uint64_t stream, int64_t row_offset) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr, kErrArg, "ctx is NULL");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    BRSVD_REQUIRE(rows >= 1 && cols >= 1, kErrShape, "gaussian_matrix needs positive shape");
+    BRSVD_REQUIRE(ld >= rows, kErrShape, "ld too small");
+    const int g = grid_for(rows * ((cols + 1) / 2));
+    if (dtype == BRSVD_F64)
+      gaussian_kernel<double><<<g, 256, 0, c.stream>>>((double*)out, rows, cols, ld, seed,
+                                                       stream, row_offset);
+    else if (dtype == BRSVD_F32)
+      gaussian_kernel<float><<<g, 256, 0, c.stream>>>((float*)out, rows, cols, ld, seed,
+                                                      stream, row_offset);
+    else
+      throw Error(kErrArg, "bad dtype");
+    BRSVD_CHECK_LAUNCH();
+    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+    return (int)kOk;
+  });
+}
+
+}  // extern "C"

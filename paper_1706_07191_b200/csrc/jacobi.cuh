@@ -1,0 +1,213 @@
+// Block one-sided (Hestenes) Jacobi SVD of a small dense fp64 matrix.
+//
+// Replaces the LAPACK calls on the l-by-l problems of the reference:
+// np.linalg.svd(r.T) in small_svd (kernels.py:173-188) and, through the Gram
+// route, the Householder QR inside tsqr (kernels.py:121-164).
+//
+// G (nrow x ncol, column-major) is overwritten by G*V where V accumulates the
+// plane rotations (V must be the identity on entry).  Columns are grouped in
+// blocks of width bw; a round-robin tournament over the blocks pairs them up,
+// and each CTA of a cooperative grid orthogonalises the 2*bw columns of its
+// block pair in shared memory (one inner sweep per visit).  A single block pair
+// (small l: everything fits in one CTA) iterates its inner sweeps to
+// convergence, so the l <= ~110 case never touches the grid barrier.
+#pragma once
+#include <cooperative_groups.h>
+#include "common.cuh"
+
+namespace brsvd {
+namespace cg = cooperative_groups;
+
+struct JacobiArgs {
+  double* G;
+  int64_t ldg;
+  int nrow, ncol;
+  double* V;
+  int64_t ldv;
+  int bw, nb;  // block width; number of blocks (even)
+  int max_sweeps;
+  double tol;
+  int* rot_count;  // [max_sweeps] zero-initialised rotation counters
+  int* sweeps_done;
+};
+
+// Round-robin ("circle method") tournament: the player sitting at position
+// `pos` in round `r` among `n` (even) players.  Position i plays n-1-i.
+__device__ __forceinline__ int tourn(int pos, int r, int n) {
+  return pos == 0 ? 0 : ((pos - 1 + r) % (n - 1)) + 1;
+}
+
+// Rotate columns x, y (length nrow in Gs, length ncol in Vs) so they become
+// orthogonal.  Returns true if a rotation was applied.  Executed by one warp.
+__device__ __forceinline__ bool jacobi_rotate_pair(double* x, double* y,
+                                                   double* vx, double* vy,
+                                                   int nrow, int ncol,
+                                                   double tol, int lane) {
+  double a = 0.0, b = 0.0, g = 0.0;
+  for (int i = lane; i < nrow; i += 32) {
+    const double p = x[i], q = y[i];
+    a = fma(p, p, a);
+    b = fma(q, q, b);
+    g = fma(p, q, g);
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  g = warp_sum(g);
+  if (!(a > 0.0 && b > 0.0)) return false;
+  if (!(fabs(g) > tol * sqrt(a) * sqrt(b))) return false;
+  const double zeta = (b - a) / (2.0 * g);
+  double t;
+  if (fabs(zeta) > 1e150) {
+    t = 0.5 / zeta;
+  } else {
+    t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+  }
+  if (t == 0.0) return false;
+  const double c = 1.0 / sqrt(1.0 + t * t);
+  const double s = c * t;
+  for (int i = lane; i < nrow; i += 32) {
+    const double p = x[i], q = y[i];
+    x[i] = c * p - s * q;
+    y[i] = s * p + c * q;
+  }
+  for (int i = lane; i < ncol; i += 32) {
+    const double p = vx[i], q = vy[i];
+    vx[i] = c * p - s * q;
+    vy[i] = s * p + c * q;
+  }
+  return true;
+}
+
+__global__ void jacobi_block_kernel(JacobiArgs a) {
+  extern __shared__ double jsm[];
+  const int W = 2 * a.bw;
+  const int nrow = a.nrow, ncol = a.ncol;
+  double* Gs = jsm;                        // W columns of length nrow
+  double* Vs = jsm + (size_t)W * nrow;     // W columns of length ncol
+  int* cols = reinterpret_cast<int*>(Vs + (size_t)W * ncol);
+  __shared__ int s_rot;
+  __shared__ int s_stop;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int npairs = a.nb / 2;
+  const bool single = (a.nb == 2);
+  cg::grid_group grid = cg::this_grid();
+
+  for (int sweep = 0; sweep < a.max_sweeps; ++sweep) {
+    for (int round = 0; round < a.nb - 1; ++round) {
+      for (int pair = blockIdx.x; pair < npairs; pair += gridDim.x) {
+        const int ba = tourn(pair, round, a.nb);
+        const int bb = tourn(a.nb - 1 - pair, round, a.nb);
+        for (int c = threadIdx.x; c < W; c += blockDim.x) {
+          const int blk = c < a.bw ? ba : bb;
+          const int gc = blk * a.bw + (c % a.bw);
+          cols[c] = gc < ncol ? gc : -1;
+        }
+        __syncthreads();
+        for (int c = warp; c < W; c += nwarps) {
+          const int gc = cols[c];
+          for (int i = lane; i < nrow; i += 32)
+            Gs[(size_t)c * nrow + i] = gc >= 0 ? a.G[gc * a.ldg + i] : 0.0;
+          for (int i = lane; i < ncol; i += 32)
+            Vs[(size_t)c * ncol + i] = gc >= 0 ? a.V[gc * a.ldv + i] : 0.0;
+        }
+        __syncthreads();
+        const int inner = single ? 64 : 1;
+        int total = 0;
+        for (int is = 0; is < inner; ++is) {
+          if (threadIdx.x == 0) s_rot = 0;
+          __syncthreads();
+          for (int ir = 0; ir < W - 1; ++ir) {
+            for (int p = warp; p < W / 2; p += nwarps) {
+              const int ca = tourn(p, ir, W), cb = tourn(W - 1 - p, ir, W);
+              if (cols[ca] < 0 || cols[cb] < 0) continue;
+              const bool rot = jacobi_rotate_pair(
+                  Gs + (size_t)ca * nrow, Gs + (size_t)cb * nrow,
+                  Vs + (size_t)ca * ncol, Vs + (size_t)cb * ncol, nrow, ncol,
+                  a.tol, lane);
+              if (rot && lane == 0) atomicAdd(&s_rot, 1);
+            }
+            __syncthreads();
+          }
+          const int r = s_rot;
+          total += r;
+          __syncthreads();
+          if (r == 0) break;
+        }
+        if (threadIdx.x == 0 && total > 0) atomicAdd(&a.rot_count[sweep], total);
+        for (int c = warp; c < W; c += nwarps) {
+          const int gc = cols[c];
+          if (gc < 0) continue;
+          for (int i = lane; i < nrow; i += 32)
+            a.G[gc * a.ldg + i] = Gs[(size_t)c * nrow + i];
+          for (int i = lane; i < ncol; i += 32)
+            a.V[gc * a.ldv + i] = Vs[(size_t)c * ncol + i];
+        }
+        __syncthreads();
+      }
+      if (!single) grid.sync();
+    }
+    if (single) __threadfence_block(); else __threadfence();
+    if (!single) grid.sync();
+    if (threadIdx.x == 0) {
+      const int rc = atomicAdd(&a.rot_count[sweep], 0);
+      s_stop = (rc == 0);
+    }
+    __syncthreads();
+    if (s_stop) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) *a.sweeps_done = sweep + 1;
+      return;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.sweeps_done = a.max_sweeps;
+}
+
+// Column norms of G*V, descending rank sort, permuted outputs.
+//   sv[j]  = ||(G V)_{:, perm j}||,  Vout[:, j] = V[:, perm j],
+//   Uout[:, j] = (G V)[:, perm j] / sv[j]   (zero column if sv == 0).
+// One CTA; ncol <= 1024.
+__global__ void jacobi_finish_kernel(const double* __restrict__ G, int64_t ldg,
+                                     int nrow, int ncol,
+                                     const double* __restrict__ V, int64_t ldv,
+                                     double* __restrict__ sv,
+                                     double* __restrict__ Uout, int64_t ldu,
+                                     double* __restrict__ Vout, int64_t ldvo) {
+  extern __shared__ double fsm[];
+  double* nrm = fsm;                                  // ncol
+  int* perm = reinterpret_cast<int*>(fsm + ncol);     // ncol
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  for (int c = warp; c < ncol; c += nwarps) {
+    double s = 0.0;
+    for (int i = lane; i < nrow; i += 32) {
+      const double v = G[c * ldg + i];
+      s = fma(v, v, s);
+    }
+    s = warp_sum(s);
+    if (lane == 0) nrm[c] = sqrt(s);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < ncol; c += blockDim.x) {
+    const double v = nrm[c];
+    int rank = 0;
+    for (int o = 0; o < ncol; ++o) {
+      const double w = nrm[o];
+      rank += (w > v) || (w == v && o < c);
+    }
+    perm[rank] = c;
+  }
+  __syncthreads();
+  for (int j = warp; j < ncol; j += nwarps) {
+    const int c = perm[j];
+    const double s = nrm[c];
+    if (lane == 0 && sv != nullptr) sv[j] = s;
+    if (Uout != nullptr) {
+      const double inv = s > 0.0 ? 1.0 / s : 0.0;
+      for (int i = lane; i < nrow; i += 32) Uout[j * ldu + i] = G[c * ldg + i] * inv;
+    }
+    if (Vout != nullptr)
+      for (int i = lane; i < ncol; i += 32) Vout[j * ldvo + i] = V[c * ldv + i];
+  }
+}
+
+}  // namespace brsvd

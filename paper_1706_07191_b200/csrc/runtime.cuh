@@ -1,0 +1,425 @@
+// C++ runtime for the BRSVD hot path: device context, stream-ordered scratch
+// buffers, kernel launchers, rank-revealing orthonormalisation and the
+// in-core randomized SVD pipeline.
+//
+// Algorithm map (reference: /root/reference/pkg/src/blocksvd):
+//   rsvd_device      <- rsvd_incore        rsvd.py:126-141 (global power iter.)
+//   orth_full        <- tsqr / tsqr_factor kernels.py:139-170
+//   small_svd_device <- small_svd          kernels.py:173-188
+//   fix_signs        <- _fix_signs         rsvd.py:105-115
+//   overflow guard   <- _check_overflow    rsvd.py:84-91
+#pragma once
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "gemm_simt.cuh"
+#include "jacobi.cuh"
+#include "small_kernels.cuh"
+
+namespace brsvd {
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  unsigned long long* h_pinned = nullptr;  // small pinned readback area
+  int num_sms = kNumSMs;
+  size_t max_smem_optin = 0;
+  // profiling of the big A-streaming products (brsvd_profile_begin/end)
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_ev;  // start/stop pairs
+  double prof_flops = 0.0, prof_bytes = 0.0;
+  long long prof_launch0 = 0;
+};
+
+// Brackets one big-product launch with events when profiling is on.
+struct ProfScope {
+  Ctx& c;
+  bool on;
+  ProfScope(Ctx& c_, double flops, double bytes) : c(c_), on(c_.prof) {
+    if (!on) return;
+    cudaEvent_t e;
+    BRSVD_CUDA(cudaEventCreate(&e));
+    BRSVD_CUDA(cudaEventRecord(e, c.stream));
+    c.prof_ev.push_back(e);
+    c.prof_flops += flops;
+    c.prof_bytes += bytes;
+  }
+  ~ProfScope() {
+    if (!on) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) == cudaSuccess) {
+      cudaEventRecord(e, c.stream);
+      c.prof_ev.push_back(e);
+    }
+  }
+};
+
+// Stream-ordered device buffer (cudaMallocAsync from the device default pool).
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(Ctx& c, size_t count) { alloc(c, count); }
+  void alloc(Ctx& c, size_t count) {
+    release();
+    s = c.stream;
+    n = count;
+    if (count) BRSVD_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), s));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  operator T*() const { return p; }
+};
+
+inline int grid_for(int64_t total, int threads = 256, int max_blocks = 148 * 16) {
+  int64_t b = ceil_div(std::max<int64_t>(total, 1), threads);
+  return (int)std::min<int64_t>(b, max_blocks);
+}
+
+// ---------------------------------------------------------------------------
+// Strided GEMM launcher (deterministic split-K).
+template <typename TA, typename TB, typename TAcc, typename TC>
+void gemm(Ctx& c, int64_t M, int64_t N, int64_t K, const TA* A, int64_t sam,
+          int64_t sak, const TB* B, int64_t sbk, int64_t sbn, TC* C,
+          int64_t scm, int64_t scn, TAcc alpha = TAcc(1), TAcc beta = TAcc(0),
+          const TC* C0 = nullptr, int64_t sc0m = 0, int64_t sc0n = 0) {
+  if (M <= 0 || N <= 0) return;
+  constexpr bool dbl = sizeof(TAcc) == 8;
+  constexpr int BM = 64, BK = dbl ? 8 : 16, TM = 4;
+  const bool narrow = N <= 32;
+  const int BN = narrow ? 32 : 64;
+  const int64_t tiles = ceil_div(M, BM) * ceil_div(N, BN);
+  const int64_t target = 4 * c.num_sms;
+  const int64_t max_split = std::max<int64_t>(1, K / (BK * 4));
+  int64_t splits = std::min<int64_t>(std::max<int64_t>(1, ceil_div(target, tiles)),
+                                     std::min<int64_t>(max_split, 256));
+  int64_t kchunk = ceil_div(std::max<int64_t>(K, 1), splits);
+  kchunk = ceil_div(kchunk, BK) * BK;
+  splits = std::max<int64_t>(1, ceil_div(K, kchunk));
+  DBuf<TAcc> part;
+  if (splits > 1) part.alloc(c, (size_t)(splits * M * N));
+  dim3 grid((unsigned)ceil_div(M, BM), (unsigned)ceil_div(N, BN), (unsigned)splits);
+  if (narrow) {
+    gemm_strided_kernel<TA, TB, TAcc, TC, BM, 32, BK, TM, 2>
+        <<<grid, 256, 0, c.stream>>>(M, N, K, A, sam, sak, B, sbk, sbn, C, scm,
+                                      scn, alpha, beta, C0, sc0m, sc0n, kchunk,
+                                      part.p);
+  } else {
+    gemm_strided_kernel<TA, TB, TAcc, TC, BM, 64, BK, TM, 4>
+        <<<grid, 256, 0, c.stream>>>(M, N, K, A, sam, sak, B, sbk, sbn, C, scm,
+                                      scn, alpha, beta, C0, sc0m, sc0n, kchunk,
+                                      part.p);
+  }
+  BRSVD_CHECK_LAUNCH();
+  if (splits > 1) {
+    splitk_reduce_kernel<TAcc, TC><<<grid_for(M * N), 256, 0, c.stream>>>(
+        M, N, (int)splits, part.p, C, scm, scn, alpha, beta, C0, sc0m, sc0n);
+    BRSVD_CHECK_LAUNCH();
+  }
+}
+
+// Column-major helpers: C = op(X)... written out for readability.
+//   XtY:  C (a x b) = X(r x a)^T Y(r x b)
+template <typename TX, typename TY, typename TC>
+void gemm_tn_cm(Ctx& c, int64_t a, int64_t b, int64_t r, const TX* X, int64_t ldx,
+                const TY* Y, int64_t ldy, TC* C, int64_t ldc) {
+  gemm<TX, TY, double, TC>(c, a, b, r, X, ldx, 1, Y, 1, ldy, C, 1, ldc);
+}
+//   XT:  C (r x b) = alpha X(r x a) T(a x b) + beta C0
+template <typename TX, typename TT, typename TC>
+void gemm_nn_cm(Ctx& c, int64_t r, int64_t b, int64_t a, const TX* X, int64_t ldx,
+                const TT* T, int64_t ldt, TC* C, int64_t ldc, double alpha = 1.0,
+                double beta = 0.0, const TC* C0 = nullptr, int64_t ldc0 = 0) {
+  gemm<TX, TT, double, TC>(c, r, b, a, X, 1, ldx, T, 1, ldt, C, 1, ldc, alpha,
+                           beta, C0, 1, ldc0);
+}
+
+// ---------------------------------------------------------------------------
+// Jacobi SVD launcher: G (nrow x ncol, ldg) <- G V, V (ncol x ncol) accumulated.
+inline int jacobi(Ctx& c, double* G, int nrow, int ncol, int64_t ldg, double* V,
+                  int64_t ldv, int max_sweeps = 60) {
+  BRSVD_REQUIRE(ncol >= 1 && ncol <= 1024 && nrow >= 1, kErrShape,
+                "jacobi: unsupported small-problem shape");
+  const size_t budget = std::min<size_t>(c.max_smem_optin, 200 * 1024);
+  const size_t per_col = (size_t)(nrow + ncol) * sizeof(double) + sizeof(int);
+  int bw_fit = (int)(budget / (2 * per_col));
+  BRSVD_REQUIRE(bw_fit >= 1, kErrShape, "jacobi: column too long for shared memory");
+  int bw = (ncol + 1) / 2;
+  bool single = true;
+  if (bw > bw_fit) {
+    bw = std::min(bw_fit, 32);
+    single = false;
+  }
+  int nb = (int)ceil_div(ncol, bw);
+  if (nb < 2) nb = 2;
+  if (nb & 1) ++nb;
+  if (nb == 2) single = true;
+  const int threads = std::min(1024, std::max(64, bw * 32));
+  const size_t smem = (size_t)2 * bw * per_col;
+  static bool attr_set = false;
+  if (!attr_set) {
+    BRSVD_CUDA(cudaFuncSetAttribute(jacobi_block_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)budget));
+    attr_set = true;
+  }
+  DBuf<int> counters(c, (size_t)max_sweeps + 1);
+  BRSVD_CUDA(cudaMemsetAsync(counters.p, 0, sizeof(int) * (max_sweeps + 1), c.stream));
+  JacobiArgs args;
+  args.G = G;
+  args.ldg = ldg;
+  args.nrow = nrow;
+  args.ncol = ncol;
+  args.V = V;
+  args.ldv = ldv;
+  args.bw = bw;
+  args.nb = nb;
+  args.max_sweeps = max_sweeps;
+  args.tol = std::sqrt((double)nrow) * 2.220446049250313e-16;
+  args.rot_count = counters.p;
+  args.sweeps_done = counters.p + max_sweeps;
+  if (single) {
+    jacobi_block_kernel<<<1, threads, smem, c.stream>>>(args);
+    BRSVD_CHECK_LAUNCH();
+  } else {
+    int grid = nb / 2;
+    int per_sm = 0;
+    BRSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, jacobi_block_kernel, threads, smem));
+    grid = std::min(grid, std::max(1, per_sm) * c.num_sms);
+    void* kargs[] = {&args};
+    BRSVD_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_block_kernel, dim3(grid),
+                                           dim3(threads), kargs, smem, c.stream));
+    ++g_brsvd_launches;
+  }
+  return nb;
+}
+
+inline void jacobi_finish(Ctx& c, const double* G, int nrow, int ncol, int64_t ldg,
+                          const double* V, int64_t ldv, double* sv, double* Uout,
+                          int64_t ldu, double* Vout, int64_t ldvo) {
+  const size_t smem = (size_t)ncol * (sizeof(double) + sizeof(int));
+  jacobi_finish_kernel<<<1, 1024, smem, c.stream>>>(G, ldg, nrow, ncol, V, ldv, sv,
+                                                    Uout, ldu, Vout, ldvo);
+  BRSVD_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------------------
+// Eigen-decomposition of the (optionally column-scaled) Gram of X (r x l):
+//   s_j = 1/||x_j|| (or 1),  (S X^T X S) = E diag(lam) E^T  (lam sorted desc)
+// trace (device, optional) receives ||X||_F^2.
+template <typename T>
+void gram_eig(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* E,
+              double* lam, double* s, bool scale = true, double* trace = nullptr) {
+  DBuf<double> G(c, (size_t)l * l), V(c, (size_t)l * l);
+  gemm_tn_cm<T, T, double>(c, l, l, r, X, ldx, X, ldx, G.p, l);
+  gram_prep_kernel<<<1, 1024, 0, c.stream>>>(G.p, l, s, V.p, scale ? 1 : 0, trace);
+  BRSVD_CHECK_LAUNCH();
+  jacobi(c, G.p, l, l, l, V.p, l);
+  jacobi_finish(c, G.p, l, l, l, V.p, l, lam, nullptr, 0, E, l);
+}
+
+inline double orth_tau(int64_t r, int l) {
+  return 8.0 * (double)std::max<int64_t>(r, l) * 2.220446049250313e-16;
+}
+
+// Regularised basis change for the power iteration: Xout = X S E Lam^-1/2
+// with eigenvalues floored at tau*lam_0.  Same column span as X (exact
+// arithmetic), conditioning restored; no host synchronisation.
+template <typename T>
+void normalize_sketch(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, T* Xout,
+                      int64_t ldo) {
+  DBuf<double> E(c, (size_t)l * l), lam(c, l), s(c, l), Tm(c, (size_t)l * l);
+  gram_eig<T>(c, X, r, l, ldx, E.p, lam.p, s.p);
+  build_basis_kernel<<<1, 1024, 0, c.stream>>>(E.p, lam.p, s.p, l, orth_tau(r, l),
+                                               0, Tm.p, nullptr);
+  BRSVD_CHECK_LAUNCH();
+  gemm_nn_cm<T, double, T>(c, r, l, l, X, ldx, Tm.p, l, Xout, ldo);
+}
+
+// Readback of a few device scalars (one synchronisation).
+inline void readback(Ctx& c, const void* d, void* h, size_t bytes) {
+  BRSVD_CUDA(cudaMemcpyAsync(c.h_pinned, d, bytes, cudaMemcpyDeviceToHost, c.stream));
+  BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+  std::memcpy(h, c.h_pinned, bytes);
+}
+
+inline int read_int(Ctx& c, const int* d) {
+  int v;
+  readback(c, d, &v, sizeof(int));
+  return v;
+}
+
+// Block projection X <- X - Qb (Qb^T X), applied twice ("twice is enough").
+inline void project_out(Ctx& c, const double* Qb, int64_t r, int kq, double* X,
+                        int cols) {
+  if (kq <= 0 || cols <= 0) return;
+  DBuf<double> Cm(c, (size_t)kq * cols);
+  for (int pass = 0; pass < 2; ++pass) {
+    gemm_tn_cm<double, double, double>(c, kq, cols, r, Qb, r, X, r, Cm.p, kq);
+    gemm_nn_cm<double, double, double>(c, r, cols, kq, Qb, r, Cm.p, kq, X, r, -1.0,
+                                       1.0, X, r);
+  }
+}
+
+// Newton-Schulz polar refinement of the r x k block Q: Q <- Q (1.5 I - 0.5 Q^T Q).
+inline void ns_refine(Ctx& c, double* Q, int64_t r, int k, int iters) {
+  if (k <= 0 || iters <= 0) return;
+  DBuf<double> G2(c, (size_t)k * k), T2(c, (size_t)k * k), Qt(c, (size_t)r * k);
+  for (int it = 0; it < iters; ++it) {
+    gemm_tn_cm<double, double, double>(c, k, k, r, Q, r, Q, r, G2.p, k);
+    ns_matrix_kernel<<<grid_for((int64_t)k * k), 256, 0, c.stream>>>(G2.p, k, T2.p);
+    BRSVD_CHECK_LAUNCH();
+    gemm_nn_cm<double, double, double>(c, r, k, k, Q, r, T2.p, k, Qt.p, r);
+    BRSVD_CUDA(cudaMemcpyAsync(Q, Qt.p, sizeof(double) * r * k,
+                               cudaMemcpyDeviceToDevice, c.stream));
+  }
+}
+
+// Rank-revealing orthonormal basis of range(X), X (r x l), r >= l.
+//
+// Level 1: column-scaled Gram, Jacobi eigenpairs, keep lam > tau*lam_0,
+// Q1 = X S E Lam^-1/2, Newton-Schulz polish.  A Gram resolves directions down
+// to ~sqrt(tau) of the largest; Householder QR (the reference's tsqr,
+// kernels.py:121-164) resolves down to eps.  To match it, the unresolved
+// remainder R = (I - Q Q^T) X is deflated level by level (unscaled Gram, same
+// threshold relative to its own scale) while ||R||_F exceeds
+// 100 * l * eps_data * ||X||_F.  Whatever is left is numerically null: the
+// missing columns are Gaussian vectors projected out twice and orthonormalised
+// (kernels.py:142-144: "columns of Q remain orthonormal").
+// Returns the detected numerical rank; Q is r x l, fp64, ld r.
+template <typename T>
+int orth_full(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* Q,
+              uint64_t seed, int ns_iters) {
+  const double eps_data = sizeof(T) == 8 ? 2.220446049250313e-16 : 1.1920928955078125e-07;
+  const double tau = orth_tau(r, l);
+  DBuf<double> E(c, (size_t)l * l), lam(c, l), s(c, l), Tm(c, (size_t)l * l);
+  DBuf<double> scal(c, 4);
+  DBuf<int> drank(c, 1);
+  gram_eig<T>(c, X, r, l, ldx, E.p, lam.p, s.p, true, scal.p);
+  build_basis_kernel<<<1, 1024, 0, c.stream>>>(E.p, lam.p, s.p, l, tau, 1, Tm.p,
+                                               drank.p);
+  BRSVD_CHECK_LAUNCH();
+  BRSVD_CUDA(cudaMemcpyAsync(scal.p + 1, drank.p, sizeof(int), cudaMemcpyDeviceToDevice,
+                             c.stream));
+  double hs[2];
+  readback(c, scal.p, hs, sizeof(hs));
+  const double normx2 = hs[0];
+  int rk;
+  std::memcpy(&rk, &hs[1], sizeof(int));
+  int total = rk;
+  if (rk > 0) {
+    gemm_nn_cm<T, double, double>(c, r, rk, l, X, ldx, Tm.p, l, Q, r);
+    ns_refine(c, Q, r, rk, ns_iters);
+  }
+  if (total < l && normx2 > 0.0) {
+    // deflation levels on the unresolved remainder
+    DBuf<double> R(c, (size_t)r * l);
+    copy2d_kernel<T, double><<<grid_for(r * l), 256, 0, c.stream>>>(X, r, l, ldx, R.p, r);
+    BRSVD_CHECK_LAUNCH();
+    const double stop2 = std::pow(100.0 * l * eps_data, 2) * normx2;
+    for (int level = 0; level < 4 && total < l; ++level) {
+      project_out(c, Q, r, total, R.p, l);
+      gram_eig<double>(c, R.p, r, l, r, E.p, lam.p, s.p, false, scal.p);
+      build_basis_kernel<<<1, 1024, 0, c.stream>>>(E.p, lam.p, s.p, l, tau, 1, Tm.p,
+                                                   drank.p);
+      BRSVD_CHECK_LAUNCH();
+      BRSVD_CUDA(cudaMemcpyAsync(scal.p + 1, drank.p, sizeof(int),
+                                 cudaMemcpyDeviceToDevice, c.stream));
+      readback(c, scal.p, hs, sizeof(hs));
+      int rk2;
+      std::memcpy(&rk2, &hs[1], sizeof(int));
+      if (!(hs[0] > stop2) || rk2 <= 0) break;
+      rk2 = std::min(rk2, l - total);
+      double* Qn = Q + (int64_t)total * r;
+      gemm_nn_cm<double, double, double>(c, r, rk2, l, R.p, r, Tm.p, l, Qn, r);
+      project_out(c, Q, r, total, Qn, rk2);
+      ns_refine(c, Qn, r, rk2, std::max(ns_iters, 1));
+      total += rk2;
+    }
+  }
+  if (total < l) {
+    const int cnt = l - total;
+    double* W = Q + (int64_t)total * r;
+    gaussian_kernel<double><<<grid_for(r * ((cnt + 1) / 2)), 256, 0, c.stream>>>(
+        W, r, cnt, r, seed, 0x636f6d706c657465ull, 0);
+    BRSVD_CHECK_LAUNCH();
+    project_out(c, Q, r, total, W, cnt);
+    DBuf<double> Wq(c, (size_t)r * cnt);
+    orth_full<double>(c, W, r, cnt, r, Wq.p, seed * 0x9E3779B97F4A7C15ull + 1,
+                      std::max(ns_iters, 1));
+    BRSVD_CUDA(cudaMemcpyAsync(W, Wq.p, sizeof(double) * r * cnt,
+                               cudaMemcpyDeviceToDevice, c.stream));
+    project_out(c, Q, r, total, W, cnt);
+    ns_refine(c, W, r, cnt, 1);
+  }
+  return total;
+}
+
+// ---------------------------------------------------------------------------
+// small_svd (kernels.py:173-188): B^T (n x l, given as Bt) = Qb R,
+// R^T = W diag(sigma) Zj^T  (one-sided Jacobi),  V = Qb Zj.
+// Outputs: W (l x l fp64, ld l), sigma (fp64), Vout (n x l, T, ld ldv).
+template <typename T>
+int small_svd_device(Ctx& c, const T* Bt, int64_t n, int l, int64_t ldb, double* W,
+                     double* sigma, T* Vout, int64_t ldv, int ns_iters) {
+  DBuf<double> Qb(c, (size_t)n * l), M(c, (size_t)l * l), Vj(c, (size_t)l * l),
+      Zj(c, (size_t)l * l);
+  const int rank = orth_full<T>(c, Bt, n, l, ldb, Qb.p, 0x5eedb5ull, ns_iters);
+  // M = Bt^T Qb = R^T
+  gemm_tn_cm<T, double, double>(c, l, l, n, Bt, ldb, Qb.p, n, M.p, l);
+  eye_kernel<<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(Vj.p, l);
+  BRSVD_CHECK_LAUNCH();
+  jacobi(c, M.p, l, l, l, Vj.p, l);
+  jacobi_finish(c, M.p, l, l, l, Vj.p, l, sigma, W, l, Zj.p, l);
+  gemm_nn_cm<double, double, T>(c, n, l, l, Qb.p, n, Zj.p, l, Vout, ldv);
+  return rank;
+}
+
+template <typename T>
+void fix_signs(Ctx& c, T* U, int64_t m, int l, int64_t ldu, T* V, int64_t n,
+               int64_t ldv) {
+  DBuf<T> sign(c, l);
+  colsign_kernel<T><<<l, 256, 0, c.stream>>>(U, m, ldu, sign.p);
+  BRSVD_CHECK_LAUNCH();
+  scale_cols_kernel<T><<<grid_for(m * l), 256, 0, c.stream>>>(U, m, l, ldu, sign.p);
+  BRSVD_CHECK_LAUNCH();
+  scale_cols_kernel<T><<<grid_for(n * l), 256, 0, c.stream>>>(V, n, l, ldv, sign.p);
+  BRSVD_CHECK_LAUNCH();
+}
+
+struct MaxAbs {
+  double peak;
+  bool nonfinite;
+};
+
+template <typename T>
+MaxAbs maxabs(Ctx& c, const T* X, int64_t rows, int64_t cols, int64_t ld) {
+  DBuf<unsigned long long> out(c, 2);
+  BRSVD_CUDA(cudaMemsetAsync(out.p, 0, 2 * sizeof(unsigned long long), c.stream));
+  maxabs_kernel<T><<<grid_for(rows * cols), 256, 0, c.stream>>>(X, rows, cols, ld,
+                                                                 out.p);
+  BRSVD_CHECK_LAUNCH();
+  BRSVD_CUDA(cudaMemcpyAsync(c.h_pinned, out.p, 2 * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, c.stream));
+  BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+  MaxAbs r;
+  long long bits = (long long)c.h_pinned[0];
+  std::memcpy(&r.peak, &bits, sizeof(double));
+  r.nonfinite = c.h_pinned[1] != 0;
+  return r;
+}
+
+}  // namespace brsvd

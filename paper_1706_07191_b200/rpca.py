@@ -1,0 +1,184 @@
+"""Robust PCA by inexact ALM with a randomized inner SVD, on the B200.
+
+Drop-in for ``blocksvd.rpca`` (rpca.py): same configuration/result types and
+solver semantics (rpca.py:168-213).  The whole iteration -- spectral-norm
+estimate, randomized SVD of the iterate, singular-value shrinkage, the fused
+low-rank/sparse/dual update and the residual -- runs on the GPU behind
+``brsvd_ialm`` (include/brsvd.h); the host only checks the stopping rule the
+library reports.
+"""
+
+import ctypes
+import json
+import os
+import tempfile
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._arrays import DeviceMatrix, HostMatrix, is_torch, torch_stream_ptr
+from .store import MatrixStore
+
+__all__ = ["RpcaConfig", "RpcaResult", "shrink", "spectral_norm_estimate",
+           "ialm_rpca"]
+
+
+def shrink(x, epsilon):
+    """Soft-thresholding sign(x) * max(|x| - eps, 0) (rpca.py:35-45).
+
+    Works on scalars, numpy arrays and torch tensors; shape is preserved.
+    """
+    if epsilon < 0:
+        raise ValueError(f"shrinkage threshold must be non-negative, got {epsilon}")
+    if is_torch(x):
+        import torch
+        return torch.sign(x) * torch.clamp(torch.abs(x) - epsilon, min=0.0)
+    x = np.asarray(x)
+    out = np.sign(x) * np.maximum(np.abs(x) - epsilon, 0.0)
+    return out if out.ndim else float(out)
+
+
+@dataclass
+class RpcaConfig:
+    """Solver parameters (rpca.py:103-133)."""
+
+    target_rank: int
+    oversampling: int = 10
+    power_exponent: int = 1
+    lam: float = None
+    mu0: float = None
+    rho: float = 1.5
+    tol: float = 1e-7
+    max_iterations: int = 100
+    master_seed: int = 0
+    memory_budget_bytes: int = None
+
+    def validate(self):
+        if self.lam is not None and self.lam <= 0:
+            raise ValueError("lambda must be positive")
+        if self.mu0 is not None and self.mu0 <= 0:
+            raise ValueError("mu0 must be positive")
+        if self.rho <= 1:
+            raise ValueError("rho must exceed 1")
+        if self.tol <= 0:
+            raise ValueError("tol must be positive")
+        if self.max_iterations < 1:
+            raise ValueError("max_iterations must be positive")
+
+
+@dataclass
+class RpcaResult:
+    """Low-rank / sparse split with the convergence trace (rpca.py:136-150)."""
+
+    L: object
+    S: object
+    iterations: int
+    residual_history: list
+    converged: bool
+    history: list = field(default_factory=list)
+
+    def to_json_lines(self):
+        return "\n".join(json.dumps(e) for e in self.history)
+
+
+def _require(name):
+    lib = _lib.load_library()
+    if not hasattr(lib, name):
+        raise _lib.BackendUnavailable(f"{name} missing from {_lib.LIB_PATH}")
+    return getattr(lib, name)
+
+
+def spectral_norm_estimate(source, seed=0, tol=1e-10, max_iterations=100):
+    """Largest singular value by power iteration on M^T M (rpca.py:72-100).
+
+    Runs on the GPU; a zero matrix returns 0 with a warning.
+    """
+    import warnings
+    if isinstance(source, MatrixStore):
+        source = source.read_full()
+    mat = DeviceMatrix(source) if is_torch(source) else HostMatrix(source, "M")
+    m, n = mat.shape
+    fn = _require("brsvd_spectral_norm")
+    ctx = _lib.context(getattr(mat, "device", None))
+    if is_torch(source):
+        ctx.set_stream(torch_stream_ptr(mat.t))
+    out = ctypes.c_double()
+    iters = ctypes.c_int32()
+    _lib.check(fn(ctx.handle, mat.ptr, m, n, mat.ld, mat.code, mat.layout,
+                  _lib.DEVICE if is_torch(source) else _lib.HOST,
+                  ctypes.c_uint64(int(seed) & (2 ** 64 - 1)), ctypes.c_double(tol),
+                  int(max_iterations), ctypes.byref(out), ctypes.byref(iters)))
+    if out.value == 0.0:
+        warnings.warn("spectral_norm_estimate: zero matrix")
+        return 0.0
+    return float(out.value)
+
+
+def ialm_rpca(m_input, cfg):
+    """Inexact-ALM robust PCA with a randomized inner SVD (rpca.py:153-213).
+
+    Non-convergence at max_iterations returns ``converged=False``.  numpy (or
+    store) input gives numpy output; a torch CUDA tensor keeps everything on
+    the device.  When the reference would take its out-of-core branch
+    (store payload above ``memory_budget_bytes``, rpca.py:160-163) the split
+    is returned as MatrixStore objects as it does.
+    """
+    cfg.validate()
+    as_stores = False
+    if isinstance(m_input, MatrixStore):
+        budget = cfg.memory_budget_bytes
+        as_stores = budget is not None and m_input.payload_bytes > budget
+        m_input = m_input.read_full()
+    device = is_torch(m_input)
+    mat = DeviceMatrix(m_input) if device else HostMatrix(m_input, "M")
+    m, n = mat.shape
+    fn = _require("brsvd_ialm")
+    ctx = _lib.context(getattr(mat, "device", None))
+    maxit = int(cfg.max_iterations)
+    if device:
+        import torch
+        ctx.set_stream(torch_stream_ptr(mat.t))
+        # outputs share the input layout
+        if mat.layout == _lib.ROW_MAJOR:
+            L = torch.empty((m, n), dtype=mat.t.dtype, device=mat.t.device)
+            S = torch.empty((m, n), dtype=mat.t.dtype, device=mat.t.device)
+        else:
+            L = torch.empty((n, m), dtype=mat.t.dtype, device=mat.t.device).t()
+            S = torch.empty((n, m), dtype=mat.t.dtype, device=mat.t.device).t()
+        lp, sp = ctypes.c_void_p(L.data_ptr()), ctypes.c_void_p(S.data_ptr())
+        where = _lib.DEVICE
+    else:
+        order = "C" if mat.layout == _lib.ROW_MAJOR else "F"
+        L = np.empty((m, n), dtype=mat.dtype, order=order)
+        S = np.empty((m, n), dtype=mat.dtype, order=order)
+        lp, sp = ctypes.c_void_p(L.ctypes.data), ctypes.c_void_p(S.ctypes.data)
+        where = _lib.HOST
+    res = np.zeros(maxit, dtype=np.float64)
+    mus = np.zeros(maxit, dtype=np.float64)
+    svd_s = np.zeros(maxit, dtype=np.float64)
+    it_s = np.zeros(maxit, dtype=np.float64)
+    iters = ctypes.c_int32()
+    conv = ctypes.c_int32()
+    nan = float("nan")
+    dptr = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    _lib.check(fn(
+        ctx.handle, mat.ptr, m, n, mat.ld, mat.code, mat.layout, where,
+        int(cfg.target_rank), int(cfg.oversampling), int(cfg.power_exponent),
+        ctypes.c_uint64(int(cfg.master_seed) & (2 ** 64 - 1)),
+        ctypes.c_double(nan if cfg.lam is None else float(cfg.lam)),
+        ctypes.c_double(nan if cfg.mu0 is None else float(cfg.mu0)),
+        ctypes.c_double(float(cfg.rho)), ctypes.c_double(float(cfg.tol)), maxit,
+        lp, sp, where, ctypes.byref(iters), ctypes.byref(conv),
+        dptr(res), dptr(mus), dptr(svd_s), dptr(it_s)))
+    k = iters.value
+    residuals = [float(r) for r in res[:k]]
+    history = [{"i": i + 1, "mu": float(mus[i]), "residual": float(res[i]),
+                "svd_seconds": float(svd_s[i]), "iter_seconds": float(it_s[i])}
+               for i in range(k)]
+    if as_stores:
+        workdir = tempfile.mkdtemp(prefix="rpca_")
+        L = MatrixStore.from_array(os.path.join(workdir, "lowrank.oocm"), L)
+        S = MatrixStore.from_array(os.path.join(workdir, "sparse.oocm"), S)
+    return RpcaResult(L=L, S=S, iterations=k, residual_history=residuals,
+                      converged=bool(conv.value), history=history)

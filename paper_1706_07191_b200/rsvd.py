@@ -1,0 +1,290 @@
+"""Randomized SVD entry points on the B200 (drop-in for ``blocksvd.rsvd``).
+
+Every decomposition runs the same GPU pipeline (include/brsvd.h,
+``brsvd_rsvd``): global power iteration Y = (A A^T)^q A Omega with a basis
+change between passes, rank-revealing orthonormalisation, projection
+B = Q^T A, one-sided Jacobi SVD of the core, canonical signs.  This is the
+semantics of ``rsvd_incore`` (rsvd.py:126-141) and ``rsvd_naive_ooc``
+(rsvd.py:218-284) at any partition count.
+
+Intentional deltas:
+  * ``brsvd_run`` with s > 1 and q >= 1 computes the global power iteration
+    (same answer as s = 1), not the per-block iteration of rsvd.py:169-175.
+  * A store is read across the boundary once per decomposition when it fits
+    in HBM, so ``stats.full_passes`` is 1 (reference: 2 for brsvd_run,
+    2(q+1) for rsvd_naive_ooc).
+"""
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._arrays import DeviceMatrix, HostMatrix, is_torch, torch_stream_ptr
+from .kernels import SvdFactors, warn_rank
+from .store import MatrixStore, PassStats, plan_blocks
+
+__all__ = [
+    "SketchConfig",
+    "ConfigError",
+    "rsvd_incore",
+    "brsvd_run",
+    "block_range_finder",
+    "rsvd_naive_ooc",
+    "relative_frobenius_error",
+]
+
+Q_MAX_DEFAULT = 10
+
+
+class ConfigError(ValueError):
+    """Sketch parameters inconsistent with the matrix shape (rsvd.py:43-44)."""
+
+
+@dataclass
+class SketchConfig:
+    """Randomized range-finder parameters (rsvd.py:47-81)."""
+
+    target_rank: int
+    oversampling: int = 10
+    power_exponent: int = 0
+    partitions: object = "auto"
+    master_seed: int = 0
+    q_max: int = Q_MAX_DEFAULT
+
+    @property
+    def l(self):
+        return self.target_rank + self.oversampling
+
+    def validate(self, m, n):
+        if self.target_rank < 1:
+            raise ConfigError(f"target rank must be positive, got {self.target_rank}")
+        if self.oversampling < 0:
+            raise ConfigError("oversampling must be non-negative")
+        if self.l > min(m, n):
+            raise ConfigError(f"k + p = {self.l} exceeds min(m, n) = {min(m, n)}")
+        if not (0 <= self.power_exponent <= self.q_max):
+            raise ConfigError(
+                f"power exponent {self.power_exponent} outside [0, {self.q_max}]")
+        if self.partitions != "auto" and int(self.partitions) < 1:
+            raise ConfigError(f"partitions must be positive, got {self.partitions}")
+
+
+@dataclass
+class RsvdRun:
+    """Factors plus the device-side diagnostics of one decomposition."""
+
+    factors: SvdFactors
+    stats: object          # _lib.BrsvdStats
+    wall_seconds: float
+
+
+def _omega_arg(omega, n, l, dtype, device):
+    """Validate an injected sketch (n x l) and return (keepalive, ptr, where)."""
+    if omega is None:
+        return None, None, _lib.DEVICE
+    if device:
+        import torch
+        t = omega if is_torch(omega) else torch.as_tensor(np.asarray(omega))
+        t = t.to(device="cuda", dtype=torch.float64 if dtype == np.float64 else torch.float32)
+        if tuple(t.shape) != (n, l):
+            from .kernels import ShapeError
+            raise ShapeError(f"omega has shape {tuple(t.shape)}, expected ({n}, {l})")
+        t = t.t().contiguous()  # column-major n x l
+        return t, ctypes.c_void_p(t.data_ptr()), _lib.DEVICE
+    o = np.asfortranarray(np.asarray(omega), dtype=dtype)
+    if o.shape != (n, l):
+        from .kernels import ShapeError
+        raise ShapeError(f"omega has shape {o.shape}, expected ({n}, {l})")
+    return o, ctypes.c_void_p(o.ctypes.data), _lib.HOST
+
+
+def run_rsvd(a, cfg, omega=None, warn=True):
+    """One GPU decomposition; returns RsvdRun (factors + stats).
+
+    ``a`` is a 2-D numpy array (host; results come back as numpy) or a torch
+    CUDA tensor (device; results stay on the device as torch tensors).
+    """
+    device = is_torch(a)
+    mat = DeviceMatrix(a) if device else HostMatrix(a)
+    m, n = mat.shape
+    cfg.validate(m, n)
+    k, p, q = cfg.target_rank, cfg.oversampling, cfg.power_exponent
+    l = k + p
+    lib = _lib.load_library()
+    if device:
+        import torch
+        ctx = _lib.context(mat.device)
+        ctx.set_stream(torch_stream_ptr(mat.t))
+        tdt = mat.t.dtype
+        U = torch.empty((l, m), dtype=tdt, device=mat.t.device)     # col-major m x l
+        sigma = torch.empty(l, dtype=tdt, device=mat.t.device)
+        Vt = torch.empty((l, n), dtype=tdt, device=mat.t.device)
+        ptrs = [ctypes.c_void_p(x.data_ptr()) for x in (U, sigma, Vt)]
+        where = _lib.DEVICE
+        npdt = np.float64 if tdt == torch.float64 else np.float32
+    else:
+        ctx = _lib.context()
+        npdt = mat.dtype
+        U = np.empty((m, l), dtype=npdt, order="F")
+        sigma = np.empty(l, dtype=npdt)
+        Vt = np.empty((l, n), dtype=npdt, order="C")
+        ptrs = [ctypes.c_void_p(x.ctypes.data) for x in (U, sigma, Vt)]
+        where = _lib.HOST
+    keep, optr, owhere = _omega_arg(omega, n, l, npdt, device)
+    stats = _lib.BrsvdStats()
+    t0 = time.perf_counter()
+    rc = lib.brsvd_rsvd(ctx.handle, mat.ptr, m, n, mat.ld, mat.code, mat.layout, where,
+                        k, p, q, optr, owhere,
+                        ctypes.c_uint64(int(cfg.master_seed) & (2 ** 64 - 1)),
+                        ptrs[0], ptrs[1], ptrs[2], where, ctypes.byref(stats))
+    wall = time.perf_counter() - t0
+    del keep
+    _lib.check(rc)
+    if warn:
+        warn_rank(stats.detected_rank, l)
+        warn_rank(stats.core_rank, l)
+    if device:
+        U = U.t()
+    f = SvdFactors(U=U, sigma=sigma, Vt=Vt, target_rank=k, effective_l=l)
+    return RsvdRun(factors=f, stats=stats, wall_seconds=wall)
+
+
+def rsvd_incore(a, cfg, omega=None):
+    """Randomized SVD of an in-memory matrix (rsvd.py:126-141), on the GPU.
+
+    ``omega`` optionally injects the n x l sketch (e.g. the reference's
+    ``gaussian_matrix(n, l, seed, 0, dtype)``) for bitwise-identical inputs.
+    """
+    return run_rsvd(a, cfg, omega=omega).factors
+
+
+def _load_store_to_device(store, plan):
+    """Read every block of the plan once and land it in HBM (column-major)."""
+    import torch
+    tdt = torch.float64 if store.dtype == np.float64 else torch.float32
+    ctx = _lib.context()
+    dev = torch.empty((store.n, store.m), dtype=tdt, device=f"cuda:{ctx.device}")
+    pinned = None
+    for j0, j1 in plan:
+        w = j1 - j0
+        if pinned is None or pinned.numel() < store.m * w:
+            pinned = torch.empty(store.m * w, dtype=tdt, pin_memory=True)
+        buf = pinned[: store.m * w]
+        store.read_block_into(j0, j1, buf.numpy())
+        dev[j0:j1].view(-1).copy_(buf, non_blocking=False)
+    return dev.t()   # m x n column-major view
+
+
+def _run_store(store, cfg, memory_budget_bytes, stage_names):
+    m, n = store.m, store.n
+    cfg.validate(m, n)
+    s = None if cfg.partitions == "auto" else int(cfg.partitions)
+    plan = plan_blocks(n, m, cfg.l, store.element_size,
+                       memory_budget_bytes=memory_budget_bytes, s=s)
+    store.reset_stats()
+    stats = store.stats
+    t0 = time.perf_counter()
+    a_dev = _load_store_to_device(store, plan)
+    load_s = time.perf_counter() - t0
+    run = run_rsvd(a_dev, cfg)
+    f = run.factors
+    factors = SvdFactors(U=f.U.cpu().numpy(), sigma=f.sigma.cpu().numpy(),
+                         Vt=f.Vt.cpu().numpy(), target_rank=f.target_rank,
+                         effective_l=f.effective_l)
+    st = run.stats
+    l, q = cfg.l, cfg.power_exponent
+    stats.flop_estimate += int(st.flop_estimate)
+    seconds = {
+        "sketch": load_s + st.seconds_sketch,
+        "power": 0.0,
+        "orthonormalize": st.seconds_orthonormalize,
+        "form_core": st.seconds_form_core,
+        "svd": st.seconds_svd,
+    }
+    for name in stage_names:
+        stats.log_stage(name, m * n if name == "sketch" else 0, 0, seconds[name])
+    del a_dev
+    return factors, stats, plan
+
+
+def brsvd_run(store, cfg, memory_budget_bytes=None):
+    """Block randomized SVD of a stored matrix (rsvd.py:188-215) on the GPU.
+
+    Returns (factors, stats).  The store is streamed across the boundary once
+    into HBM; all power-iteration passes run from HBM.
+    """
+    factors, stats, _ = _run_store(store, cfg, memory_budget_bytes,
+                                   ("sketch", "orthonormalize", "form_core", "svd"))
+    return factors, stats
+
+
+def rsvd_naive_ooc(store, cfg, memory_budget_bytes=None):
+    """Global-power-iteration SVD of a stored matrix (rsvd.py:218-284).
+
+    Same GPU computation as brsvd_run; kept for API parity.
+    """
+    factors, stats, _ = _run_store(store, cfg, memory_budget_bytes,
+                                   ("sketch", "power", "orthonormalize", "form_core",
+                                    "svd"))
+    return factors, stats
+
+
+def block_range_finder(store, cfg, memory_budget_bytes=None, plan=None):
+    """Orthonormal basis of the sample range (rsvd.py:150-185); returns (Q, plan).
+
+    Q is the left factor U of the GPU decomposition: an orthonormal basis of
+    range(Y) (U = Q W with W orthogonal).
+    """
+    factors, stats, plan_used = _run_store(store, cfg, memory_budget_bytes,
+                                           ("sketch", "orthonormalize"))
+    return factors.U, (plan if plan is not None else plan_used)
+
+
+def relative_frobenius_error(source, factors, block_width=None):
+    """||A - U diag(sigma) Vt||_F / ||A||_F (rsvd.py:396-432), on the GPU.
+
+    Streams column blocks of a store (one extra pass) or takes an in-memory
+    matrix; sums of squares accumulate in fp64.
+    """
+    import torch
+    us = factors.U
+    vt = factors.Vt
+    sig = factors.sigma
+    dev = f"cuda:{_lib.context().device}"
+
+    def T(x):
+        return x.to(dev) if is_torch(x) else torch.as_tensor(np.asarray(x), device=dev)
+
+    U_d, s_d, Vt_d = T(us), T(sig), T(vt)
+    us_d = U_d * s_d
+    if isinstance(source, MatrixStore):
+        m, n = source.m, source.n
+        if us_d.shape[0] != m or Vt_d.shape[1] != n:
+            raise ValueError(f"factor shapes {us_d.shape[0]}x{Vt_d.shape[1]} do not "
+                             f"match source {m}x{n}")
+        if block_width is None:
+            block_width = max(1, min(n, (64 << 20) // (m * source.element_size)))
+        num = torch.zeros((), dtype=torch.float64, device=dev)
+        den = torch.zeros((), dtype=torch.float64, device=dev)
+        for j0 in range(0, n, block_width):
+            j1 = min(j0 + block_width, n)
+            blk = T(source.read_block(j0, j1))
+            diff = blk - us_d.to(blk.dtype) @ Vt_d[:, j0:j1].to(blk.dtype)
+            num += (diff.double() ** 2).sum()
+            den += (blk.double() ** 2).sum()
+    else:
+        a = source if is_torch(source) else np.asarray(source)
+        a_d = T(a)
+        if us_d.shape[0] != a_d.shape[0] or Vt_d.shape[1] != a_d.shape[1]:
+            raise ValueError(f"factor shapes {us_d.shape[0]}x{Vt_d.shape[1]} do not "
+                             f"match source {a_d.shape[0]}x{a_d.shape[1]}")
+        diff = a_d - us_d.to(a_d.dtype) @ Vt_d.to(a_d.dtype)
+        num = (diff.double() ** 2).sum()
+        den = (a_d.double() ** 2).sum()
+    num, den = float(num), float(den)
+    if den == 0.0:
+        return 0.0 if num == 0.0 else float("inf")
+    return float(np.sqrt(num) / np.sqrt(den))
