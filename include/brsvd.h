@@ -137,6 +137,29 @@ BRSVD_API int brsvd_gaussian(brsvd_ctx* ctx, void* out, int64_t rows, int64_t co
                    int64_t ld, int dtype, uint64_t seed, uint64_t stream,
                    int64_t row_offset);
 
+/* Largest singular value by power iteration on M^T M
+ * (spectral_norm_estimate, rpca.py:72-100): stops when the estimate changes
+ * by at most tol relative or after max_iterations; *out = 0 for a zero
+ * matrix.  M is m x n, dense, `layout`, in `where` memory. */
+BRSVD_API int brsvd_spectral_norm(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n,
+                                  int64_t ldm, int dtype, int layout, int where,
+                                  uint64_t seed, double tol, int max_iterations,
+                                  double* out, int32_t* iterations);
+
+/* Inexact-ALM robust PCA with the randomized SVD inside
+ * (ialm_rpca / _ialm_rpca_incore, rpca.py:153-213).  lam / mu0 = NaN select
+ * the defaults 1/sqrt(max(m, n)) and 1.25/||M||_2.  L and S (m x n, same
+ * layout as M) are written to out_where memory; residuals, mus,
+ * svd_seconds, iter_seconds (host arrays of max_iterations entries) receive
+ * the history.  Non-convergence is not an error (*converged = 0). */
+BRSVD_API int brsvd_ialm(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n,
+                         int64_t ldm, int dtype, int layout, int where, int k, int p,
+                         int q, uint64_t seed, double lam, double mu0, double rho,
+                         double tol, int max_iterations, void* L, void* S,
+                         int out_where, int32_t* iterations, int32_t* converged,
+                         double* residuals, double* mus, double* svd_seconds,
+                         double* iter_seconds);
+
 #ifdef __cplusplus
 }
 #endif

@@ -4,7 +4,10 @@
 #include <string>
 
 #include "../../include/brsvd.h"
+#include <chrono>
+
 #include "pipeline.cuh"
+#include "rpca.cuh"
 
 using namespace brsvd;
 
@@ -357,6 +360,78 @@ int brsvd_gaussian(brsvd_ctx* ctx, void* out, int64_t rows, int64_t cols, int64_
       throw Error(kErrArg, "bad dtype");
     BRSVD_CHECK_LAUNCH();
     BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+    return (int)kOk;
+  });
+}
+
+int brsvd_spectral_norm(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n, int64_t ldm,
+                        int dtype, int layout, int where, uint64_t seed, double tol,
+                        int max_iterations, double* out, int32_t* iterations) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && out != nullptr, kErrArg, "NULL argument");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    const size_t es = esize(dtype);
+    BRSVD_REQUIRE(m >= 1 && n >= 1, kErrShape, "matrix must be non-empty");
+    const bool row_major = layout == BRSVD_ROW_MAJOR;
+    const int64_t a_rows = row_major ? n : m, a_cols = row_major ? m : n;
+    InView mv(c, M, a_rows, a_cols, ldm, es, where);
+    const int64_t sm = row_major ? mv.ld : 1, sn = row_major ? 1 : mv.ld;
+    int it = 0;
+    double v;
+    if (dtype == BRSVD_F64)
+      v = spectral_norm<double>(c, (const double*)mv.dptr, m, n, sm, sn, seed, tol,
+                                max_iterations, &it);
+    else
+      v = spectral_norm<float>(c, (const float*)mv.dptr, m, n, sm, sn, seed, tol,
+                               max_iterations, &it);
+    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+    *out = v;
+    if (iterations) *iterations = it;
+    return (int)kOk;
+  });
+}
+
+int brsvd_ialm(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n, int64_t ldm,
+               int dtype, int layout, int where, int k, int p, int q, uint64_t seed,
+               double lam, double mu0, double rho, double tol, int max_iterations,
+               void* L, void* S, int out_where, int32_t* iterations,
+               int32_t* converged, double* residuals, double* mus, double* svd_seconds,
+               double* iter_seconds) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr, kErrArg, "ctx is NULL");
+    BRSVD_REQUIRE(residuals && mus && svd_seconds && iter_seconds, kErrArg,
+                  "history arrays are required");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    const size_t es = esize(dtype);
+    BRSVD_REQUIRE(m >= 1 && n >= 1, kErrShape, "matrix must be non-empty");
+    BRSVD_REQUIRE(k >= 1 && p >= 0 && k + p <= std::min(m, n), kErrConfig,
+                  "k + p exceeds min(m, n)");
+    BRSVD_REQUIRE(q >= 0, kErrConfig, "power exponent must be non-negative");
+    BRSVD_REQUIRE(rho > 1.0 && tol > 0.0 && max_iterations >= 1, kErrArg,
+                  "rho must exceed 1, tol and max_iterations must be positive");
+    const bool row_major = layout == BRSVD_ROW_MAJOR;
+    const int64_t a_rows = row_major ? n : m, a_cols = row_major ? m : n;
+    BRSVD_REQUIRE(ldm == a_rows, kErrShape, "M must be dense");
+    InView mv(c, M, a_rows, a_cols, ldm, es, where);
+    OutView lo(c, L, (size_t)m * n * es, out_where);
+    OutView so(c, S, (size_t)m * n * es, out_where);
+    IalmOut r;
+    if (dtype == BRSVD_F64)
+      r = ialm_device<double>(c, (const double*)mv.dptr, m, n, row_major, k, p, q, seed,
+                              lam, mu0, rho, tol, max_iterations, (double*)lo.dptr,
+                              (double*)so.dptr, residuals, mus, svd_seconds,
+                              iter_seconds);
+    else
+      r = ialm_device<float>(c, (const float*)mv.dptr, m, n, row_major, k, p, q, seed,
+                             lam, mu0, rho, tol, max_iterations, (float*)lo.dptr,
+                             (float*)so.dptr, residuals, mus, svd_seconds, iter_seconds);
+    lo.flush();
+    so.flush();
+    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+    if (iterations) *iterations = r.iterations;
+    if (converged) *converged = r.converged ? 1 : 0;
     return (int)kOk;
   });
 }

@@ -222,10 +222,12 @@ inline void jacobi_finish(Ctx& c, const double* G, int nrow, int ncol, int64_t l
 // trace (device, optional) receives ||X||_F^2.
 template <typename T>
 void gram_eig(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* E,
-              double* lam, double* s, bool scale = true, double* trace = nullptr) {
+              double* lam, double* s, bool scale = true, double* trace = nullptr,
+              double drop = 0.0) {
   DBuf<double> G(c, (size_t)l * l), V(c, (size_t)l * l);
   gemm_tn_cm<T, T, double>(c, l, l, r, X, ldx, X, ldx, G.p, l);
-  gram_prep_kernel<<<1, 1024, 0, c.stream>>>(G.p, l, s, V.p, scale ? 1 : 0, trace);
+  gram_prep_kernel<<<1, 1024, 0, c.stream>>>(G.p, l, s, V.p, scale ? 1 : 0, trace,
+                                             drop);
   BRSVD_CHECK_LAUNCH();
   jacobi(c, G.p, l, l, l, V.p, l);
   jacobi_finish(c, G.p, l, l, l, V.p, l, lam, nullptr, 0, E, l);
@@ -308,7 +310,8 @@ int orth_full(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* Q,
   DBuf<double> E(c, (size_t)l * l), lam(c, l), s(c, l), Tm(c, (size_t)l * l);
   DBuf<double> scal(c, 4);
   DBuf<int> drank(c, 1);
-  gram_eig<T>(c, X, r, l, ldx, E.p, lam.p, s.p, true, scal.p);
+  const double drop = 4.0 * l * eps_data;  // the reference's rank cut, kernels.py:155-157
+  gram_eig<T>(c, X, r, l, ldx, E.p, lam.p, s.p, true, scal.p, drop);
   build_basis_kernel<<<1, 1024, 0, c.stream>>>(E.p, lam.p, s.p, l, tau, 1, Tm.p,
                                                drank.p);
   BRSVD_CHECK_LAUNCH();
@@ -329,7 +332,7 @@ int orth_full(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* Q,
     DBuf<double> R(c, (size_t)r * l);
     copy2d_kernel<T, double><<<grid_for(r * l), 256, 0, c.stream>>>(X, r, l, ldx, R.p, r);
     BRSVD_CHECK_LAUNCH();
-    const double stop2 = std::pow(100.0 * l * eps_data, 2) * normx2;
+    const double stop2 = std::pow(drop, 2) * normx2;
     for (int level = 0; level < 4 && total < l; ++level) {
       project_out(c, Q, r, total, R.p, l);
       gram_eig<double>(c, R.p, r, l, r, E.p, lam.p, s.p, false, scal.p);

@@ -11,22 +11,41 @@ namespace brsvd {
 __global__ void gram_prep_kernel(double* __restrict__ G, int l,
                                  double* __restrict__ s,
                                  double* __restrict__ V, int scale,
-                                 double* __restrict__ trace) {
-  __shared__ double red[32];
-  double tr = 0.0;
+                                 double* __restrict__ trace, double drop) {
+  __shared__ double red[32], redm[32];
+  double tr = 0.0, dmax = 0.0;
   for (int j = threadIdx.x; j < l; j += blockDim.x) {
     const double d = G[j * (int64_t)l + j];
     tr += d;
-    s[j] = scale ? (d > 0.0 ? 1.0 / sqrt(d) : 0.0) : 1.0;
+    dmax = fmax(dmax, d);
   }
   tr = warp_sum(tr);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = tr;
-  __syncthreads();
-  if (threadIdx.x == 0 && trace != nullptr) {
-    double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    *trace = t;
+  dmax = warp_max(dmax);
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = tr;
+    redm[threadIdx.x >> 5] = dmax;
   }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0, mx = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      t += red[w];
+      mx = fmax(mx, redm[w]);
+    }
+    red[0] = t;
+    redm[0] = mx;
+    if (trace != nullptr) *trace = t;
+  }
+  __syncthreads();
+  // Columns negligible against the largest (||x_j|| <= drop * max ||x_i||)
+  // are left out of the scaled problem: their content is below the data's
+  // resolution, and the deflation level / completion of orth_full handles it.
+  const double floor2 = drop * drop * redm[0];
+  for (int j = threadIdx.x; j < l; j += blockDim.x) {
+    const double d = G[j * (int64_t)l + j];
+    s[j] = scale ? (d > floor2 && d > 0.0 ? 1.0 / sqrt(d) : 0.0) : 1.0;
+  }
+  __syncthreads();
   for (int idx = threadIdx.x; idx < l * l; idx += blockDim.x) {
     const int i = idx % l, j = idx / l;
     if (i > j) continue;

@@ -25,7 +25,7 @@ def test_header_declares_entry_points():
     syms = declared_symbols()
     for s in ("brsvd_rsvd", "brsvd_tsqr", "brsvd_small_svd", "brsvd_gaussian",
               "brsvd_ctx_create", "brsvd_last_error", "brsvd_ialm",
-              "brsvd_spectral_norm", "brsvd_rsvd_stream"):
+              "brsvd_spectral_norm"):
         assert s in syms, s
 
 
