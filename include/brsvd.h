@@ -151,10 +151,13 @@ BRSVD_API int brsvd_spectral_norm(brsvd_ctx* ctx, const void* M, int64_t m, int6
  * the defaults 1/sqrt(max(m, n)) and 1.25/||M||_2.  L and S (m x n, same
  * layout as M) are written to out_where memory; residuals, mus,
  * svd_seconds, iter_seconds (host arrays of max_iterations entries) receive
- * the history.  Non-convergence is not an error (*converged = 0). */
+ * the history.  Non-convergence is not an error (*converged = 0).  `omega`
+ * (optional, n x (k+p) column-major, `where` memory) injects the sketch the
+ * inner SVD uses every iteration (rpca.py:180-192: same seed each time). */
 BRSVD_API int brsvd_ialm(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n,
                          int64_t ldm, int dtype, int layout, int where, int k, int p,
-                         int q, uint64_t seed, double lam, double mu0, double rho,
+                         int q, uint64_t seed, const void* omega, double lam,
+                         double mu0, double rho,
                          double tol, int max_iterations, void* L, void* S,
                          int out_where, int32_t* iterations, int32_t* converged,
                          double* residuals, double* mus, double* svd_seconds,

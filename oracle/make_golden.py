@@ -119,7 +119,9 @@ def main():
         warnings.simplefilter("ignore")
         res = ref.ialm_rpca(M, ref.RpcaConfig(target_rank=10, tol=1e-7))
         n2 = ref.spectral_norm_estimate(M)
+    omega = ref.gaussian_matrix(200, 20, 0, stream_index=0)
     np.savez_compressed(os.path.join(OUT, "rpca_planted.npz"), M=M, L0=L0, mask=mask,
+                        omega=omega,
                         L=res.L, S=res.S, iterations=res.iterations,
                         residuals=np.array(res.residual_history),
                         mus=np.array([h["mu"] for h in res.history]),

@@ -88,7 +88,7 @@ def _declare(lib):
                                         dbl, c_int, ctypes.POINTER(dbl),
                                         ctypes.POINTER(i32)]
     lib.brsvd_ialm.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, c_int, c_int,
-                               c_int, u64, dbl, dbl, dbl, dbl, c_int, vp, vp, c_int,
+                               c_int, u64, vp, dbl, dbl, dbl, dbl, c_int, vp, vp, c_int,
                                ctypes.POINTER(i32), ctypes.POINTER(i32), vp, vp, vp, vp]
     lib.brsvd_profile_begin.argtypes = [vp]
     lib.brsvd_profile_end.argtypes = [vp, ctypes.POINTER(BrsvdProfile)]

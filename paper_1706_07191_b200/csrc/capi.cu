@@ -394,7 +394,8 @@ int brsvd_spectral_norm(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n, int
 
 int brsvd_ialm(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n, int64_t ldm,
                int dtype, int layout, int where, int k, int p, int q, uint64_t seed,
-               double lam, double mu0, double rho, double tol, int max_iterations,
+               const void* omega, double lam, double mu0, double rho, double tol,
+               int max_iterations,
                void* L, void* S, int out_where, int32_t* iterations,
                int32_t* converged, double* residuals, double* mus, double* svd_seconds,
                double* iter_seconds) {
@@ -415,17 +416,18 @@ int brsvd_ialm(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n, int64_t ldm,
     const int64_t a_rows = row_major ? n : m, a_cols = row_major ? m : n;
     BRSVD_REQUIRE(ldm == a_rows, kErrShape, "M must be dense");
     InView mv(c, M, a_rows, a_cols, ldm, es, where);
+    InView ov(c, omega, n, k + p, n, es, omega ? where : BRSVD_DEVICE);
     OutView lo(c, L, (size_t)m * n * es, out_where);
     OutView so(c, S, (size_t)m * n * es, out_where);
     IalmOut r;
     if (dtype == BRSVD_F64)
       r = ialm_device<double>(c, (const double*)mv.dptr, m, n, row_major, k, p, q, seed,
-                              lam, mu0, rho, tol, max_iterations, (double*)lo.dptr,
+                              (const double*)ov.dptr, lam, mu0, rho, tol, max_iterations, (double*)lo.dptr,
                               (double*)so.dptr, residuals, mus, svd_seconds,
                               iter_seconds);
     else
       r = ialm_device<float>(c, (const float*)mv.dptr, m, n, row_major, k, p, q, seed,
-                             lam, mu0, rho, tol, max_iterations, (float*)lo.dptr,
+                             (const float*)ov.dptr, lam, mu0, rho, tol, max_iterations, (float*)lo.dptr,
                              (float*)so.dptr, residuals, mus, svd_seconds, iter_seconds);
     lo.flush();
     so.flush();

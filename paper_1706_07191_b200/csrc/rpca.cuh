@@ -317,7 +317,8 @@ struct IalmOut {
 // have max_it entries.
 template <typename T>
 IalmOut ialm_device(Ctx& c, const T* Mx, int64_t m, int64_t n, bool row_major, int k,
-                    int p, int q, uint64_t seed, double lam, double mu0, double rho,
+                    int p, int q, uint64_t seed, const T* omega, double lam, double mu0,
+                    double rho,
                     double tol, int max_it, T* Lout, T* Sout, double* residuals,
                     double* mus, double* svd_s, double* iter_s) {
   const int l = k + p;
@@ -345,9 +346,14 @@ IalmOut ialm_device(Ctx& c, const T* Mx, int64_t m, int64_t n, bool row_major, i
       Mx, total, scale, mu, Y.p, S, W.p);
   BRSVD_CHECK_LAUNCH();
   DBuf<T> Om(c, (size_t)n * l), U(c, (size_t)m * l), V(c, (size_t)n * l), sig(c, l);
-  gaussian_kernel<T><<<grid_for(n * ((l + 1) / 2)), 256, 0, c.stream>>>(Om.p, n, l, n,
-                                                                         seed, 0, 0);
-  BRSVD_CHECK_LAUNCH();
+  if (omega != nullptr) {
+    BRSVD_CUDA(cudaMemcpyAsync(Om.p, omega, sizeof(T) * n * l, cudaMemcpyDeviceToDevice,
+                               c.stream));
+  } else {
+    gaussian_kernel<T><<<grid_for(n * ((l + 1) / 2)), 256, 0, c.stream>>>(Om.p, n, l, n,
+                                                                           seed, 0, 0);
+    BRSVD_CHECK_LAUNCH();
+  }
   const int64_t nf = row_major ? n : m, ns = row_major ? m : n;
   const T* F = row_major ? V.p : U.p;
   const T* G = row_major ? U.p : V.p;

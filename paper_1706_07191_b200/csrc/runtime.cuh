@@ -148,8 +148,18 @@ void gemm_nn_cm(Ctx& c, int64_t r, int64_t b, int64_t a, const TX* X, int64_t ld
 
 // ---------------------------------------------------------------------------
 // Jacobi SVD launcher: G (nrow x ncol, ldg) <- G V, V (ncol x ncol) accumulated.
+// tol: rotate a column pair while |x.y| > tol * ||x|| ||y||.  The dot products
+// carry ~sqrt(nrow) eps of rounding, so tol_tight() is the accuracy floor; the
+// Gram-based basis changes only need tol ~ 1e-8 (a Newton-Schulz step absorbs
+// the rest) and the power-iteration normalisation ~ 1e-4.
+inline double jacobi_tol_tight(int nrow) {
+  return 8.0 * std::sqrt((double)nrow) * 2.220446049250313e-16;
+}
+constexpr double kJacobiTolOrth = 1e-8;
+constexpr double kJacobiTolNormalize = 1e-4;
+
 inline int jacobi(Ctx& c, double* G, int nrow, int ncol, int64_t ldg, double* V,
-                  int64_t ldv, int max_sweeps = 60) {
+                  int64_t ldv, double tol, int max_sweeps = 40) {
   BRSVD_REQUIRE(ncol >= 1 && ncol <= 1024 && nrow >= 1, kErrShape,
                 "jacobi: unsupported small-problem shape");
   const size_t budget = std::min<size_t>(c.max_smem_optin, 200 * 1024);
@@ -187,7 +197,7 @@ inline int jacobi(Ctx& c, double* G, int nrow, int ncol, int64_t ldg, double* V,
   args.bw = bw;
   args.nb = nb;
   args.max_sweeps = max_sweeps;
-  args.tol = std::sqrt((double)nrow) * 2.220446049250313e-16;
+  args.tol = std::max(tol, jacobi_tol_tight(nrow));
   args.rot_count = counters.p;
   args.sweeps_done = counters.p + max_sweeps;
   if (single) {
@@ -222,14 +232,14 @@ inline void jacobi_finish(Ctx& c, const double* G, int nrow, int ncol, int64_t l
 // trace (device, optional) receives ||X||_F^2.
 template <typename T>
 void gram_eig(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* E,
-              double* lam, double* s, bool scale = true, double* trace = nullptr,
-              double drop = 0.0) {
+              double* lam, double* s, double tol, bool scale = true,
+              double* trace = nullptr, double drop = 0.0) {
   DBuf<double> G(c, (size_t)l * l), V(c, (size_t)l * l);
   gemm_tn_cm<T, T, double>(c, l, l, r, X, ldx, X, ldx, G.p, l);
   gram_prep_kernel<<<1, 1024, 0, c.stream>>>(G.p, l, s, V.p, scale ? 1 : 0, trace,
                                              drop);
   BRSVD_CHECK_LAUNCH();
-  jacobi(c, G.p, l, l, l, V.p, l);
+  jacobi(c, G.p, l, l, l, V.p, l, tol);
   jacobi_finish(c, G.p, l, l, l, V.p, l, lam, nullptr, 0, E, l);
 }
 
@@ -244,7 +254,7 @@ template <typename T>
 void normalize_sketch(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, T* Xout,
                       int64_t ldo) {
   DBuf<double> E(c, (size_t)l * l), lam(c, l), s(c, l), Tm(c, (size_t)l * l);
-  gram_eig<T>(c, X, r, l, ldx, E.p, lam.p, s.p);
+  gram_eig<T>(c, X, r, l, ldx, E.p, lam.p, s.p, kJacobiTolNormalize);
   build_basis_kernel<<<1, 1024, 0, c.stream>>>(E.p, lam.p, s.p, l, orth_tau(r, l),
                                                0, Tm.p, nullptr);
   BRSVD_CHECK_LAUNCH();
@@ -311,7 +321,7 @@ int orth_full(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* Q,
   DBuf<double> scal(c, 4);
   DBuf<int> drank(c, 1);
   const double drop = 4.0 * l * eps_data;  // the reference's rank cut, kernels.py:155-157
-  gram_eig<T>(c, X, r, l, ldx, E.p, lam.p, s.p, true, scal.p, drop);
+  gram_eig<T>(c, X, r, l, ldx, E.p, lam.p, s.p, kJacobiTolOrth, true, scal.p, drop);
   build_basis_kernel<<<1, 1024, 0, c.stream>>>(E.p, lam.p, s.p, l, tau, 1, Tm.p,
                                                drank.p);
   BRSVD_CHECK_LAUNCH();
@@ -335,7 +345,7 @@ int orth_full(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* Q,
     const double stop2 = std::pow(drop, 2) * normx2;
     for (int level = 0; level < 4 && total < l; ++level) {
       project_out(c, Q, r, total, R.p, l);
-      gram_eig<double>(c, R.p, r, l, r, E.p, lam.p, s.p, false, scal.p);
+      gram_eig<double>(c, R.p, r, l, r, E.p, lam.p, s.p, kJacobiTolOrth, false, scal.p);
       build_basis_kernel<<<1, 1024, 0, c.stream>>>(E.p, lam.p, s.p, l, tau, 1, Tm.p,
                                                    drank.p);
       BRSVD_CHECK_LAUNCH();
@@ -385,7 +395,7 @@ int small_svd_device(Ctx& c, const T* Bt, int64_t n, int l, int64_t ldb, double*
   gemm_tn_cm<T, double, double>(c, l, l, n, Bt, ldb, Qb.p, n, M.p, l);
   eye_kernel<<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(Vj.p, l);
   BRSVD_CHECK_LAUNCH();
-  jacobi(c, M.p, l, l, l, Vj.p, l);
+  jacobi(c, M.p, l, l, l, Vj.p, l, jacobi_tol_tight(l));
   jacobi_finish(c, M.p, l, l, l, Vj.p, l, sigma, W, l, Zj.p, l);
   gemm_nn_cm<double, double, T>(c, n, l, l, Qb.p, n, Zj.p, l, Vout, ldv);
   return rank;

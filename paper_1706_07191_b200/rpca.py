@@ -115,14 +115,16 @@ def spectral_norm_estimate(source, seed=0, tol=1e-10, max_iterations=100):
     return float(out.value)
 
 
-def ialm_rpca(m_input, cfg):
+def ialm_rpca(m_input, cfg, omega=None):
     """Inexact-ALM robust PCA with a randomized inner SVD (rpca.py:153-213).
 
     Non-convergence at max_iterations returns ``converged=False``.  numpy (or
     store) input gives numpy output; a torch CUDA tensor keeps everything on
     the device.  When the reference would take its out-of-core branch
     (store payload above ``memory_budget_bytes``, rpca.py:160-163) the split
-    is returned as MatrixStore objects as it does.
+    is returned as MatrixStore objects as it does.  ``omega`` optionally
+    injects the n x (k+p) sketch used by every inner SVD (parity runs pass the
+    reference's ``gaussian_matrix(n, k+p, seed, 0, dtype)``).
     """
     cfg.validate()
     as_stores = False
@@ -161,11 +163,25 @@ def ialm_rpca(m_input, cfg):
     iters = ctypes.c_int32()
     conv = ctypes.c_int32()
     nan = float("nan")
+    l = int(cfg.target_rank) + int(cfg.oversampling)
+    if omega is not None:
+        if device:
+            import torch
+            om = torch.as_tensor(np.asarray(omega) if not is_torch(omega) else omega)
+            om = om.to(device=mat.t.device, dtype=mat.t.dtype).t().contiguous()
+            optr = ctypes.c_void_p(om.data_ptr())
+        else:
+            om = np.asfortranarray(np.asarray(omega), dtype=mat.dtype)
+            optr = ctypes.c_void_p(om.ctypes.data)
+        if tuple(np.shape(omega)) != (n, l):
+            raise ValueError(f"omega has shape {np.shape(omega)}, expected ({n}, {l})")
+    else:
+        om, optr = None, None
     dptr = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
     _lib.check(fn(
         ctx.handle, mat.ptr, m, n, mat.ld, mat.code, mat.layout, where,
         int(cfg.target_rank), int(cfg.oversampling), int(cfg.power_exponent),
-        ctypes.c_uint64(int(cfg.master_seed) & (2 ** 64 - 1)),
+        ctypes.c_uint64(int(cfg.master_seed) & (2 ** 64 - 1)), optr,
         ctypes.c_double(nan if cfg.lam is None else float(cfg.lam)),
         ctypes.c_double(nan if cfg.mu0 is None else float(cfg.mu0)),
         ctypes.c_double(float(cfg.rho)), ctypes.c_double(float(cfg.tol)), maxit,

@@ -169,7 +169,7 @@ def test_overflow_guard_raises():
     with pytest.raises(FloatingPointError):
         bad = np.ones((20, 10))
         bad[3, 4] = np.inf
-        rsvd_incore(bad, SketchConfig(target_rank=2))
+        rsvd_incore(bad, SketchConfig(target_rank=2, oversampling=2))
 
 
 def test_config_errors_before_device_work():

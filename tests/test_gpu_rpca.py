@@ -25,11 +25,13 @@ def planted(m=200, n=200, rank=5, density=0.05, seed=0):
 def test_planted_matches_reference_golden():
     from paper_1706_07191_b200 import RpcaConfig, ialm_rpca
     g = np.load(os.path.join(GOLDEN, "rpca_planted.npz"))
-    res = ialm_rpca(g["M"], RpcaConfig(target_rank=10, tol=1e-7))
+    res = ialm_rpca(g["M"], RpcaConfig(target_rank=10, tol=1e-7), omega=g["omega"])
     assert res.converged
     assert abs(res.iterations - int(g["iterations"])) <= 1
     k = min(res.iterations, int(g["iterations"])) - 1
-    np.testing.assert_allclose(res.residual_history[:k], g["residuals"][:k], rtol=1e-3)
+    # same sketch as the reference: same trajectory (the spectral-norm start
+    # vector differs, which moves mu0 by ~1e-10 relative)
+    np.testing.assert_allclose(res.residual_history[:k], g["residuals"][:k], rtol=1e-4)
     np.testing.assert_allclose([h["mu"] for h in res.history][:k], g["mus"][:k],
                                rtol=1e-9)
     rel = np.linalg.norm(res.L - g["L"]) / np.linalg.norm(g["L"])
