@@ -116,6 +116,17 @@ BRSVD_API int brsvd_rsvd(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, in
                const void* omega, int omega_where, uint64_t seed, void* U,
                void* sigma, void* Vt, int out_where, brsvd_stats* stats);
 
+/* One pass over A -- the A-streaming product of the power iteration and of
+ * the core projection (a @ omega, a.T @ y: rsvd.py:94-102, :140):
+ *   trans = 0:  C (m x l) = A X,    X (n x l)
+ *   trans = 1:  C (n x l) = A^T X,  X (m x l)
+ * Device pointers; X and C column-major (ldx, ldc).  fp32 runs on the
+ * tcgen05 3xTF32 kernel, fp64 on the fp64 SIMT kernel. */
+BRSVD_API int brsvd_sketch_product(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n,
+                                   int64_t lda, int dtype, int layout, int trans,
+                                   const void* X, int64_t ldx, int64_t l, void* C,
+                                   int64_t ldc);
+
 /* Orthonormal basis of range(Y) (tsqr_factor, kernels.py:139-164).
  *   Y m x l column-major (ldy); Q m x l column-major; R (optional) l x l
  *   column-major with Y = Q R.  *detected_rank receives the numerical rank. */

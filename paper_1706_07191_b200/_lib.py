@@ -24,7 +24,7 @@ EXPORTED = (
     "brsvd_version", "brsvd_last_error", "brsvd_ctx_create", "brsvd_ctx_set_stream",
     "brsvd_ctx_destroy", "brsvd_rsvd", "brsvd_tsqr", "brsvd_small_svd",
     "brsvd_gaussian", "brsvd_profile_begin", "brsvd_profile_end",
-    "brsvd_spectral_norm", "brsvd_ialm",
+    "brsvd_spectral_norm", "brsvd_ialm", "brsvd_sketch_product",
 )
 
 
@@ -90,6 +90,8 @@ def _declare(lib):
     lib.brsvd_ialm.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, c_int, c_int,
                                c_int, u64, vp, dbl, dbl, dbl, dbl, c_int, vp, vp, c_int,
                                ctypes.POINTER(i32), ctypes.POINTER(i32), vp, vp, vp, vp]
+    lib.brsvd_sketch_product.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, vp,
+                                         i64, i64, vp, i64]
     lib.brsvd_profile_begin.argtypes = [vp]
     lib.brsvd_profile_end.argtypes = [vp, ctypes.POINTER(BrsvdProfile)]
     for name in EXPORTED:

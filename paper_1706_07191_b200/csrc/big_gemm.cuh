@@ -14,7 +14,7 @@ template <typename T>
 void big_nn(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool row_major,
             const T* X, int64_t ldx, int l, T* Y, int64_t ldy) {
   ProfScope ps(c, 2.0 * m * n * l, (double)m * n * sizeof(T));
-  if (tc_gemm_supported<T>(c, row_major, m, n, l, /*trans=*/false)) {
+  if (tc_gemm_supported<T>(c, A, lda, m, n, l)) {
     tc_gemm_launch<T>(c, A, m, n, lda, row_major, /*trans=*/false, X, ldx, l, Y, ldy);
     return;
   }
@@ -26,7 +26,7 @@ template <typename T>
 void big_tn(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool row_major,
             const T* Yin, int64_t ldy, int l, T* Z, int64_t ldz) {
   ProfScope ps(c, 2.0 * m * n * l, (double)m * n * sizeof(T));
-  if (tc_gemm_supported<T>(c, row_major, m, n, l, /*trans=*/true)) {
+  if (tc_gemm_supported<T>(c, A, lda, m, n, l)) {
     tc_gemm_launch<T>(c, A, m, n, lda, row_major, /*trans=*/true, Yin, ldy, l, Z, ldz);
     return;
   }

@@ -121,6 +121,8 @@ int brsvd_ctx_create(int device, void* stream, brsvd_ctx** out) {
     BRSVD_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin,
                                       device));
     h->c.num_sms = sms;
+    BRSVD_CUDA(cudaDeviceGetAttribute(&h->c.cc_major, cudaDevAttrComputeCapabilityMajor, device));
+    BRSVD_CUDA(cudaDeviceGetAttribute(&h->c.cc_minor, cudaDevAttrComputeCapabilityMinor, device));
     h->c.max_smem_optin = (size_t)optin;
     cudaMemPool_t pool;
     BRSVD_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -253,6 +255,36 @@ int brsvd_rsvd(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda,
                   "sample matrix magnitude exceeds the overflow guard; lower the "
                   "power exponent or rescale the input");
     }
+    return (int)kOk;
+  });
+}
+
+int brsvd_sketch_product(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda,
+                         int dtype, int layout, int trans, const void* X, int64_t ldx,
+                         int64_t l, void* C, int64_t ldc) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr, kErrArg, "ctx is NULL");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    esize(dtype);
+    BRSVD_REQUIRE(m >= 1 && n >= 1 && l >= 1 && l <= 1024, kErrShape, "bad shape");
+    const bool row_major = layout == BRSVD_ROW_MAJOR;
+    if (dtype == BRSVD_F64) {
+      if (trans)
+        big_tn<double>(c, (const double*)A, m, n, lda, row_major, (const double*)X, ldx,
+                       (int)l, (double*)C, ldc);
+      else
+        big_nn<double>(c, (const double*)A, m, n, lda, row_major, (const double*)X, ldx,
+                       (int)l, (double*)C, ldc);
+    } else {
+      if (trans)
+        big_tn<float>(c, (const float*)A, m, n, lda, row_major, (const float*)X, ldx,
+                      (int)l, (float*)C, ldc);
+      else
+        big_nn<float>(c, (const float*)A, m, n, lda, row_major, (const float*)X, ldx,
+                      (int)l, (float*)C, ldc);
+    }
+    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
     return (int)kOk;
   });
 }

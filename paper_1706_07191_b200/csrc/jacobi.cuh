@@ -184,7 +184,9 @@ __global__ void jacobi_finish_kernel(const double* __restrict__ G, int64_t ldg,
       s = fma(v, v, s);
     }
     s = warp_sum(s);
-    if (lane == 0) nrm[c] = sqrt(s);
+    // NaN (non-finite input) sorts last: the key order must be total so the
+    // ranks form a permutation.
+    if (lane == 0) nrm[c] = (s == s) ? sqrt(s) : -1.0;
   }
   __syncthreads();
   for (int c = threadIdx.x; c < ncol; c += blockDim.x) {

@@ -64,6 +64,11 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
   const MaxAbs p0 = maxabs<T>(c, Y.p, m, l, m);
   info.max_abs_y0 = p0.peak;
   bool nonfinite = p0.nonfinite;
+  if (nonfinite) {  // the reference's guard fires on the first sample already
+    info.overflow = true;
+    info.log10_peak = INFINITY;
+    return info;
+  }
   for (int it = 0; it < q; ++it) {
     big_tn<T>(c, A, m, n, lda, row_major, Y.p, m, l, Z.p, n);
     normalize_sketch<T>(c, Z.p, n, l, n, Zn.p, n);
@@ -73,7 +78,11 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
   info.block_reads += 2 * q + 1;
   if (q > 0) {
     const MaxAbs pq = maxabs<T>(c, Y.p, m, l, m);
-    nonfinite = nonfinite || pq.nonfinite;
+    if (pq.nonfinite) {
+      info.overflow = true;
+      info.log10_peak = INFINITY;
+      return info;
+    }
   }
   ev.rec(1, c.stream);
   Zn.release();

@@ -27,6 +27,7 @@ struct Ctx {
   bool own_stream = false;
   unsigned long long* h_pinned = nullptr;  // small pinned readback area
   int num_sms = kNumSMs;
+  int cc_major = 0, cc_minor = 0;
   size_t max_smem_optin = 0;
   // profiling of the big A-streaming products (brsvd_profile_begin/end)
   bool prof = false;

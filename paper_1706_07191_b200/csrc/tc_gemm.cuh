@@ -1,17 +1,449 @@
-// tcgen05 (5th-gen tensor core) path for the big tall-skinny products.
-// Placeholder until the 3xTF32 kernel lands: the SIMT path handles every case.
+// 5th-generation tensor-core (tcgen05) path for the A-streaming products of
+// the fp32 pipeline (big_nn / big_tn):   C (M x N) = opA (M x K) * B (K x N)
+// with opA the big matrix (A or A^T, K-major or MN-major in memory) and B the
+// tall-skinny sketch (column-major, N = l <= 320).
+//
+// Precision: 3xTF32 split.  a = a_hi + a_lo, b = b_hi + b_lo with tf32 hi
+// parts (cvt.rna) and fp32 remainders; C += a_lo b_hi + a_hi b_lo + a_hi b_hi
+// in the fp32 TMEM accumulator -- fp32-level products, the sgemm the
+// reference calls (rsvd.py:99-101, :140) to within accumulation order.
+//
+// Data flow per CTA (one 128-row tile of C, all N columns):
+//   warp 0   TMA producer: A tile (128 x 16 fp32) + B_hi/B_lo tiles
+//            (N x 16 each, K-major, 64B swizzle) into a 4-stage smem ring;
+//   warps4-7 converters: A tile smem -> registers -> (hi, lo) -> tcgen05.st
+//            into a TMEM staging slot (one TMEM lane per row of the tile);
+//   warp 1   MMA issuer: tcgen05.mma.kind::tf32 with A from TMEM (.ts form)
+//            and B from shared memory, N split in <=256 chunks, accumulator
+//            N fp32 columns of TMEM; tcgen05.commit frees the stage;
+//   warps4-7 epilogue: tcgen05.ld the accumulator, coalesced column-major
+//            stores of C.
+// Putting A in TMEM keeps the tensor core's shared-memory reads to the B
+// operand only; B_hi/B_lo are split once per product (tc_split_kernel) and
+// stay L2-resident across the M tiles.
 #pragma once
+#include <cuda.h>
+
+#include <cstdlib>
+
 #include "runtime.cuh"
 
 namespace brsvd {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 16;              // fp32 K elements per stage (64-byte rows)
+constexpr int STAGES = 4;
+constexpr int NPAD_MAX = 320;
+constexpr int kThreads = 256;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kASlot = 384;    // TMEM columns [384, 512): A staging slots
+constexpr uint32_t A_STAGE_BYTES = BM * BK * 4;
+
+struct Params {
+  int64_t M, K;
+  int npad, nchunks, rows_c, n_out;
+  float* C;
+  int64_t ldc;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tc_before_sync() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_after_sync() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// K-major operand, 64-byte swizzle: 8-row groups 512 B apart (SBO), version 1.
+__device__ __forceinline__ uint64_t desc_kmajor_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;            // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(512 >> 4) << 32;   // SBO
+  d |= (uint64_t)1 << 46;            // descriptor version (sm100)
+  d |= (uint64_t)4 << 61;            // SWIZZLE_64B
+  return d;
+}
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  return h;
+}
+
+template <bool A_KMAJOR>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc3_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
+                    const __grid_constant__ CUtensorMap mapBhi,
+                    const __grid_constant__ CUtensorMap mapBlo, const Params p) {
+  extern __shared__ uint8_t smem_dyn[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_dyn + 1023) & ~(uintptr_t)1023);
+  const uint32_t b_bytes = (uint32_t)p.npad * BK * 4;  // one of hi / lo
+  const uint32_t stage_bytes = A_STAGE_BYTES + 2 * b_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * stage_bytes);
+  uint64_t* freeb = full + STAGES;
+  uint64_t* tfull = freeb + STAGES;
+  uint64_t* accfull = tfull + STAGES;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int nk = (int)((p.K + BK - 1) / BK);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&freeb[s], 1);
+      mbar_init(&tfull[s], 4);
+    }
+    mbar_init(accfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapBhi) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapBlo) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (kb / STAGES) & 1;
+        mbar_wait(&freeb[s], ph ^ 1);
+        uint8_t* st = smem + (size_t)s * stage_bytes;
+        mbar_expect_tx(&full[s], stage_bytes);
+        const int k0 = kb * BK;
+        if (A_KMAJOR) {
+          tma_load_2d(st, &mapA, &full[s], k0, (int)m0);
+        } else {
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            tma_load_2d(st + b * (32 * BK * 4), &mapA, &full[s], (int)m0 + 32 * b, k0);
+        }
+        uint8_t* bh = st + A_STAGE_BYTES;
+        uint8_t* bl = bh + b_bytes;
+        for (int ch = 0; ch < p.nchunks; ++ch) {
+          tma_load_2d(bh + ch * p.rows_c * (BK * 4), &mapBhi, &full[s], k0, ch * p.rows_c);
+          tma_load_2d(bl + ch * p.rows_c * (BK * 4), &mapBlo, &full[s], k0, ch * p.rows_c);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
+                             ((uint32_t)(p.rows_c >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (kb / STAGES) & 1;
+        mbar_wait(&tfull[s], ph);
+        mbar_wait(&full[s], ph);
+        tc_after_sync();
+        const uint32_t bh = smem_u32(smem + (size_t)s * stage_bytes + A_STAGE_BYTES);
+        const uint32_t bl = bh + b_bytes;
+        const uint32_t a_hi = tmem + kASlot + s * 32, a_lo = a_hi + 16;
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          for (int ch = 0; ch < p.nchunks; ++ch) {
+            const uint32_t boff = ch * p.rows_c * (BK * 4) + kk * 32;
+            const uint64_t dh = desc_kmajor_sw64(bh + boff);
+            const uint64_t dl = desc_kmajor_sw64(bl + boff);
+            const uint32_t d = tmem + ch * p.rows_c;
+            const uint32_t first = (kb | kk) ? 1u : 0u;
+            mma_tf32_ts(d, a_lo + kk * 8, dh, idesc, first);
+            mma_tf32_ts(d, a_hi + kk * 8, dl, idesc, 1u);
+            mma_tf32_ts(d, a_hi + kk * 8, dh, idesc, 1u);
+          }
+        }
+        mma_commit(&freeb[s]);
+      }
+      mma_commit(accfull);
+    }
+  } else if (warp >= 4) {  // ---------------- converters, then epilogue
+    const int wq = warp - 4;
+    const int r = wq * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (kb / STAGES) & 1;
+      mbar_wait(&full[s], ph);
+      const uint8_t* sa = smem + (size_t)s * stage_bytes;
+      float v[16];
+      if (A_KMAJOR) {
+        // 64-byte rows; TMA 64B swizzle puts 16B chunk j of row r at j^((r>>1)&3)
+        const uint8_t* row = sa + r * 64;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 x =
+              *reinterpret_cast<const float4*>(row + ((j ^ ((r >> 1) & 3)) << 4));
+          v[4 * j + 0] = x.x;
+          v[4 * j + 1] = x.y;
+          v[4 * j + 2] = x.z;
+          v[4 * j + 3] = x.w;
+        }
+      } else {
+        // four (32 rows x 16 k) boxes, 32 consecutive rows per k
+        const float* box = reinterpret_cast<const float*>(sa + wq * (32 * BK * 4));
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = box[k * 32 + lane];
+      }
+      uint32_t hi[16], lo[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const uint32_t h = tf32_rna(v[i]);
+        hi[i] = h;
+        lo[i] = __float_as_uint(v[i] - __uint_as_float(h));
+      }
+      tmem_st16(tmem + lane_base + kASlot + s * 32, hi);
+      tmem_st16(tmem + lane_base + kASlot + s * 32 + 16, lo);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tfull[s]);
+    }
+    mbar_wait(accfull, 0);
+    tc_after_sync();
+    const int64_t row = m0 + r;
+    for (int j0 = 0; j0 < p.npad; j0 += 16) {
+      uint32_t acc[16];
+      tmem_ld16(tmem + lane_base + j0, acc);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < p.M) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int j = j0 + i;
+          if (j < p.n_out) p.C[row + (int64_t)j * p.ldc] = __uint_as_float(acc[i]);
+        }
+      }
+    }
+  }
+  tc_before_sync();
+  __syncthreads();
+  if (warp == 2) {
+    tc_after_sync();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kTmemCols)
+                 : "memory");
+  }
+}
+
+// B (K x n_src, column-major, ld ldx) -> hi, lo ([npad][kld] row-major, zero
+// padded): the tf32 split of the sketch, done once per product.
+__global__ void tc_split_kernel(const float* __restrict__ X, int64_t K, int n_src,
+                                int64_t ldx, int npad, int64_t kld,
+                                float* __restrict__ hi, float* __restrict__ lo) {
+  const int64_t total = (int64_t)npad * kld;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = idx % kld, j = idx / kld;
+    const float x = (j < n_src && k < K) ? X[k + j * ldx] : 0.f;
+    const uint32_t h = tf32_rna(x);
+    hi[idx] = __uint_as_float(h);
+    lo[idx] = x - __uint_as_float(h);
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+
+inline EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    BRSVD_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q));
+    BRSVD_REQUIRE(ptr != nullptr && q == cudaDriverEntryPointSuccess, kErrCuda,
+                  "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// 2-D fp32 tensor map: inner dimension `inner` (contiguous), `outer` rows of
+// `row_bytes` stride; box (box_inner x box_outer).
+inline CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer,
+                            uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+                            CUtensorMapSwizzle swz) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {row_bytes};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base),
+                                 dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  BRSVD_REQUIRE(r == CUDA_SUCCESS, kErrCuda, "cuTensorMapEncodeTiled failed");
+  return m;
+}
+
+struct Geometry {
+  int npad, nchunks, rows_c;
+};
+
+inline Geometry geometry(int l) {
+  Geometry g;
+  g.nchunks = (int)ceil_div(l, 256);
+  g.rows_c = (int)ceil_div(ceil_div(l, g.nchunks), 16) * 16;
+  g.npad = g.rows_c * g.nchunks;
+  return g;
+}
+
+inline size_t smem_bytes(int npad) {
+  return (size_t)STAGES * (A_STAGE_BYTES + 2u * (uint32_t)npad * BK * 4) + 128 + 1024;
+}
+
+inline bool env_enabled() {
+  const char* e = std::getenv("BRSVD_TC");
+  return !(e && e[0] == '0');
+}
+
+}  // namespace tc
 
 template <typename T>
-bool tc_gemm_supported(Ctx&, bool, int64_t, int64_t, int, bool) {
-  return false;
+bool tc_gemm_supported(Ctx& c, const T* A, int64_t lda, int64_t m, int64_t n, int l) {
+  if (sizeof(T) != 4 || !tc::env_enabled() || c.cc_major != 10) return false;
+  // TMA: 16-byte aligned base and row stride
+  if ((reinterpret_cast<uintptr_t>(A) & 15) != 0 || (lda * (int64_t)sizeof(T)) % 16 != 0)
+    return false;
+  const tc::Geometry g = tc::geometry(l);
+  if (g.npad > tc::NPAD_MAX) return false;
+  if (tc::smem_bytes(g.npad) > c.max_smem_optin) return false;
+  return m >= 1 && n >= 1;
 }
 
 template <typename T>
-void tc_gemm_launch(Ctx&, const T*, int64_t, int64_t, int64_t, bool, bool, const T*,
-                    int64_t, int, T*, int64_t) {}
+void tc_gemm_launch(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool row_major,
+                    bool trans, const T* X, int64_t ldx, int l, T* C, int64_t ldc);
+
+template <>
+inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, int64_t lda,
+                                  bool row_major, bool trans, const float* X, int64_t ldx,
+                                  int l, float* C, int64_t ldc) {
+  using namespace tc;
+  const int64_t M = trans ? n : m, K = trans ? m : n;
+  const bool kmajor = row_major != trans;
+  const Geometry g = geometry(l);
+  const int64_t kld = ceil_div(K, 4) * 4;
+  DBuf<float> hi(c, (size_t)g.npad * kld), lo(c, (size_t)g.npad * kld);
+  tc_split_kernel<<<grid_for((int64_t)g.npad * kld), 256, 0, c.stream>>>(
+      X, K, l, ldx, g.npad, kld, hi.p, lo.p);
+  BRSVD_CHECK_LAUNCH();
+  // A as stored: row-major (m x n) has n contiguous; column-major has m contiguous.
+  const uint64_t inner = row_major ? (uint64_t)n : (uint64_t)m;
+  const uint64_t outer = row_major ? (uint64_t)m : (uint64_t)n;
+  const CUtensorMap mapA =
+      kmajor ? make_map(A, inner, outer, (uint64_t)lda * 4, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B)
+             : make_map(A, inner, outer, (uint64_t)lda * 4, 32, BK, CU_TENSOR_MAP_SWIZZLE_NONE);
+  const CUtensorMap mapBhi = make_map(hi.p, (uint64_t)kld, (uint64_t)g.npad, (uint64_t)kld * 4,
+                                      BK, (uint32_t)g.rows_c, CU_TENSOR_MAP_SWIZZLE_64B);
+  const CUtensorMap mapBlo = make_map(lo.p, (uint64_t)kld, (uint64_t)g.npad, (uint64_t)kld * 4,
+                                      BK, (uint32_t)g.rows_c, CU_TENSOR_MAP_SWIZZLE_64B);
+  Params p;
+  p.M = M;
+  p.K = K;
+  p.npad = g.npad;
+  p.nchunks = g.nchunks;
+  p.rows_c = g.rows_c;
+  p.n_out = l;
+  p.C = C;
+  p.ldc = ldc;
+  const size_t smem = smem_bytes(g.npad);
+  const dim3 grid((unsigned)ceil_div(M, BM));
+  if (kmajor) {
+    BRSVD_CUDA(cudaFuncSetAttribute(tc3_gemm_kernel<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    tc3_gemm_kernel<true><<<grid, kThreads, smem, c.stream>>>(mapA, mapBhi, mapBlo, p);
+  } else {
+    BRSVD_CUDA(cudaFuncSetAttribute(tc3_gemm_kernel<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    tc3_gemm_kernel<false><<<grid, kThreads, smem, c.stream>>>(mapA, mapBhi, mapBlo, p);
+  }
+  BRSVD_CHECK_LAUNCH();
+}
+
+template <>
+inline void tc_gemm_launch<double>(Ctx&, const double*, int64_t, int64_t, int64_t, bool, bool,
+                                   const double*, int64_t, int, double*, int64_t) {
+  throw Error(kErrArg, "tcgen05 path is fp32-only");
+}
 
 }  // namespace brsvd

@@ -288,3 +288,29 @@ def relative_frobenius_error(source, factors, block_width=None):
     if den == 0.0:
         return 0.0 if num == 0.0 else float("inf")
     return float(np.sqrt(num) / np.sqrt(den))
+
+
+def sketch_product(A, X, trans=False):
+    """One A-streaming product on the GPU: A @ X (trans=False) or A.T @ X.
+
+    ``A`` (m x n) and ``X`` are torch CUDA tensors; returns a new tensor
+    (column-major storage).  This is the unit each power-iteration pass is made
+    of (rsvd.py:94-102); exposed for the sharded driver and for tests.
+    """
+    import torch
+    mat = DeviceMatrix(A)
+    m, n = mat.shape
+    rows = n if trans else m
+    xin = m if trans else n
+    if X.dim() != 2 or X.shape[0] != xin:
+        from .kernels import ShapeError
+        raise ShapeError(f"X has shape {tuple(X.shape)}, expected ({xin}, l)")
+    l = X.shape[1]
+    Xc = X.to(dtype=mat.t.dtype).t().contiguous()          # column-major
+    C = torch.empty((l, rows), dtype=mat.t.dtype, device=mat.t.device)
+    ctx = _lib.context(mat.device)
+    ctx.set_stream(torch_stream_ptr(mat.t))
+    _lib.check(_lib.load_library().brsvd_sketch_product(
+        ctx.handle, mat.ptr, m, n, mat.ld, mat.code, mat.layout, int(bool(trans)),
+        ctypes.c_void_p(Xc.data_ptr()), xin, l, ctypes.c_void_p(C.data_ptr()), rows))
+    return C.t()
