@@ -33,11 +33,11 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 16;              // fp32 K elements per stage (64-byte rows)
-constexpr int STAGES = 4;
-constexpr int NPAD_MAX = 320;
+constexpr int STAGES = 6;
+constexpr int NPAD_MAX = 320;   // l <= 320: two CTAs of <= 160 columns
 constexpr int kThreads = 256;
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kASlot = 384;    // TMEM columns [384, 512): A staging slots
+constexpr uint32_t kASlot = 320;    // TMEM columns [320, 512): six A staging slots
 constexpr uint32_t A_STAGE_BYTES = BM * BK * 4;
 
 struct Params {
@@ -137,24 +137,37 @@ __device__ __forceinline__ uint32_t tf32_rna(float x) {
   return h;
 }
 
-template <bool A_KMAJOR>
+// Tensor-core accumulation truncates (round-toward-zero) on every MMA add
+// into TMEM, a bias of ~0.4 ulp per add that grows linearly with K
+// (scripts/exp_tc_bias.py: -2.3e-6 at K=256, -1.7e-4 at K=16384).  The
+// accumulator is therefore double-buffered and flushed every kChunkKB
+// k-blocks (128 k values = 48 MMA adds, bias ~1e-6) into round-to-nearest
+// fp32 running sums held in the converter warps' registers.
+constexpr int kChunkKB = 8;
+
+template <bool A_KMAJOR, int NCMAX>
 __global__ void __launch_bounds__(kThreads, 1)
     tc3_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
                     const __grid_constant__ CUtensorMap mapBhi,
                     const __grid_constant__ CUtensorMap mapBlo, const Params p) {
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_dyn + 1023) & ~(uintptr_t)1023);
-  const uint32_t b_bytes = (uint32_t)p.npad * BK * 4;  // one of hi / lo
+  const int nc = p.rows_c;                               // columns of this CTA
+  const uint32_t b_bytes = (uint32_t)nc * BK * 4;        // one of hi / lo
   const uint32_t stage_bytes = A_STAGE_BYTES + 2 * b_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * stage_bytes);
   uint64_t* freeb = full + STAGES;
   uint64_t* tfull = freeb + STAGES;
-  uint64_t* accfull = tfull + STAGES;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accfull + 1);
+  uint64_t* accready = tfull + STAGES;                   // [2]
+  uint64_t* accfree = accready + 2;                      // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accfree + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int64_t m0 = (int64_t)(blockIdx.x / p.nchunks) * BM;
+  const int nhalf = blockIdx.x % p.nchunks;
+  const int n0 = nhalf * nc;
   const int nk = (int)((p.K + BK - 1) / BK);
+  const int nchunk = (nk + kChunkKB - 1) / kChunkKB;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -162,7 +175,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&freeb[s], 1);
       mbar_init(&tfull[s], 4);
     }
-    mbar_init(accfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accready[b], 1);
+      mbar_init(&accfree[b], 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapBhi) : "memory");
@@ -196,48 +212,66 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int b = 0; b < 4; ++b)
             tma_load_2d(st + b * (32 * BK * 4), &mapA, &full[s], (int)m0 + 32 * b, k0);
         }
-        uint8_t* bh = st + A_STAGE_BYTES;
-        uint8_t* bl = bh + b_bytes;
-        for (int ch = 0; ch < p.nchunks; ++ch) {
-          tma_load_2d(bh + ch * p.rows_c * (BK * 4), &mapBhi, &full[s], k0, ch * p.rows_c);
-          tma_load_2d(bl + ch * p.rows_c * (BK * 4), &mapBlo, &full[s], k0, ch * p.rows_c);
-        }
+        tma_load_2d(st + A_STAGE_BYTES, &mapBhi, &full[s], k0, n0);
+        tma_load_2d(st + A_STAGE_BYTES + b_bytes, &mapBlo, &full[s], k0, n0);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
-                             ((uint32_t)(p.rows_c >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+                             ((uint32_t)(nc >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % STAGES;
         const uint32_t ph = (kb / STAGES) & 1;
+        const int chunk = kb / kChunkKB;
+        const int buf = chunk & 1;
+        const bool chunk_start = (kb % kChunkKB) == 0;
+        if (chunk_start && chunk >= 2) mbar_wait(&accfree[buf], ((chunk >> 1) - 1) & 1);
         mbar_wait(&tfull[s], ph);
         mbar_wait(&full[s], ph);
         tc_after_sync();
         const uint32_t bh = smem_u32(smem + (size_t)s * stage_bytes + A_STAGE_BYTES);
         const uint32_t bl = bh + b_bytes;
         const uint32_t a_hi = tmem + kASlot + s * 32, a_lo = a_hi + 16;
+        const uint32_t d = tmem + (uint32_t)(buf * nc);
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
-          for (int ch = 0; ch < p.nchunks; ++ch) {
-            const uint32_t boff = ch * p.rows_c * (BK * 4) + kk * 32;
-            const uint64_t dh = desc_kmajor_sw64(bh + boff);
-            const uint64_t dl = desc_kmajor_sw64(bl + boff);
-            const uint32_t d = tmem + ch * p.rows_c;
-            const uint32_t first = (kb | kk) ? 1u : 0u;
-            mma_tf32_ts(d, a_lo + kk * 8, dh, idesc, first);
-            mma_tf32_ts(d, a_hi + kk * 8, dl, idesc, 1u);
-            mma_tf32_ts(d, a_hi + kk * 8, dh, idesc, 1u);
-          }
+          const uint64_t dh = desc_kmajor_sw64(bh + kk * 32);
+          const uint64_t dl = desc_kmajor_sw64(bl + kk * 32);
+          const uint32_t acc = (chunk_start && kk == 0) ? 0u : 1u;
+          mma_tf32_ts(d, a_lo + kk * 8, dh, idesc, acc);
+          mma_tf32_ts(d, a_hi + kk * 8, dl, idesc, 1u);
+          mma_tf32_ts(d, a_hi + kk * 8, dh, idesc, 1u);
         }
         mma_commit(&freeb[s]);
+        if ((kb % kChunkKB) == kChunkKB - 1 || kb == nk - 1) mma_commit(&accready[buf]);
       }
-      mma_commit(accfull);
     }
-  } else if (warp >= 4) {  // ---------------- converters, then epilogue
+  } else if (warp >= 4) {  // ---------------- converters + accumulator flushes
     const int wq = warp - 4;
     const int r = wq * 32 + lane;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    float run[NCMAX];
+#pragma unroll
+    for (int j = 0; j < NCMAX; ++j) run[j] = 0.f;
+    auto flush = [&](int chunk) {
+      const int buf = chunk & 1;
+      mbar_wait(&accready[buf], (chunk >> 1) & 1);
+      tc_after_sync();
+#pragma unroll
+      for (int j0 = 0; j0 < NCMAX; j0 += 16) {
+        if (j0 < nc) {
+          uint32_t acc[16];
+          tmem_ld16(tmem + lane_base + (uint32_t)(buf * nc + j0), acc);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int i = 0; i < 16; ++i) run[j0 + i] += __uint_as_float(acc[i]);
+        }
+      }
+      tc_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&accfree[buf]);
+    };
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % STAGES;
       const uint32_t ph = (kb / STAGES) & 1;
@@ -275,20 +309,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_before_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tfull[s]);
+      // the previous chunk's accumulator is complete once this chunk started
+      if (kb > 0 && (kb % kChunkKB) == 0) flush(kb / kChunkKB - 1);
     }
-    mbar_wait(accfull, 0);
-    tc_after_sync();
+    flush(nchunk - 1);
     const int64_t row = m0 + r;
-    for (int j0 = 0; j0 < p.npad; j0 += 16) {
-      uint32_t acc[16];
-      tmem_ld16(tmem + lane_base + j0, acc);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (row < p.M) {
+    if (row < p.M) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int j = j0 + i;
-          if (j < p.n_out) p.C[row + (int64_t)j * p.ldc] = __uint_as_float(acc[i]);
-        }
+      for (int j = 0; j < NCMAX; ++j) {
+        const int col = n0 + j;
+        if (j < nc && col < p.n_out) p.C[row + (int64_t)col * p.ldc] = run[j];
       }
     }
   }
@@ -359,16 +389,18 @@ struct Geometry {
   int npad, nchunks, rows_c;
 };
 
+// Columns are split over CTAs so that two accumulator buffers (2 x rows_c)
+// plus the A staging slots fit the 512 TMEM columns: rows_c <= 192.
 inline Geometry geometry(int l) {
   Geometry g;
-  g.nchunks = (int)ceil_div(l, 256);
+  g.nchunks = (int)ceil_div(l, 160);
   g.rows_c = (int)ceil_div(ceil_div(l, g.nchunks), 16) * 16;
   g.npad = g.rows_c * g.nchunks;
   return g;
 }
 
-inline size_t smem_bytes(int npad) {
-  return (size_t)STAGES * (A_STAGE_BYTES + 2u * (uint32_t)npad * BK * 4) + 128 + 1024;
+inline size_t smem_bytes(int rows_c) {
+  return (size_t)STAGES * (A_STAGE_BYTES + 2u * (uint32_t)rows_c * BK * 4) + 128 + 1024;
 }
 
 inline bool env_enabled() {
@@ -386,7 +418,7 @@ bool tc_gemm_supported(Ctx& c, const T* A, int64_t lda, int64_t m, int64_t n, in
     return false;
   const tc::Geometry g = tc::geometry(l);
   if (g.npad > tc::NPAD_MAX) return false;
-  if (tc::smem_bytes(g.npad) > c.max_smem_optin) return false;
+  if (tc::smem_bytes(g.rows_c) > c.max_smem_optin) return false;
   return m >= 1 && n >= 1;
 }
 
@@ -426,17 +458,28 @@ inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, 
   p.n_out = l;
   p.C = C;
   p.ldc = ldc;
-  const size_t smem = smem_bytes(g.npad);
-  const dim3 grid((unsigned)ceil_div(M, BM));
-  if (kmajor) {
-    BRSVD_CUDA(cudaFuncSetAttribute(tc3_gemm_kernel<true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    tc3_gemm_kernel<true><<<grid, kThreads, smem, c.stream>>>(mapA, mapBhi, mapBlo, p);
-  } else {
-    BRSVD_CUDA(cudaFuncSetAttribute(tc3_gemm_kernel<false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    tc3_gemm_kernel<false><<<grid, kThreads, smem, c.stream>>>(mapA, mapBhi, mapBlo, p);
-  }
+  const size_t smem = smem_bytes(g.rows_c);
+  const dim3 grid((unsigned)(ceil_div(M, BM) * g.nchunks));
+#define BRSVD_TC_LAUNCH(KM, NCM)                                                      \
+  do {                                                                                \
+    BRSVD_CUDA(cudaFuncSetAttribute(tc3_gemm_kernel<KM, NCM>,                         \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                                    (int)smem));                                      \
+    tc3_gemm_kernel<KM, NCM><<<grid, kThreads, smem, c.stream>>>(mapA, mapBhi, mapBlo, \
+                                                                 p);                  \
+  } while (0)
+#define BRSVD_TC_NC(KM)                                          \
+  do {                                                           \
+    if (g.rows_c <= 32) BRSVD_TC_LAUNCH(KM, 32);                 \
+    else if (g.rows_c <= 64) BRSVD_TC_LAUNCH(KM, 64);            \
+    else if (g.rows_c <= 96) BRSVD_TC_LAUNCH(KM, 96);            \
+    else if (g.rows_c <= 128) BRSVD_TC_LAUNCH(KM, 128);          \
+    else BRSVD_TC_LAUNCH(KM, 160);                               \
+  } while (0)
+  if (kmajor) BRSVD_TC_NC(true);
+  else BRSVD_TC_NC(false);
+#undef BRSVD_TC_NC
+#undef BRSVD_TC_LAUNCH
   BRSVD_CHECK_LAUNCH();
 }
 
