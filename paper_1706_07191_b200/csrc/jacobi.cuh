@@ -27,6 +27,7 @@ struct JacobiArgs {
   int bw, nb;  // block width; number of blocks (even)
   int max_sweeps;
   double tol;
+  double floor_rel;  // columns below floor_rel * ||G||_F are numerically null
   int* rot_count;  // [max_sweeps] zero-initialised rotation counters
   int* sweeps_done;
 };
@@ -42,7 +43,7 @@ __device__ __forceinline__ int tourn(int pos, int r, int n) {
 __device__ __forceinline__ bool jacobi_rotate_pair(double* x, double* y,
                                                    double* vx, double* vy,
                                                    int nrow, int ncol,
-                                                   double tol, int lane) {
+                                                   double tol, double floor2, int lane) {
   double a = 0.0, b = 0.0, g = 0.0;
   for (int i = lane; i < nrow; i += 32) {
     const double p = x[i], q = y[i];
@@ -53,7 +54,9 @@ __device__ __forceinline__ bool jacobi_rotate_pair(double* x, double* y,
   a = warp_sum(a);
   b = warp_sum(b);
   g = warp_sum(g);
-  if (!(a > 0.0 && b > 0.0)) return false;
+  // a pair involving a numerically null column (rounding noise) never
+  // converges in the relative sense and carries no information: skip it
+  if (!(a > floor2 && b > floor2)) return false;
   if (!(fabs(g) > tol * sqrt(a) * sqrt(b))) return false;
   const double zeta = (b - a) / (2.0 * g);
   double t;
@@ -92,6 +95,26 @@ __global__ void jacobi_block_kernel(JacobiArgs a) {
   const int npairs = a.nb / 2;
   const bool single = (a.nb == 2);
   cg::grid_group grid = cg::this_grid();
+  // ||G||_F^2 is invariant under the rotations: fix the null floor once
+  __shared__ double s_fro[32];
+  {
+    double f = 0.0;
+    for (int c = warp; c < ncol; c += nwarps)
+      for (int i = lane; i < nrow; i += 32) {
+        const double v = a.G[c * a.ldg + i];
+        f = fma(v, v, f);
+      }
+    f = warp_sum(f);
+    if (lane == 0) s_fro[warp] = f;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < nwarps; ++w) t += s_fro[w];
+      s_fro[0] = t;
+    }
+    __syncthreads();
+  }
+  const double floor2 = a.floor_rel * a.floor_rel * s_fro[0];
 
   for (int sweep = 0; sweep < a.max_sweeps; ++sweep) {
     for (int round = 0; round < a.nb - 1; ++round) {
@@ -124,7 +147,7 @@ __global__ void jacobi_block_kernel(JacobiArgs a) {
               const bool rot = jacobi_rotate_pair(
                   Gs + (size_t)ca * nrow, Gs + (size_t)cb * nrow,
                   Vs + (size_t)ca * ncol, Vs + (size_t)cb * ncol, nrow, ncol,
-                  a.tol, lane);
+                  a.tol, floor2, lane);
               if (rot && lane == 0) atomicAdd(&s_rot, 1);
             }
             __syncthreads();
@@ -209,6 +232,72 @@ __global__ void jacobi_finish_kernel(const double* __restrict__ G, int64_t ldg,
     }
     if (Vout != nullptr)
       for (int i = lane; i < ncol; i += 32) Vout[j * ldvo + i] = V[c * ldv + i];
+  }
+}
+
+// Left singular vectors of numerically null singular values (sv_j below
+// floor_rel * ||sv||_2; the Jacobi sweep never rotates those columns, so their
+// normalised columns are rounding noise) are replaced by an orthonormal
+// completion, as LAPACK's SVD returns a full orthonormal U (the reference's
+// np.linalg.svd in small_svd, kernels.py:186).  sv is sorted descending, so the
+// null columns are a suffix.  One CTA.
+__global__ void complete_null_columns_kernel(double* __restrict__ U, int64_t ldu, int nrow,
+                                             int ncol, const double* __restrict__ sv,
+                                             double floor_rel) {
+  extern __shared__ double csm[];
+  double* coef = csm;  // ncol
+  __shared__ int s_r0;
+  __shared__ double s_red[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  if (threadIdx.x == 0) {
+    double f = 0.0;
+    for (int j = 0; j < ncol; ++j) f += sv[j] * sv[j];
+    const double fl = floor_rel * sqrt(f);
+    int r0 = ncol;
+    for (int j = 0; j < ncol; ++j)
+      if (!(sv[j] > fl)) { r0 = j; break; }
+    s_r0 = r0;
+  }
+  __syncthreads();
+  const int r0 = s_r0;
+  for (int j = r0; j < ncol; ++j) {
+    double* v = U + (int64_t)j * ldu;
+    for (int i = threadIdx.x; i < nrow; i += blockDim.x) {
+      uint32_t h = (uint32_t)(i * 0x9E3779B1u) ^ (uint32_t)(j * 0x85EBCA77u) ^ 0xC2B2AE3Du;
+      h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12; h *= 0x297A2D39u; h ^= h >> 15;
+      v[i] = (double)h * (1.0 / 4294967296.0) - 0.5;
+    }
+    __syncthreads();
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int c = warp; c < j; c += nwarps) {
+        const double* u = U + (int64_t)c * ldu;
+        double d = 0.0;
+        for (int i = lane; i < nrow; i += 32) d = fma(u[i], v[i], d);
+        d = warp_sum(d);
+        if (lane == 0) coef[c] = d;
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < nrow; i += blockDim.x) {
+        double acc = v[i];
+        for (int c = 0; c < j; ++c) acc = fma(-coef[c], U[(int64_t)c * ldu + i], acc);
+        v[i] = acc;
+      }
+      __syncthreads();
+    }
+    double nn = 0.0;
+    for (int i = threadIdx.x; i < nrow; i += blockDim.x) nn = fma(v[i], v[i], nn);
+    nn = warp_sum(nn);
+    if (lane == 0) s_red[warp] = nn;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < nwarps; ++w) t += s_red[w];
+      s_red[0] = t > 0.0 ? 1.0 / sqrt(t) : 0.0;
+    }
+    __syncthreads();
+    const double inv = s_red[0];
+    for (int i = threadIdx.x; i < nrow; i += blockDim.x) v[i] *= inv;
+    __syncthreads();
   }
 }
 

@@ -11,6 +11,8 @@
 #pragma once
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -147,6 +149,13 @@ void gemm_nn_cm(Ctx& c, int64_t r, int64_t b, int64_t a, const TX* X, int64_t ld
                            beta, C0, 1, ldc0);
 }
 
+// Readback of a few device scalars (one synchronisation).
+inline void readback(Ctx& c, const void* d, void* h, size_t bytes) {
+  BRSVD_CUDA(cudaMemcpyAsync(c.h_pinned, d, bytes, cudaMemcpyDeviceToHost, c.stream));
+  BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+  std::memcpy(h, c.h_pinned, bytes);
+}
+
 // ---------------------------------------------------------------------------
 // Jacobi SVD launcher: G (nrow x ncol, ldg) <- G V, V (ncol x ncol) accumulated.
 // tol: rotate a column pair while |x.y| > tol * ||x|| ||y||.  The dot products
@@ -199,6 +208,7 @@ inline int jacobi(Ctx& c, double* G, int nrow, int ncol, int64_t ldg, double* V,
   args.nb = nb;
   args.max_sweeps = max_sweeps;
   args.tol = std::max(tol, jacobi_tol_tight(nrow));
+  args.floor_rel = 16.0 * nrow * 2.220446049250313e-16;
   args.rot_count = counters.p;
   args.sweeps_done = counters.p + max_sweeps;
   if (single) {
@@ -214,6 +224,12 @@ inline int jacobi(Ctx& c, double* G, int nrow, int ncol, int64_t ldg, double* V,
     BRSVD_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_block_kernel, dim3(grid),
                                            dim3(threads), kargs, smem, c.stream));
     ++g_brsvd_launches;
+  }
+  if (std::getenv("BRSVD_DEBUG")) {
+    int sw = 0;
+    readback(c, counters.p + max_sweeps, &sw, sizeof(int));
+    std::fprintf(stderr, "[brsvd] jacobi %dx%d tol %.1e: %d sweeps (nb %d, bw %d)\n", nrow,
+                 ncol, args.tol, sw, nb, bw);
   }
   return nb;
 }
@@ -260,13 +276,6 @@ void normalize_sketch(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, T* Xout
                                                0, Tm.p, nullptr);
   BRSVD_CHECK_LAUNCH();
   gemm_nn_cm<T, double, T>(c, r, l, l, X, ldx, Tm.p, l, Xout, ldo);
-}
-
-// Readback of a few device scalars (one synchronisation).
-inline void readback(Ctx& c, const void* d, void* h, size_t bytes) {
-  BRSVD_CUDA(cudaMemcpyAsync(c.h_pinned, d, bytes, cudaMemcpyDeviceToHost, c.stream));
-  BRSVD_CUDA(cudaStreamSynchronize(c.stream));
-  std::memcpy(h, c.h_pinned, bytes);
 }
 
 inline int read_int(Ctx& c, const int* d) {
@@ -398,6 +407,9 @@ int small_svd_device(Ctx& c, const T* Bt, int64_t n, int l, int64_t ldb, double*
   BRSVD_CHECK_LAUNCH();
   jacobi(c, M.p, l, l, l, Vj.p, l, jacobi_tol_tight(l));
   jacobi_finish(c, M.p, l, l, l, Vj.p, l, sigma, W, l, Zj.p, l);
+  complete_null_columns_kernel<<<1, 1024, (size_t)l * sizeof(double), c.stream>>>(
+      W, l, l, l, sigma, 16.0 * l * 2.220446049250313e-16);
+  BRSVD_CHECK_LAUNCH();
   gemm_nn_cm<double, double, T>(c, n, l, l, Qb.p, n, Zj.p, l, Vout, ldv);
   return rank;
 }
