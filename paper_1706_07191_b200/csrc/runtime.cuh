@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "gemm_simt.cuh"
+#include "chol.cuh"
 #include "jacobi.cuh"
 #include "small_kernels.cuh"
 
@@ -264,24 +265,58 @@ inline double orth_tau(int64_t r, int l) {
   return 8.0 * (double)std::max<int64_t>(r, l) * 2.220446049250313e-16;
 }
 
-// Regularised basis change for the power iteration: Xout = X S E Lam^-1/2
-// with eigenvalues floored at tau*lam_0.  Same column span as X (exact
-// arithmetic), conditioning restored; no host synchronisation.
+constexpr int kCholMaxL = 400;  // chol_kernel shared-memory limit
+
+// Cholesky basis change of X (r x l): with s_j = 1/||x_j|| and the scaled Gram
+// G~ = S X^T X S, factor G~ + shift I = L L^T and return T = S L^-T in Tm
+// (l x l, column-major).  Returns min pivot / diagonal (1 = orthogonal
+// columns, ~1/cond^2 otherwise, <= 0 on breakdown) when `ratio` is requested.
+template <typename T>
+double chol_basis(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double shift,
+                  double* Tm, bool read_ratio, double drop = 0.0) {
+  DBuf<double> G(c, (size_t)l * l), W(c, (size_t)l * l), s(c, l), info(c, 1);
+  gemm_tn_cm<T, T, double>(c, l, l, r, X, ldx, X, ldx, G.p, l);
+  gram_prep_kernel<<<1, 1024, 0, c.stream>>>(G.p, l, s.p, W.p, 1, nullptr, drop);
+  BRSVD_CHECK_LAUNCH();
+  chol_kernel<<<1, 1024, chol_smem(l), c.stream>>>(G.p, l, l, shift, info.p);
+  BRSVD_CHECK_LAUNCH();
+  trinv_t_kernel<<<1, 1024, trinv_smem(l), c.stream>>>(G.p, l, l, s.p, W.p, Tm);
+  BRSVD_CHECK_LAUNCH();
+  double ratio = 0.0;
+  if (read_ratio) readback(c, info.p, &ratio, sizeof(double));
+  return ratio;
+}
+
+inline void set_chol_attrs(Ctx& c) {
+  static bool done = false;
+  if (done) return;
+  const int lim = (int)std::min<size_t>(c.max_smem_optin, 227 * 1024);
+  BRSVD_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+  BRSVD_CUDA(cudaFuncSetAttribute(trinv_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  lim));
+  done = true;
+}
+
+// Basis change for the power iteration: Xout spans range(X) with restored
+// conditioning.  Shifted Cholesky QR (shift ~ l*eps of the unit diagonal,
+// never breaks down) when l fits the Cholesky kernel, else the regularised
+// Gram-eigen basis X S E Lam^-1/2 (eigenvalues floored at tau*lam_0).  No
+// host synchronisation either way.
 template <typename T>
 void normalize_sketch(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, T* Xout,
                       int64_t ldo) {
-  DBuf<double> E(c, (size_t)l * l), lam(c, l), s(c, l), Tm(c, (size_t)l * l);
-  gram_eig<T>(c, X, r, l, ldx, E.p, lam.p, s.p, kJacobiTolNormalize);
-  build_basis_kernel<<<1, 1024, 0, c.stream>>>(E.p, lam.p, s.p, l, orth_tau(r, l),
-                                               0, Tm.p, nullptr);
-  BRSVD_CHECK_LAUNCH();
+  DBuf<double> Tm(c, (size_t)l * l);
+  if (l <= kCholMaxL) {
+    set_chol_attrs(c);
+    chol_basis<T>(c, X, r, l, ldx, 16.0 * l * 2.220446049250313e-16, Tm.p, false);
+  } else {
+    DBuf<double> E(c, (size_t)l * l), lam(c, l), s(c, l);
+    gram_eig<T>(c, X, r, l, ldx, E.p, lam.p, s.p, kJacobiTolNormalize);
+    build_basis_kernel<<<1, 1024, 0, c.stream>>>(E.p, lam.p, s.p, l, orth_tau(r, l), 0,
+                                                 Tm.p, nullptr);
+    BRSVD_CHECK_LAUNCH();
+  }
   gemm_nn_cm<T, double, T>(c, r, l, l, X, ldx, Tm.p, l, Xout, ldo);
-}
-
-inline int read_int(Ctx& c, const int* d) {
-  int v;
-  readback(c, d, &v, sizeof(int));
-  return v;
 }
 
 // Block projection X <- X - Qb (Qb^T X), applied twice ("twice is enough").
@@ -331,6 +366,17 @@ int orth_full(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* Q,
   DBuf<double> scal(c, 4);
   DBuf<int> drank(c, 1);
   const double drop = 4.0 * l * eps_data;  // the reference's rank cut, kernels.py:155-157
+  // Fast path: Cholesky QR + Newton-Schulz when the scaled Gram is safely
+  // positive definite (every pivot above tau: nothing to reveal).
+  if (l <= kCholMaxL) {
+    set_chol_attrs(c);
+    const double ratio = chol_basis<T>(c, X, r, l, ldx, 0.0, Tm.p, true, drop);
+    if (ratio > tau) {
+      gemm_nn_cm<T, double, double>(c, r, l, l, X, ldx, Tm.p, l, Q, r);
+      ns_refine(c, Q, r, l, std::max(ns_iters, 1));
+      return l;
+    }
+  }
   gram_eig<T>(c, X, r, l, ldx, E.p, lam.p, s.p, kJacobiTolOrth, true, scal.p, drop);
   build_basis_kernel<<<1, 1024, 0, c.stream>>>(E.p, lam.p, s.p, l, tau, 1, Tm.p,
                                                drank.p);
