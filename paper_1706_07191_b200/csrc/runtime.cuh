@@ -265,7 +265,7 @@ inline double orth_tau(int64_t r, int l) {
   return 8.0 * (double)std::max<int64_t>(r, l) * 2.220446049250313e-16;
 }
 
-constexpr int kCholMaxL = 400;  // chol_kernel shared-memory limit
+constexpr int kCholMaxL = 384;  // chol_kernel shared-memory limit (~197 KB)
 
 // Cholesky basis change of X (r x l): with s_j = 1/||x_j|| and the scaled Gram
 // G~ = S X^T X S, factor G~ + shift I = L L^T and return T = S L^-T in Tm
@@ -290,7 +290,7 @@ double chol_basis(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double shif
 inline void set_chol_attrs(Ctx& c) {
   static bool done = false;
   if (done) return;
-  const int lim = (int)std::min<size_t>(c.max_smem_optin, 227 * 1024);
+  const int lim = (int)c.max_smem_optin - 2048;  // leave room for static smem
   BRSVD_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
   BRSVD_CUDA(cudaFuncSetAttribute(trinv_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   lim));
