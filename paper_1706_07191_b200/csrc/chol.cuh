@@ -58,7 +58,9 @@ __global__ void chol_kernel(double* __restrict__ A, int n, int64_t ld, double sh
       __shared__ double s_d;
       if (tid == 0) {
         double piv = P[c * n + c];
-        const double ratio = piv / diag0[p0 + c];
+        const double dg = diag0[p0 + c];
+        // a zero (dropped) column or a NaN pivot counts as a breakdown
+        const double ratio = (dg > 0.0 && piv == piv) ? piv / dg : -1.0;
         if (ratio < s_minr) s_minr = ratio;
         if (!(piv > 0.0)) piv = 1e-300;
         s_d = sqrt(piv);
