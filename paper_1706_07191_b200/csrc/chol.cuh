@@ -17,8 +17,15 @@ constexpr int kCholNB = 32;
 // info[0] = min_j pivot_j / (A_jj + shift) (1 for a perfectly orthogonal
 // problem, <= 0 when the factorisation broke down); non-positive pivots are
 // replaced by a tiny positive value so the output stays finite.
+//
+// With colnorm (||x_j||, the inverse column scaling) and rank_tol > 0,
+// info[1] = #{j : L_jj ||x_j|| > rank_tol ||X||_F} -- the |diag R| criterion of
+// the reference's tsqr_factor (kernels.py:155-157), since the Cholesky factor
+// of the Gram is the R of an unpivoted QR of X.
 __global__ void chol_kernel(double* __restrict__ A, int n, int64_t ld, double shift,
-                            double* __restrict__ info) {
+                            double* __restrict__ info,
+                            const double* __restrict__ colnorm_inv = nullptr,
+                            double rank_tol = 0.0) {
   extern __shared__ double csm[];
   double* P = csm;                          // panel, rows x NB  (P[c * n + i])
   double* Lp = csm + (size_t)n * kCholNB;   // panel rows of L: Lp[k * NB + c], k < p0
@@ -87,7 +94,19 @@ __global__ void chol_kernel(double* __restrict__ A, int n, int64_t ld, double sh
     const int i = e % n, j = e / n;
     if (i < j) A[(int64_t)j * ld + i] = 0.0;
   }
-  if (tid == 0 && info) info[0] = s_minr;
+  if (tid == 0 && info) {
+    info[0] = s_minr;
+    if (colnorm_inv != nullptr) {
+      double fro2 = 0.0;
+      for (int j = 0; j < n; ++j)
+        if (colnorm_inv[j] > 0.0) fro2 += 1.0 / (colnorm_inv[j] * colnorm_inv[j]);
+      const double cut = rank_tol * sqrt(fro2);
+      int rk = 0;
+      for (int j = 0; j < n; ++j)
+        if (colnorm_inv[j] > 0.0 && A[(int64_t)j * ld + j] / colnorm_inv[j] > cut) ++rk;
+      info[1] = (double)rk;
+    }
+  }
 }
 
 // X = L^-1 for lower-triangular L (n x n, column-major), by block rows:

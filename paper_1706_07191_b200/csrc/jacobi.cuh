@@ -39,11 +39,12 @@ __device__ __forceinline__ int tourn(int pos, int r, int n) {
 }
 
 // Rotate columns x, y (length nrow in Gs, length ncol in Vs) so they become
-// orthogonal.  Returns true if a rotation was applied.  Executed by one warp.
+// orthogonal.  Returns true if a rotation was applied.  Executed by one warp;
+// the three reductions share one butterfly so their shuffles overlap.
 __device__ __forceinline__ bool jacobi_rotate_pair(double* x, double* y,
                                                    double* vx, double* vy,
                                                    int nrow, int ncol,
-                                                   double tol, double floor2, int lane) {
+                                                   double tol2, double floor2, int lane) {
   double a = 0.0, b = 0.0, g = 0.0;
   for (int i = lane; i < nrow; i += 32) {
     const double p = x[i], q = y[i];
@@ -51,32 +52,45 @@ __device__ __forceinline__ bool jacobi_rotate_pair(double* x, double* y,
     b = fma(q, q, b);
     g = fma(p, q, g);
   }
-  a = warp_sum(a);
-  b = warp_sum(b);
-  g = warp_sum(g);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    g += __shfl_xor_sync(0xffffffffu, g, o);
+  }
   // a pair involving a numerically null column (rounding noise) never
   // converges in the relative sense and carries no information: skip it
   if (!(a > floor2 && b > floor2)) return false;
-  if (!(fabs(g) > tol * sqrt(a) * sqrt(b))) return false;
+  if (!(g * g > tol2 * a * b)) return false;
   const double zeta = (b - a) / (2.0 * g);
   double t;
   if (fabs(zeta) > 1e150) {
     t = 0.5 / zeta;
   } else {
-    t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+    t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
   }
   if (t == 0.0) return false;
-  const double c = 1.0 / sqrt(1.0 + t * t);
+  const double c = 1.0 / sqrt(fma(t, t, 1.0));
   const double s = c * t;
-  for (int i = lane; i < nrow; i += 32) {
-    const double p = x[i], q = y[i];
-    x[i] = c * p - s * q;
-    y[i] = s * p + c * q;
-  }
-  for (int i = lane; i < ncol; i += 32) {
-    const double p = vx[i], q = vy[i];
-    vx[i] = c * p - s * q;
-    vy[i] = s * p + c * q;
+  if (nrow == ncol) {
+    for (int i = lane; i < nrow; i += 32) {
+      const double p = x[i], q = y[i], pv = vx[i], qv = vy[i];
+      x[i] = c * p - s * q;
+      y[i] = s * p + c * q;
+      vx[i] = c * pv - s * qv;
+      vy[i] = s * pv + c * qv;
+    }
+  } else {
+    for (int i = lane; i < nrow; i += 32) {
+      const double p = x[i], q = y[i];
+      x[i] = c * p - s * q;
+      y[i] = s * p + c * q;
+    }
+    for (int i = lane; i < ncol; i += 32) {
+      const double p = vx[i], q = vy[i];
+      vx[i] = c * p - s * q;
+      vy[i] = s * p + c * q;
+    }
   }
   return true;
 }
@@ -136,18 +150,31 @@ __global__ void jacobi_block_kernel(JacobiArgs a) {
         }
         __syncthreads();
         const int inner = single ? 64 : 1;
+        // Round 0 of a sweep orthogonalises all 2bw columns of the pair
+        // (within-block and cross pairs); later rounds only need the cross
+        // pairs (block a column i against block b column (i + ir) mod bw),
+        // which halves the sequential depth of a sweep to ~l + bw rounds.
+        const bool full_inner = single || round == 0;
+        const int n_inner = full_inner ? W - 1 : a.bw;
         int total = 0;
         for (int is = 0; is < inner; ++is) {
           if (threadIdx.x == 0) s_rot = 0;
           __syncthreads();
-          for (int ir = 0; ir < W - 1; ++ir) {
+          for (int ir = 0; ir < n_inner; ++ir) {
             for (int p = warp; p < W / 2; p += nwarps) {
-              const int ca = tourn(p, ir, W), cb = tourn(W - 1 - p, ir, W);
+              int ca, cb;
+              if (full_inner) {
+                ca = tourn(p, ir, W);
+                cb = tourn(W - 1 - p, ir, W);
+              } else {
+                ca = p;
+                cb = a.bw + (p + ir) % a.bw;
+              }
               if (cols[ca] < 0 || cols[cb] < 0) continue;
               const bool rot = jacobi_rotate_pair(
                   Gs + (size_t)ca * nrow, Gs + (size_t)cb * nrow,
                   Vs + (size_t)ca * ncol, Vs + (size_t)cb * ncol, nrow, ncol,
-                  a.tol, floor2, lane);
+                  a.tol * a.tol, floor2, lane);
               if (rot && lane == 0) atomicAdd(&s_rot, 1);
             }
             __syncthreads();

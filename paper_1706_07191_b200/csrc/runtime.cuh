@@ -273,18 +273,21 @@ constexpr int kCholMaxL = 384;  // chol_kernel shared-memory limit (~197 KB)
 // columns, ~1/cond^2 otherwise, <= 0 on breakdown) when `ratio` is requested.
 template <typename T>
 double chol_basis(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double shift,
-                  double* Tm, bool read_ratio, double drop = 0.0) {
-  DBuf<double> G(c, (size_t)l * l), W(c, (size_t)l * l), s(c, l), info(c, 1);
+                  double* Tm, bool read_ratio, double drop = 0.0, double rank_tol = 0.0,
+                  int* rank_ref = nullptr) {
+  DBuf<double> G(c, (size_t)l * l), W(c, (size_t)l * l), s(c, l), info(c, 2);
   gemm_tn_cm<T, T, double>(c, l, l, r, X, ldx, X, ldx, G.p, l);
   gram_prep_kernel<<<1, 1024, 0, c.stream>>>(G.p, l, s.p, W.p, 1, nullptr, drop);
   BRSVD_CHECK_LAUNCH();
-  chol_kernel<<<1, 1024, chol_smem(l), c.stream>>>(G.p, l, l, shift, info.p);
+  chol_kernel<<<1, 1024, chol_smem(l), c.stream>>>(G.p, l, l, shift, info.p,
+                                                   rank_ref ? s.p : nullptr, rank_tol);
   BRSVD_CHECK_LAUNCH();
   trinv_t_kernel<<<1, 1024, trinv_smem(l), c.stream>>>(G.p, l, l, s.p, W.p, Tm);
   BRSVD_CHECK_LAUNCH();
-  double ratio = 0.0;
-  if (read_ratio) readback(c, info.p, &ratio, sizeof(double));
-  return ratio;
+  double h[2] = {0.0, 0.0};
+  if (read_ratio || rank_ref) readback(c, info.p, h, sizeof(h));
+  if (rank_ref) *rank_ref = (int)h[1];
+  return h[0];
 }
 
 inline void set_chol_attrs(Ctx& c) {
@@ -368,13 +371,22 @@ int orth_full(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* Q,
   const double drop = 4.0 * l * eps_data;  // the reference's rank cut, kernels.py:155-157
   // Fast path: Cholesky QR + Newton-Schulz when the scaled Gram is safely
   // positive definite (every pivot above tau: nothing to reveal).
+  // The reported rank follows the reference's |diag R| > l eps ||X||_F cut.
+  // A healthy fp64 Cholesky (pivots above 1e-12 of the unit diagonal) resolves
+  // every direction Householder QR would, so the second CholQR pass makes Q
+  // orthonormal to rounding.
   if (l <= kCholMaxL) {
     set_chol_attrs(c);
-    const double ratio = chol_basis<T>(c, X, r, l, ldx, 0.0, Tm.p, true, drop);
-    if (ratio > tau) {
-      gemm_nn_cm<T, double, double>(c, r, l, l, X, ldx, Tm.p, l, Q, r);
-      ns_refine(c, Q, r, l, std::max(ns_iters, 1));
-      return l;
+    int rank_ref = l;
+    const double ratio =
+        chol_basis<T>(c, X, r, l, ldx, 0.0, Tm.p, true, drop, l * eps_data, &rank_ref);
+    if (ratio > 1e-12) {
+      DBuf<double> Q1(c, (size_t)r * l);
+      gemm_nn_cm<T, double, double>(c, r, l, l, X, ldx, Tm.p, l, Q1.p, r);
+      chol_basis<double>(c, Q1.p, r, l, r, 0.0, Tm.p, false);
+      gemm_nn_cm<double, double, double>(c, r, l, l, Q1.p, r, Tm.p, l, Q, r);
+      if (ns_iters > 1) ns_refine(c, Q, r, l, 1);
+      return rank_ref;
     }
   }
   gram_eig<T>(c, X, r, l, ldx, E.p, lam.p, s.p, kJacobiTolOrth, true, scal.p, drop);
