@@ -22,14 +22,22 @@ constexpr int kCholNB = 32;
 // info[1] = #{j : L_jj ||x_j|| > rank_tol ||X||_F} -- the |diag R| criterion of
 // the reference's tsqr_factor (kernels.py:155-157), since the Cholesky factor
 // of the Gram is the R of an unpivoted QR of X.
+//
+// drop_ratio > 0 turns the factorisation rank-revealing in column order: a
+// column whose pivot falls below drop_ratio of its diagonal lies numerically in
+// the span of the earlier ones; its L column is zeroed (unit diagonal, so L
+// stays invertible) and it is left out of `keep` (kept column indices, in
+// order).  info[2] = number of kept columns, info[0] = min ratio over kept.
 __global__ void chol_kernel(double* __restrict__ A, int n, int64_t ld, double shift,
                             double* __restrict__ info,
                             const double* __restrict__ colnorm_inv = nullptr,
-                            double rank_tol = 0.0) {
+                            double rank_tol = 0.0, double drop_ratio = 0.0,
+                            int* __restrict__ keep = nullptr) {
   extern __shared__ double csm[];
   double* P = csm;                          // panel, rows x NB  (P[c * n + i])
   double* Lp = csm + (size_t)n * kCholNB;   // panel rows of L: Lp[k * NB + c], k < p0
   double* diag0 = Lp + (size_t)n * kCholNB; // original diagonal (+ shift)
+  int* dropped = reinterpret_cast<int*>(diag0 + n);
   __shared__ double s_minr;
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int j = tid; j < n; j += nt) diag0[j] = A[j * ld + j] + shift;
@@ -68,14 +76,25 @@ __global__ void chol_kernel(double* __restrict__ A, int n, int64_t ld, double sh
         const double dg = diag0[p0 + c];
         // a zero (dropped) column or a NaN pivot counts as a breakdown
         const double ratio = (dg > 0.0 && piv == piv) ? piv / dg : -1.0;
-        if (ratio < s_minr) s_minr = ratio;
-        if (!(piv > 0.0)) piv = 1e-300;
-        s_d = sqrt(piv);
-        P[c * n + c] = s_d;
+        if (drop_ratio > 0.0 && !(ratio > drop_ratio)) {
+          s_d = 0.0;                       // dropped: zero column, unit diagonal
+          P[c * n + c] = 1.0;
+          dropped[p0 + c] = 1;
+        } else {
+          if (ratio < s_minr) s_minr = ratio;
+          if (!(piv > 0.0)) piv = 1e-300;
+          s_d = sqrt(piv);
+          P[c * n + c] = s_d;
+          dropped[p0 + c] = 0;
+        }
       }
       __syncthreads();
       const double d = s_d;
-      for (int i = c + 1 + tid; i < rows; i += nt) P[c * n + i] /= d;
+      if (d == 0.0) {
+        for (int i = c + 1 + tid; i < rows; i += nt) P[c * n + i] = 0.0;
+      } else {
+        for (int i = c + 1 + tid; i < rows; i += nt) P[c * n + i] /= d;
+      }
       __syncthreads();
       for (int e = tid; e < rows * (nb - c - 1); e += nt) {
         const int i = e % rows, c2 = c + 1 + e / rows;
@@ -94,8 +113,16 @@ __global__ void chol_kernel(double* __restrict__ A, int n, int64_t ld, double sh
     const int i = e % n, j = e / n;
     if (i < j) A[(int64_t)j * ld + i] = 0.0;
   }
+  __syncthreads();
   if (tid == 0 && info) {
     info[0] = s_minr;
+    int kept = 0;
+    for (int j = 0; j < n; ++j)
+      if (!dropped[j]) {
+        if (keep) keep[kept] = j;
+        ++kept;
+      }
+    info[2] = (double)kept;
     if (colnorm_inv != nullptr) {
       double fro2 = 0.0;
       for (int j = 0; j < n; ++j)
@@ -103,9 +130,21 @@ __global__ void chol_kernel(double* __restrict__ A, int n, int64_t ld, double sh
       const double cut = rank_tol * sqrt(fro2);
       int rk = 0;
       for (int j = 0; j < n; ++j)
-        if (colnorm_inv[j] > 0.0 && A[(int64_t)j * ld + j] / colnorm_inv[j] > cut) ++rk;
+        if (!dropped[j] && colnorm_inv[j] > 0.0 && A[(int64_t)j * ld + j] / colnorm_inv[j] > cut)
+          ++rk;
       info[1] = (double)rk;
     }
+  }
+}
+
+// Tc[:, c] = T[:, keep[c]] for the kept columns (count from info[2]).
+__global__ void compact_cols_kernel(const double* __restrict__ T, int l,
+                                    const int* __restrict__ keep,
+                                    const double* __restrict__ info, double* __restrict__ Tc) {
+  const int k = (int)info[2];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < l * k; e += gridDim.x * blockDim.x) {
+    const int i = e % l, c = e / l;
+    Tc[(int64_t)c * l + i] = T[(int64_t)keep[c] * l + i];
   }
 }
 
@@ -166,7 +205,7 @@ __global__ void trinv_t_kernel(const double* __restrict__ L, int n, int64_t ld,
 }
 
 inline size_t chol_smem(int n) {
-  return ((size_t)n * kCholNB * 2 + (size_t)n) * sizeof(double);
+  return ((size_t)n * kCholNB * 2 + (size_t)n) * sizeof(double) + (size_t)n * sizeof(int);
 }
 inline size_t trinv_smem(int n) {
   return ((size_t)n * kCholNB + kCholNB * kCholNB + (size_t)n * kCholNB) * sizeof(double);

@@ -157,6 +157,12 @@ inline void readback(Ctx& c, const void* d, void* h, size_t bytes) {
   std::memcpy(h, c.h_pinned, bytes);
 }
 
+inline int read_int(Ctx& c, const int* d) {
+  int v;
+  readback(c, d, &v, sizeof(int));
+  return v;
+}
+
 // ---------------------------------------------------------------------------
 // Jacobi SVD launcher: G (nrow x ncol, ldg) <- G V, V (ncol x ncol) accumulated.
 // tol: rotate a column pair while |x.y| > tol * ||x|| ||y||.  The dot products
@@ -271,23 +277,46 @@ constexpr int kCholMaxL = 384;  // chol_kernel shared-memory limit (~197 KB)
 // G~ = S X^T X S, factor G~ + shift I = L L^T and return T = S L^-T in Tm
 // (l x l, column-major).  Returns min pivot / diagonal (1 = orthogonal
 // columns, ~1/cond^2 otherwise, <= 0 on breakdown) when `ratio` is requested.
+struct CholInfo {
+  double min_ratio = 0.0;  // min pivot / diagonal over the kept columns
+  int rank_ref = 0;        // reference-style |diag R| rank (kernels.py:155-157)
+  int kept = 0;            // columns kept by the rank-revealing pass
+};
+
+// Cholesky basis change of X (r x l): with s_j = 1/||x_j|| and the scaled Gram
+// G~ = S X^T X S, factor G~ + shift I = L L^T and return T = S L^-T in Tm
+// (l x l, column-major).  drop_ratio > 0 drops (in column order) the columns
+// whose pivot falls below it; `keep` (device, l ints) then lists the kept
+// columns.  Host-visible diagnostics only when `sync` is set.
 template <typename T>
-double chol_basis(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double shift,
-                  double* Tm, bool read_ratio, double drop = 0.0, double rank_tol = 0.0,
-                  int* rank_ref = nullptr) {
-  DBuf<double> G(c, (size_t)l * l), W(c, (size_t)l * l), s(c, l), info(c, 2);
+CholInfo chol_basis(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double shift,
+                    double* Tm, bool sync, double col_drop = 0.0, double rank_tol = 0.0,
+                    double drop_ratio = 0.0, int* keep = nullptr,
+                    double* info_dev = nullptr) {
+  DBuf<double> G(c, (size_t)l * l), W(c, (size_t)l * l), s(c, l), infob;
+  double* info = info_dev;
+  if (!info) {
+    infob.alloc(c, 3);
+    info = infob.p;
+  }
   gemm_tn_cm<T, T, double>(c, l, l, r, X, ldx, X, ldx, G.p, l);
-  gram_prep_kernel<<<1, 1024, 0, c.stream>>>(G.p, l, s.p, W.p, 1, nullptr, drop);
+  gram_prep_kernel<<<1, 1024, 0, c.stream>>>(G.p, l, s.p, W.p, 1, nullptr, col_drop);
   BRSVD_CHECK_LAUNCH();
-  chol_kernel<<<1, 1024, chol_smem(l), c.stream>>>(G.p, l, l, shift, info.p,
-                                                   rank_ref ? s.p : nullptr, rank_tol);
+  chol_kernel<<<1, 1024, chol_smem(l), c.stream>>>(G.p, l, l, shift, info,
+                                                   rank_tol > 0.0 ? s.p : nullptr, rank_tol,
+                                                   drop_ratio, keep);
   BRSVD_CHECK_LAUNCH();
   trinv_t_kernel<<<1, 1024, trinv_smem(l), c.stream>>>(G.p, l, l, s.p, W.p, Tm);
   BRSVD_CHECK_LAUNCH();
-  double h[2] = {0.0, 0.0};
-  if (read_ratio || rank_ref) readback(c, info.p, h, sizeof(h));
-  if (rank_ref) *rank_ref = (int)h[1];
-  return h[0];
+  CholInfo ci;
+  if (sync) {
+    double h[3];
+    readback(c, info, h, sizeof(h));
+    ci.min_ratio = h[0];
+    ci.rank_ref = (int)h[1];
+    ci.kept = (int)h[2];
+  }
+  return ci;
 }
 
 inline void set_chol_attrs(Ctx& c) {
@@ -348,105 +377,154 @@ inline void ns_refine(Ctx& c, double* Q, int64_t r, int k, int iters) {
   }
 }
 
-// Rank-revealing orthonormal basis of range(X), X (r x l), r >= l.
+// Deflation levels: the part of X that level 1 left unresolved,
+// R = (I - Q Q^T) X, is re-factored with an unscaled Gram (eigen route, so the
+// threshold is relative to R's own scale) while ||R||_F^2 > stop2.  A Gram
+// resolves directions down to ~sqrt(tau) of its largest, Householder QR (the
+// reference's tsqr, kernels.py:121-164) down to eps; each level buys another
+// factor sqrt(tau).  Appends columns to Q and to the reported rank.
+template <typename T>
+void deflate_levels(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* Q,
+                    int& total, int& rank, double stop2, double tau, int ns_iters) {
+  if (total >= l || !(stop2 > 0.0)) return;
+  DBuf<double> E(c, (size_t)l * l), lam(c, l), s(c, l), Tm(c, (size_t)l * l);
+  DBuf<double> scal(c, 4);
+  DBuf<int> drank(c, 1);
+  DBuf<double> R(c, (size_t)r * l);
+  copy2d_kernel<T, double><<<grid_for(r * l), 256, 0, c.stream>>>(X, r, l, ldx, R.p, r);
+  BRSVD_CHECK_LAUNCH();
+  DBuf<double> G(c, (size_t)l * l), V(c, (size_t)l * l);
+  for (int level = 0; level < 4 && total < l; ++level) {
+    project_out(c, Q, r, total, R.p, l);
+    // ||R||_F^2 first: most calls stop here without an eigen-solve
+    gemm_tn_cm<double, double, double>(c, l, l, r, R.p, r, R.p, r, G.p, l);
+    gram_prep_kernel<<<1, 1024, 0, c.stream>>>(G.p, l, s.p, V.p, 0, scal.p, 0.0);
+    BRSVD_CHECK_LAUNCH();
+    double nr2;
+    readback(c, scal.p, &nr2, sizeof(double));
+    if (!(nr2 > stop2)) break;
+    jacobi(c, G.p, l, l, l, V.p, l, kJacobiTolOrth);
+    jacobi_finish(c, G.p, l, l, l, V.p, l, lam.p, nullptr, 0, E.p, l);
+    build_basis_kernel<<<1, 1024, 0, c.stream>>>(E.p, lam.p, s.p, l, tau, 1, Tm.p,
+                                                 drank.p);
+    BRSVD_CHECK_LAUNCH();
+    int rk2 = read_int(c, drank.p);
+    if (rk2 <= 0) break;
+    rk2 = std::min(rk2, l - total);
+    double* Qn = Q + (int64_t)total * r;
+    gemm_nn_cm<double, double, double>(c, r, rk2, l, R.p, r, Tm.p, l, Qn, r);
+    project_out(c, Q, r, total, Qn, rk2);
+    ns_refine(c, Qn, r, rk2, std::max(ns_iters, 1));
+    total += rk2;
+    rank += rk2;
+  }
+}
+
+template <typename T>
+int orth_full(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* Q,
+              uint64_t seed, int ns_iters);
+
+// Numerically null directions: Gaussian columns projected out twice and
+// orthonormalised (kernels.py:142-144, "columns of Q remain orthonormal").
+inline void complete_basis(Ctx& c, double* Q, int64_t r, int l, int total, uint64_t seed,
+                           int ns_iters) {
+  if (total >= l) return;
+  const int cnt = l - total;
+  double* W = Q + (int64_t)total * r;
+  gaussian_kernel<double><<<grid_for(r * ((cnt + 1) / 2)), 256, 0, c.stream>>>(
+      W, r, cnt, r, seed, 0x636f6d706c657465ull, 0);
+  BRSVD_CHECK_LAUNCH();
+  project_out(c, Q, r, total, W, cnt);
+  DBuf<double> Wq(c, (size_t)r * cnt);
+  orth_full<double>(c, W, r, cnt, r, Wq.p, seed * 0x9E3779B97F4A7C15ull + 1,
+                    std::max(ns_iters, 1));
+  BRSVD_CUDA(cudaMemcpyAsync(W, Wq.p, sizeof(double) * r * cnt, cudaMemcpyDeviceToDevice,
+                             c.stream));
+  project_out(c, Q, r, total, W, cnt);
+  ns_refine(c, W, r, cnt, 1);
+}
+
+// Rank-revealing orthonormal basis of range(X), X (r x l), r >= l
+// (tsqr / tsqr_factor, kernels.py:139-170).  Returns the detected numerical
+// rank; Q is r x l, fp64, ld r, always with l orthonormal columns.
 //
-// Level 1: column-scaled Gram, Jacobi eigenpairs, keep lam > tau*lam_0,
-// Q1 = X S E Lam^-1/2, Newton-Schulz polish.  A Gram resolves directions down
-// to ~sqrt(tau) of the largest; Householder QR (the reference's tsqr,
-// kernels.py:121-164) resolves down to eps.  To match it, the unresolved
-// remainder R = (I - Q Q^T) X is deflated level by level (unscaled Gram, same
-// threshold relative to its own scale) while ||R||_F exceeds
-// 100 * l * eps_data * ||X||_F.  Whatever is left is numerically null: the
-// missing columns are Gaussian vectors projected out twice and orthonormalised
-// (kernels.py:142-144: "columns of Q remain orthonormal").
-// Returns the detected numerical rank; Q is r x l, fp64, ld r.
+// Level 1 (l <= kCholMaxL): rank-revealing Cholesky QR in column order.
+// Columns whose pivot falls below 1e-12 of their norm lie numerically in the
+// span of the earlier ones and are set aside; the kept ones get a second
+// CholQR pass (orthonormal to rounding).  The reported rank is the
+// reference's |diag R| > l eps ||X||_F cut, since the Cholesky factor of the
+// Gram is the R of an unpivoted QR (kernels.py:155-157).
+// Level 1 (larger l): Gram eigenpairs by Jacobi, keep lam > tau lam_0.
+// Then deflation levels for what is still resolvable in the data's precision
+// and a Gaussian completion of the null directions.
 template <typename T>
 int orth_full(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* Q,
               uint64_t seed, int ns_iters) {
   const double eps_data = sizeof(T) == 8 ? 2.220446049250313e-16 : 1.1920928955078125e-07;
   const double tau = orth_tau(r, l);
-  DBuf<double> E(c, (size_t)l * l), lam(c, l), s(c, l), Tm(c, (size_t)l * l);
-  DBuf<double> scal(c, 4);
-  DBuf<int> drank(c, 1);
   const double drop = 4.0 * l * eps_data;  // the reference's rank cut, kernels.py:155-157
-  // Fast path: Cholesky QR + Newton-Schulz when the scaled Gram is safely
-  // positive definite (every pivot above tau: nothing to reveal).
-  // The reported rank follows the reference's |diag R| > l eps ||X||_F cut.
-  // A healthy fp64 Cholesky (pivots above 1e-12 of the unit diagonal) resolves
-  // every direction Householder QR would, so the second CholQR pass makes Q
-  // orthonormal to rounding.
+  int total = 0, rank = 0;
+  double normx2 = 0.0;
   if (l <= kCholMaxL) {
     set_chol_attrs(c);
-    int rank_ref = l;
-    const double ratio =
-        chol_basis<T>(c, X, r, l, ldx, 0.0, Tm.p, true, drop, l * eps_data, &rank_ref);
-    if (ratio > 1e-12) {
-      DBuf<double> Q1(c, (size_t)r * l);
-      gemm_nn_cm<T, double, double>(c, r, l, l, X, ldx, Tm.p, l, Q1.p, r);
-      chol_basis<double>(c, Q1.p, r, l, r, 0.0, Tm.p, false);
-      gemm_nn_cm<double, double, double>(c, r, l, l, Q1.p, r, Tm.p, l, Q, r);
-      if (ns_iters > 1) ns_refine(c, Q, r, l, 1);
-      return rank_ref;
+    DBuf<int> keep(c, l);
+    DBuf<double> info(c, 3), Tm(c, (size_t)l * l), Tc(c, (size_t)l * l);
+    const CholInfo ci = chol_basis<T>(c, X, r, l, ldx, 0.0, Tm.p, true, drop, l * eps_data,
+                                      1e-12, keep.p, info.p);
+    const int k1 = ci.kept;
+    if (k1 > 0) {
+      const double* Tk = Tm.p;
+      if (k1 < l) {
+        compact_cols_kernel<<<grid_for((int64_t)l * k1), 256, 0, c.stream>>>(
+            Tm.p, l, keep.p, info.p, Tc.p);
+        BRSVD_CHECK_LAUNCH();
+        Tk = Tc.p;
+      }
+      DBuf<double> Q1(c, (size_t)r * k1);
+      gemm_nn_cm<T, double, double>(c, r, k1, l, X, ldx, Tk, l, Q1.p, r);
+      chol_basis<double>(c, Q1.p, r, k1, r, 0.0, Tm.p, false);
+      gemm_nn_cm<double, double, double>(c, r, k1, k1, Q1.p, r, Tm.p, k1, Q, r);
+      if (ns_iters > 1) ns_refine(c, Q, r, k1, 1);
+    }
+    total = k1;
+    rank = std::min(ci.rank_ref, k1);
+    if (total == l) return rank;
+    if (sizeof(T) == 4) {
+      complete_basis(c, Q, r, l, total, seed, ns_iters);
+      return rank;
+    }
+    // ||X||_F^2 for the deflation stop rule
+    DBuf<double> nf(c, 1);
+    DBuf<double> G(c, (size_t)l * l), Wd(c, (size_t)l * l), sd(c, l);
+    gemm_tn_cm<T, T, double>(c, l, l, r, X, ldx, X, ldx, G.p, l);
+    gram_prep_kernel<<<1, 1024, 0, c.stream>>>(G.p, l, sd.p, Wd.p, 0, nf.p, 0.0);
+    BRSVD_CHECK_LAUNCH();
+    readback(c, nf.p, &normx2, sizeof(double));
+  } else {
+    DBuf<double> E(c, (size_t)l * l), lam(c, l), s(c, l), Tm(c, (size_t)l * l);
+    DBuf<double> scal(c, 4);
+    DBuf<int> drank(c, 1);
+    gram_eig<T>(c, X, r, l, ldx, E.p, lam.p, s.p, kJacobiTolOrth, true, scal.p, drop);
+    build_basis_kernel<<<1, 1024, 0, c.stream>>>(E.p, lam.p, s.p, l, tau, 1, Tm.p, drank.p);
+    BRSVD_CHECK_LAUNCH();
+    BRSVD_CUDA(cudaMemcpyAsync(scal.p + 1, drank.p, sizeof(int), cudaMemcpyDeviceToDevice,
+                               c.stream));
+    double hs[2];
+    readback(c, scal.p, hs, sizeof(hs));
+    normx2 = hs[0];
+    std::memcpy(&total, &hs[1], sizeof(int));
+    rank = total;
+    if (total > 0) {
+      gemm_nn_cm<T, double, double>(c, r, total, l, X, ldx, Tm.p, l, Q, r);
+      ns_refine(c, Q, r, total, ns_iters);
     }
   }
-  gram_eig<T>(c, X, r, l, ldx, E.p, lam.p, s.p, kJacobiTolOrth, true, scal.p, drop);
-  build_basis_kernel<<<1, 1024, 0, c.stream>>>(E.p, lam.p, s.p, l, tau, 1, Tm.p,
-                                               drank.p);
-  BRSVD_CHECK_LAUNCH();
-  BRSVD_CUDA(cudaMemcpyAsync(scal.p + 1, drank.p, sizeof(int), cudaMemcpyDeviceToDevice,
-                             c.stream));
-  double hs[2];
-  readback(c, scal.p, hs, sizeof(hs));
-  const double normx2 = hs[0];
-  int rk;
-  std::memcpy(&rk, &hs[1], sizeof(int));
-  int total = rk;
-  if (rk > 0) {
-    gemm_nn_cm<T, double, double>(c, r, rk, l, X, ldx, Tm.p, l, Q, r);
-    ns_refine(c, Q, r, rk, ns_iters);
-  }
-  if (total < l && normx2 > 0.0) {
-    // deflation levels on the unresolved remainder
-    DBuf<double> R(c, (size_t)r * l);
-    copy2d_kernel<T, double><<<grid_for(r * l), 256, 0, c.stream>>>(X, r, l, ldx, R.p, r);
-    BRSVD_CHECK_LAUNCH();
-    const double stop2 = std::pow(drop, 2) * normx2;
-    for (int level = 0; level < 4 && total < l; ++level) {
-      project_out(c, Q, r, total, R.p, l);
-      gram_eig<double>(c, R.p, r, l, r, E.p, lam.p, s.p, kJacobiTolOrth, false, scal.p);
-      build_basis_kernel<<<1, 1024, 0, c.stream>>>(E.p, lam.p, s.p, l, tau, 1, Tm.p,
-                                                   drank.p);
-      BRSVD_CHECK_LAUNCH();
-      BRSVD_CUDA(cudaMemcpyAsync(scal.p + 1, drank.p, sizeof(int),
-                                 cudaMemcpyDeviceToDevice, c.stream));
-      readback(c, scal.p, hs, sizeof(hs));
-      int rk2;
-      std::memcpy(&rk2, &hs[1], sizeof(int));
-      if (!(hs[0] > stop2) || rk2 <= 0) break;
-      rk2 = std::min(rk2, l - total);
-      double* Qn = Q + (int64_t)total * r;
-      gemm_nn_cm<double, double, double>(c, r, rk2, l, R.p, r, Tm.p, l, Qn, r);
-      project_out(c, Q, r, total, Qn, rk2);
-      ns_refine(c, Qn, r, rk2, std::max(ns_iters, 1));
-      total += rk2;
-    }
-  }
-  if (total < l) {
-    const int cnt = l - total;
-    double* W = Q + (int64_t)total * r;
-    gaussian_kernel<double><<<grid_for(r * ((cnt + 1) / 2)), 256, 0, c.stream>>>(
-        W, r, cnt, r, seed, 0x636f6d706c657465ull, 0);
-    BRSVD_CHECK_LAUNCH();
-    project_out(c, Q, r, total, W, cnt);
-    DBuf<double> Wq(c, (size_t)r * cnt);
-    orth_full<double>(c, W, r, cnt, r, Wq.p, seed * 0x9E3779B97F4A7C15ull + 1,
-                      std::max(ns_iters, 1));
-    BRSVD_CUDA(cudaMemcpyAsync(W, Wq.p, sizeof(double) * r * cnt,
-                               cudaMemcpyDeviceToDevice, c.stream));
-    project_out(c, Q, r, total, W, cnt);
-    ns_refine(c, W, r, cnt, 1);
-  }
-  return total;
+  // fp64 data only: for fp32 data the level-1 cut (1e-6 of a column's norm)
+  // is already below the reference's own rank cut (l eps32 ||X||_F).
+  if (sizeof(T) == 8 && total < l && normx2 > 0.0)
+    deflate_levels<T>(c, X, r, l, ldx, Q, total, rank, drop * drop * normx2, tau, ns_iters);
+  complete_basis(c, Q, r, l, total, seed, ns_iters);
+  return rank;
 }
 
 // ---------------------------------------------------------------------------
