@@ -169,14 +169,19 @@ __global__ void trinv_t_kernel(const double* __restrict__ L, int n, int64_t ld,
       const int r = e % nb, k = e / nb;
       Lr[k * kCholNB + r] = L[(int64_t)k * ld + (i0 + r)];
     }
+    // diagonal block staged in shared memory (R doubles as scratch here)
+    for (int e = tid; e < nb * nb; e += nt) {
+      const int r = e % nb, k = e / nb;
+      R[k * kCholNB + r] = L[(int64_t)(i0 + k) * ld + (i0 + r)];
+    }
+    __syncthreads();
     // inverse of the diagonal block by forward substitution, one thread per column
     if (tid < nb) {
       const int c = tid;
       for (int r = 0; r < nb; ++r) {
         double v = (r == c) ? 1.0 : 0.0;
-        for (int k = c; k < r; ++k)
-          v = fma(-L[(int64_t)(i0 + k) * ld + (i0 + r)], Li[c * kCholNB + k], v);
-        Li[c * kCholNB + r] = (r >= c) ? v / L[(int64_t)(i0 + r) * ld + (i0 + r)] : 0.0;
+        for (int k = c; k < r; ++k) v = fma(-R[k * kCholNB + r], Li[c * kCholNB + k], v);
+        Li[c * kCholNB + r] = (r >= c) ? v / R[r * kCholNB + r] : 0.0;
       }
     }
     __syncthreads();
