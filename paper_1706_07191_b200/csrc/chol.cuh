@@ -63,6 +63,7 @@ __global__ void chol_kernel(double* __restrict__ A, int n, int64_t ld, double sh
         if (i < c) continue;
         double acc = 0.0;
         const double* lrow = A + (p0 + i);
+#pragma unroll 8
         for (int k = 0; k < p0; ++k) acc = fma(lrow[(int64_t)k * ld], Lp[k * kCholNB + c], acc);
         P[c * n + i] -= acc;
       }
