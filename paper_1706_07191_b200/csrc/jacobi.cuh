@@ -1,4 +1,4 @@
-// Block one-sided (Hestenes) Jacobi SVD of a small dense fp64 matrix.
+// Block one-sided (Hestenes) Jacobi SVD of a small dense matrix (fp32 or fp64).
 //
 // Replaces the LAPACK calls on the l-by-l problems of the reference:
 // np.linalg.svd(r.T) in small_svd (kernels.py:173-188) and, through the Gram
@@ -18,11 +18,12 @@
 namespace brsvd {
 namespace cg = cooperative_groups;
 
+template <typename R>
 struct JacobiArgs {
-  double* G;
+  R* G;
   int64_t ldg;
   int nrow, ncol;
-  double* V;
+  R* V;
   int64_t ldv;
   int bw, nb;  // block width; number of blocks (even)
   int max_sweeps;
@@ -41,13 +42,12 @@ __device__ __forceinline__ int tourn(int pos, int r, int n) {
 // Rotate columns x, y (length nrow in Gs, length ncol in Vs) so they become
 // orthogonal.  Returns true if a rotation was applied.  Executed by one warp;
 // the three reductions share one butterfly so their shuffles overlap.
-__device__ __forceinline__ bool jacobi_rotate_pair(double* x, double* y,
-                                                   double* vx, double* vy,
-                                                   int nrow, int ncol,
-                                                   double tol2, double floor2, int lane) {
-  double a = 0.0, b = 0.0, g = 0.0;
+template <typename R>
+__device__ __forceinline__ bool jacobi_rotate_pair(R* x, R* y, R* vx, R* vy, int nrow,
+                                                   int ncol, R tol2, R floor2, int lane) {
+  R a = 0, b = 0, g = 0;
   for (int i = lane; i < nrow; i += 32) {
-    const double p = x[i], q = y[i];
+    const R p = x[i], q = y[i];
     a = fma(p, p, a);
     b = fma(q, q, b);
     g = fma(p, q, g);
@@ -62,19 +62,19 @@ __device__ __forceinline__ bool jacobi_rotate_pair(double* x, double* y,
   // converges in the relative sense and carries no information: skip it
   if (!(a > floor2 && b > floor2)) return false;
   if (!(g * g > tol2 * a * b)) return false;
-  const double zeta = (b - a) / (2.0 * g);
-  double t;
-  if (fabs(zeta) > 1e150) {
-    t = 0.5 / zeta;
+  const R zeta = (b - a) / (R(2) * g);
+  R t;
+  if (fabs(zeta) > (sizeof(R) == 8 ? R(1e150) : R(1e18))) {
+    t = R(0.5) / zeta;
   } else {
-    t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+    t = copysign(R(1), zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, R(1))));
   }
-  if (t == 0.0) return false;
-  const double c = 1.0 / sqrt(fma(t, t, 1.0));
-  const double s = c * t;
+  if (t == R(0)) return false;
+  const R c = R(1) / sqrt(fma(t, t, R(1)));
+  const R s = c * t;
   if (nrow == ncol) {
     for (int i = lane; i < nrow; i += 32) {
-      const double p = x[i], q = y[i], pv = vx[i], qv = vy[i];
+      const R p = x[i], q = y[i], pv = vx[i], qv = vy[i];
       x[i] = c * p - s * q;
       y[i] = s * p + c * q;
       vx[i] = c * pv - s * qv;
@@ -82,12 +82,12 @@ __device__ __forceinline__ bool jacobi_rotate_pair(double* x, double* y,
     }
   } else {
     for (int i = lane; i < nrow; i += 32) {
-      const double p = x[i], q = y[i];
+      const R p = x[i], q = y[i];
       x[i] = c * p - s * q;
       y[i] = s * p + c * q;
     }
     for (int i = lane; i < ncol; i += 32) {
-      const double p = vx[i], q = vy[i];
+      const R p = vx[i], q = vy[i];
       vx[i] = c * p - s * q;
       vy[i] = s * p + c * q;
     }
@@ -95,12 +95,14 @@ __device__ __forceinline__ bool jacobi_rotate_pair(double* x, double* y,
   return true;
 }
 
-__global__ void jacobi_block_kernel(JacobiArgs a) {
-  extern __shared__ double jsm[];
+template <typename R>
+__global__ void jacobi_block_kernel(JacobiArgs<R> a) {
+  extern __shared__ __align__(16) unsigned char jsm_raw[];
+  R* jsm = reinterpret_cast<R*>(jsm_raw);
   const int W = 2 * a.bw;
   const int nrow = a.nrow, ncol = a.ncol;
-  double* Gs = jsm;                        // W columns of length nrow
-  double* Vs = jsm + (size_t)W * nrow;     // W columns of length ncol
+  R* Gs = jsm;                        // W columns of length nrow
+  R* Vs = jsm + (size_t)W * nrow;     // W columns of length ncol
   int* cols = reinterpret_cast<int*>(Vs + (size_t)W * ncol);
   __shared__ int s_rot;
   __shared__ int s_stop;
@@ -115,7 +117,7 @@ __global__ void jacobi_block_kernel(JacobiArgs a) {
     double f = 0.0;
     for (int c = warp; c < ncol; c += nwarps)
       for (int i = lane; i < nrow; i += 32) {
-        const double v = a.G[c * a.ldg + i];
+        const double v = (double)a.G[c * a.ldg + i];
         f = fma(v, v, f);
       }
     f = warp_sum(f);
@@ -128,7 +130,7 @@ __global__ void jacobi_block_kernel(JacobiArgs a) {
     }
     __syncthreads();
   }
-  const double floor2 = a.floor_rel * a.floor_rel * s_fro[0];
+  const R floor2 = (R)(a.floor_rel * a.floor_rel * s_fro[0]);
 
   for (int sweep = 0; sweep < a.max_sweeps; ++sweep) {
     for (int round = 0; round < a.nb - 1; ++round) {
@@ -144,9 +146,9 @@ __global__ void jacobi_block_kernel(JacobiArgs a) {
         for (int c = warp; c < W; c += nwarps) {
           const int gc = cols[c];
           for (int i = lane; i < nrow; i += 32)
-            Gs[(size_t)c * nrow + i] = gc >= 0 ? a.G[gc * a.ldg + i] : 0.0;
+            Gs[(size_t)c * nrow + i] = gc >= 0 ? a.G[gc * a.ldg + i] : R(0);
           for (int i = lane; i < ncol; i += 32)
-            Vs[(size_t)c * ncol + i] = gc >= 0 ? a.V[gc * a.ldv + i] : 0.0;
+            Vs[(size_t)c * ncol + i] = gc >= 0 ? a.V[gc * a.ldv + i] : R(0);
         }
         __syncthreads();
         const int inner = single ? 64 : 1;
@@ -174,7 +176,7 @@ __global__ void jacobi_block_kernel(JacobiArgs a) {
               const bool rot = jacobi_rotate_pair(
                   Gs + (size_t)ca * nrow, Gs + (size_t)cb * nrow,
                   Vs + (size_t)ca * ncol, Vs + (size_t)cb * ncol, nrow, ncol,
-                  a.tol * a.tol, floor2, lane);
+                  (R)(a.tol * a.tol), floor2, lane);
               if (rot && lane == 0) atomicAdd(&s_rot, 1);
             }
             __syncthreads();

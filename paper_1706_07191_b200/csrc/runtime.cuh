@@ -175,12 +175,13 @@ inline double jacobi_tol_tight(int nrow) {
 constexpr double kJacobiTolOrth = 1e-8;
 constexpr double kJacobiTolNormalize = 1e-4;
 
-inline int jacobi(Ctx& c, double* G, int nrow, int ncol, int64_t ldg, double* V,
-                  int64_t ldv, double tol, int max_sweeps = 40) {
+template <typename R = double>
+inline int jacobi(Ctx& c, R* G, int nrow, int ncol, int64_t ldg, R* V, int64_t ldv,
+                  double tol, int max_sweeps = 40) {
   BRSVD_REQUIRE(ncol >= 1 && ncol <= 1024 && nrow >= 1, kErrShape,
                 "jacobi: unsupported small-problem shape");
   const size_t budget = std::min<size_t>(c.max_smem_optin, 200 * 1024);
-  const size_t per_col = (size_t)(nrow + ncol) * sizeof(double) + sizeof(int);
+  const size_t per_col = (size_t)(nrow + ncol) * sizeof(R) + sizeof(int);
   int bw_fit = (int)(budget / (2 * per_col));
   BRSVD_REQUIRE(bw_fit >= 1, kErrShape, "jacobi: column too long for shared memory");
   int bw = (ncol + 1) / 2;
@@ -197,14 +198,14 @@ inline int jacobi(Ctx& c, double* G, int nrow, int ncol, int64_t ldg, double* V,
   const size_t smem = (size_t)2 * bw * per_col;
   static bool attr_set = false;
   if (!attr_set) {
-    BRSVD_CUDA(cudaFuncSetAttribute(jacobi_block_kernel,
+    BRSVD_CUDA(cudaFuncSetAttribute(jacobi_block_kernel<R>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)budget));
     attr_set = true;
   }
   DBuf<int> counters(c, (size_t)max_sweeps + 1);
   BRSVD_CUDA(cudaMemsetAsync(counters.p, 0, sizeof(int) * (max_sweeps + 1), c.stream));
-  JacobiArgs args;
+  JacobiArgs<R> args;
   args.G = G;
   args.ldg = ldg;
   args.nrow = nrow;
@@ -214,21 +215,22 @@ inline int jacobi(Ctx& c, double* G, int nrow, int ncol, int64_t ldg, double* V,
   args.bw = bw;
   args.nb = nb;
   args.max_sweeps = max_sweeps;
-  args.tol = std::max(tol, jacobi_tol_tight(nrow));
-  args.floor_rel = 16.0 * nrow * 2.220446049250313e-16;
+  const double eps_r = sizeof(R) == 8 ? 2.220446049250313e-16 : 1.1920928955078125e-07;
+  args.tol = std::max(tol, 8.0 * std::sqrt((double)nrow) * eps_r);
+  args.floor_rel = 16.0 * nrow * eps_r;
   args.rot_count = counters.p;
   args.sweeps_done = counters.p + max_sweeps;
   if (single) {
-    jacobi_block_kernel<<<1, threads, smem, c.stream>>>(args);
+    jacobi_block_kernel<R><<<1, threads, smem, c.stream>>>(args);
     BRSVD_CHECK_LAUNCH();
   } else {
     int grid = nb / 2;
     int per_sm = 0;
     BRSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, jacobi_block_kernel, threads, smem));
+        &per_sm, jacobi_block_kernel<R>, threads, smem));
     grid = std::min(grid, std::max(1, per_sm) * c.num_sms);
     void* kargs[] = {&args};
-    BRSVD_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_block_kernel, dim3(grid),
+    BRSVD_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_block_kernel<R>, dim3(grid),
                                            dim3(threads), kargs, smem, c.stream));
     ++g_brsvd_launches;
   }
@@ -539,8 +541,29 @@ int small_svd_device(Ctx& c, const T* Bt, int64_t n, int l, int64_t ldb, double*
   const int rank = orth_full<T>(c, Bt, n, l, ldb, Qb.p, 0x5eedb5ull, ns_iters);
   // M = Bt^T Qb = R^T
   gemm_tn_cm<T, double, double>(c, l, l, n, Bt, ldb, Qb.p, n, M.p, l);
-  eye_kernel<<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(Vj.p, l);
-  BRSVD_CHECK_LAUNCH();
+  if (l > 64) {
+    // Two-phase Jacobi: sweeps in fp32 (native rsqrt/rcp, half the shuffles
+    // and shared memory) down to ~1e-5 orthogonality, then the fp64 sweeps
+    // start from M V0 with V0 polished to an fp64-orthogonal matrix; the
+    // quadratic convergence leaves only ~2 fp64 sweeps.
+    DBuf<float> M32(c, (size_t)l * l), V32(c, (size_t)l * l);
+    copy2d_kernel<double, float><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(M.p, l, l, l,
+                                                                                M32.p, l);
+    eye_kernel<float><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(V32.p, l);
+    BRSVD_CHECK_LAUNCH();
+    jacobi<float>(c, M32.p, l, l, l, V32.p, l, 1e-5);
+    copy2d_kernel<float, double><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(V32.p, l, l, l,
+                                                                                Vj.p, l);
+    BRSVD_CHECK_LAUNCH();
+    ns_refine(c, Vj.p, l, l, 2);
+    DBuf<double> M1(c, (size_t)l * l);
+    gemm_nn_cm<double, double, double>(c, l, l, l, M.p, l, Vj.p, l, M1.p, l);
+    BRSVD_CUDA(cudaMemcpyAsync(M.p, M1.p, sizeof(double) * l * l, cudaMemcpyDeviceToDevice,
+                               c.stream));
+  } else {
+    eye_kernel<double><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(Vj.p, l);
+    BRSVD_CHECK_LAUNCH();
+  }
   jacobi(c, M.p, l, l, l, Vj.p, l, jacobi_tol_tight(l));
   jacobi_finish(c, M.p, l, l, l, Vj.p, l, sigma, W, l, Zj.p, l);
   complete_null_columns_kernel<<<1, 1024, (size_t)l * sizeof(double), c.stream>>>(

@@ -118,10 +118,11 @@ __global__ void transpose_square_kernel(const double* __restrict__ A, int l,
   }
 }
 
-__global__ void eye_kernel(double* __restrict__ V, int l) {
+template <typename R = double>
+__global__ void eye_kernel(R* __restrict__ V, int l) {
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < l * l;
        idx += gridDim.x * blockDim.x)
-    V[idx] = (idx % l == idx / l) ? 1.0 : 0.0;
+    V[idx] = (idx % l == idx / l) ? R(1) : R(0);
 }
 
 // --- max |x| and finiteness (the overflow guard of rsvd.py:84-91) -------------
