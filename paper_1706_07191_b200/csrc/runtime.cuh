@@ -564,7 +564,10 @@ int small_svd_device(Ctx& c, const T* Bt, int64_t n, int l, int64_t ldb, double*
     eye_kernel<double><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(Vj.p, l);
     BRSVD_CHECK_LAUNCH();
   }
-  jacobi(c, M.p, l, l, l, Vj.p, l, jacobi_tol_tight(l));
+  // fp32 data: singular vectors orthogonal to 1e-7 (the output precision) and
+  // singular values to ~1e-14 relative; fp64 data: tight.
+  const double tol = sizeof(T) == 8 ? jacobi_tol_tight(l) : 1e-7;
+  jacobi(c, M.p, l, l, l, Vj.p, l, tol);
   jacobi_finish(c, M.p, l, l, l, Vj.p, l, sigma, W, l, Zj.p, l);
   complete_null_columns_kernel<<<1, 1024, (size_t)l * sizeof(double), c.stream>>>(
       W, l, l, l, sigma, 16.0 * l * 2.220446049250313e-16);
