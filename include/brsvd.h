@@ -174,6 +174,46 @@ BRSVD_API int brsvd_ialm(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n,
                          double* residuals, double* mus, double* svd_seconds,
                          double* iter_seconds);
 
+/* ---- stage entry points for the row-sharded driver ---------------------
+ * (paper_1706_07191_b200/distributed.py).  Device pointers only; the small
+ * matrices are fp64 column-major.  Each replaces one step of the reference
+ * pipeline when the rows of A are spread over ranks and only the small
+ * products are all-reduced. */
+
+/* G (k1 x k2, fp64) = X^T W (fp64 accumulation); W == NULL means W = X. */
+BRSVD_API int brsvd_gram(brsvd_ctx* ctx, const void* X, int64_t r, int64_t k1, int64_t ldx,
+                         int dtype, const void* W, int64_t k2, int64_t ldw, double* G);
+
+/* Rank-revealing Cholesky basis of an (all-reduced) Gram G (l x l fp64,
+ * overwritten): with s_j = 1/sqrt(G_jj), factor S G S + shift I = L L^T in
+ * column order, dropping columns whose pivot ratio is below drop_ratio
+ * (0: none) and columns with G_jj <= col_drop^2 max G_ii.  T (l x l) receives
+ * S L^-T with the kept columns first; *kept their number; *rank_ref the
+ * |diag R| > rank_tol ||X||_F count (tsqr_factor, kernels.py:155-157). */
+BRSVD_API int brsvd_chol_basis(brsvd_ctx* ctx, double* G, int64_t l, double shift,
+                               double col_drop, double rank_tol, double drop_ratio,
+                               double* T, int32_t* kept, int32_t* rank_ref);
+
+/* out (r x kt) = alpha X T + beta out, X (r x k, dtype), T (k x kt, fp64),
+ * out in out_dtype (fp64 accumulation). */
+BRSVD_API int brsvd_apply(brsvd_ctx* ctx, const void* X, int64_t r, int64_t k, int64_t ldx,
+                          int dtype, const double* T, int64_t kt, void* out, int64_t ldo,
+                          int out_dtype, double alpha, double beta);
+
+/* Power-iteration basis change of a replicated Z (n x l): Zout spans range(Z)
+ * with restored conditioning (shifted Cholesky QR). */
+BRSVD_API int brsvd_normalize(brsvd_ctx* ctx, const void* Z, int64_t n, int64_t l,
+                              int64_t ldz, int dtype, void* Zout, int64_t ldo);
+
+/* Per column of U (r x l): the largest |u_ij| and the global index
+ * row_offset + i of its first occurrence (vals, idx: host arrays of l). */
+BRSVD_API int brsvd_colmax(brsvd_ctx* ctx, const void* U, int64_t r, int64_t l, int64_t ldu,
+                           int dtype, int64_t row_offset, double* vals, int64_t* idx);
+
+/* X[:, j] *= scale[j] (scale: host array of l doubles). */
+BRSVD_API int brsvd_scale_cols(brsvd_ctx* ctx, void* X, int64_t r, int64_t l, int64_t ldx,
+                               int dtype, const double* scale);
+
 #ifdef __cplusplus
 }
 #endif

@@ -24,7 +24,9 @@ EXPORTED = (
     "brsvd_version", "brsvd_last_error", "brsvd_ctx_create", "brsvd_ctx_set_stream",
     "brsvd_ctx_destroy", "brsvd_rsvd", "brsvd_tsqr", "brsvd_small_svd",
     "brsvd_gaussian", "brsvd_profile_begin", "brsvd_profile_end",
-    "brsvd_spectral_norm", "brsvd_ialm", "brsvd_sketch_product",
+    "brsvd_spectral_norm", "brsvd_ialm", "brsvd_sketch_product", "brsvd_gram",
+    "brsvd_chol_basis", "brsvd_apply", "brsvd_normalize", "brsvd_colmax",
+    "brsvd_scale_cols",
 )
 
 
@@ -92,6 +94,14 @@ def _declare(lib):
                                ctypes.POINTER(i32), ctypes.POINTER(i32), vp, vp, vp, vp]
     lib.brsvd_sketch_product.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, vp,
                                          i64, i64, vp, i64]
+    lib.brsvd_gram.argtypes = [vp, vp, i64, i64, i64, c_int, vp, i64, i64, vp]
+    lib.brsvd_chol_basis.argtypes = [vp, vp, i64, dbl, dbl, dbl, dbl, vp,
+                                     ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    lib.brsvd_apply.argtypes = [vp, vp, i64, i64, i64, c_int, vp, i64, vp, i64, c_int, dbl,
+                                dbl]
+    lib.brsvd_normalize.argtypes = [vp, vp, i64, i64, i64, c_int, vp, i64]
+    lib.brsvd_colmax.argtypes = [vp, vp, i64, i64, i64, c_int, i64, vp, vp]
+    lib.brsvd_scale_cols.argtypes = [vp, vp, i64, i64, i64, c_int, vp]
     lib.brsvd_profile_begin.argtypes = [vp]
     lib.brsvd_profile_end.argtypes = [vp, ctypes.POINTER(BrsvdProfile)]
     for name in EXPORTED:

@@ -470,4 +470,143 @@ int brsvd_ialm(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n, int64_t ldm,
   });
 }
 
+int brsvd_gram(brsvd_ctx* ctx, const void* X, int64_t r, int64_t k1, int64_t ldx, int dtype,
+               const void* W, int64_t k2, int64_t ldw, double* G) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && X != nullptr && G != nullptr, kErrArg, "NULL argument");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    esize(dtype);
+    if (W == nullptr) {
+      W = X;
+      k2 = k1;
+      ldw = ldx;
+    }
+    if (dtype == BRSVD_F64)
+      gemm_tn_cm<double, double, double>(c, k1, k2, r, (const double*)X, ldx,
+                                         (const double*)W, ldw, G, k1);
+    else
+      gemm_tn_cm<float, float, double>(c, k1, k2, r, (const float*)X, ldx, (const float*)W,
+                                       ldw, G, k1);
+    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+    return (int)kOk;
+  });
+}
+
+int brsvd_chol_basis(brsvd_ctx* ctx, double* G, int64_t l, double shift, double col_drop,
+                     double rank_tol, double drop_ratio, double* T, int32_t* kept,
+                     int32_t* rank_ref) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && G != nullptr && T != nullptr, kErrArg, "NULL argument");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    BRSVD_REQUIRE(l >= 1 && l <= kCholMaxL, kErrShape, "chol_basis supports 1 <= l <= 384");
+    set_chol_attrs(c);
+    const int li = (int)l;
+    DBuf<double> Wd(c, (size_t)l * l), s(c, l), info(c, 3), Tm(c, (size_t)l * l);
+    DBuf<int> keep(c, l);
+    gram_prep_kernel<<<1, 1024, 0, c.stream>>>(G, li, s.p, Wd.p, 1, nullptr, col_drop);
+    BRSVD_CHECK_LAUNCH();
+    chol_kernel<<<1, 1024, chol_smem(li), c.stream>>>(G, li, li, shift, info.p,
+                                                      rank_tol > 0.0 ? s.p : nullptr,
+                                                      rank_tol, drop_ratio, keep.p);
+    BRSVD_CHECK_LAUNCH();
+    trinv_t_kernel<<<1, 1024, trinv_smem(li), c.stream>>>(G, li, li, s.p, Wd.p, Tm.p);
+    BRSVD_CHECK_LAUNCH();
+    BRSVD_CUDA(cudaMemsetAsync(T, 0, sizeof(double) * l * l, c.stream));
+    compact_cols_kernel<<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(Tm.p, li, keep.p,
+                                                                        info.p, T);
+    BRSVD_CHECK_LAUNCH();
+    double h[3];
+    readback(c, info.p, h, sizeof(h));
+    if (kept) *kept = (int32_t)h[2];
+    if (rank_ref) *rank_ref = (int32_t)h[1];
+    return (int)kOk;
+  });
+}
+
+int brsvd_apply(brsvd_ctx* ctx, const void* X, int64_t r, int64_t k, int64_t ldx, int dtype,
+                const double* T, int64_t kt, void* out, int64_t ldo, int out_dtype,
+                double alpha, double beta) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && X != nullptr && T != nullptr && out != nullptr, kErrArg,
+                  "NULL argument");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    esize(dtype);
+    esize(out_dtype);
+#define BRSVD_APPLY(TX, TO)                                                                \
+  gemm_nn_cm<TX, double, TO>(c, r, kt, k, (const TX*)X, ldx, T, k, (TO*)out, ldo, alpha, \
+                             beta, beta != 0.0 ? (const TO*)out : nullptr, ldo)
+    if (dtype == BRSVD_F64 && out_dtype == BRSVD_F64) BRSVD_APPLY(double, double);
+    else if (dtype == BRSVD_F64) BRSVD_APPLY(double, float);
+    else if (out_dtype == BRSVD_F64) BRSVD_APPLY(float, double);
+    else BRSVD_APPLY(float, float);
+#undef BRSVD_APPLY
+    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+    return (int)kOk;
+  });
+}
+
+int brsvd_normalize(brsvd_ctx* ctx, const void* Z, int64_t n, int64_t l, int64_t ldz,
+                    int dtype, void* Zout, int64_t ldo) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && Z != nullptr && Zout != nullptr, kErrArg, "NULL argument");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    esize(dtype);
+    if (dtype == BRSVD_F64)
+      normalize_sketch<double>(c, (const double*)Z, n, (int)l, ldz, (double*)Zout, ldo);
+    else
+      normalize_sketch<float>(c, (const float*)Z, n, (int)l, ldz, (float*)Zout, ldo);
+    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+    return (int)kOk;
+  });
+}
+
+int brsvd_colmax(brsvd_ctx* ctx, const void* U, int64_t r, int64_t l, int64_t ldu, int dtype,
+                 int64_t row_offset, double* vals, int64_t* idx) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && U != nullptr && vals && idx, kErrArg, "NULL argument");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    esize(dtype);
+    DBuf<double> dv(c, l);
+    DBuf<int64_t> di(c, l);
+    if (dtype == BRSVD_F64)
+      colmax_kernel<double><<<(unsigned)l, 256, 0, c.stream>>>((const double*)U, r, ldu,
+                                                               row_offset, dv.p, di.p);
+    else
+      colmax_kernel<float><<<(unsigned)l, 256, 0, c.stream>>>((const float*)U, r, ldu,
+                                                              row_offset, dv.p, di.p);
+    BRSVD_CHECK_LAUNCH();
+    BRSVD_CUDA(cudaMemcpyAsync(vals, dv.p, sizeof(double) * l, cudaMemcpyDeviceToHost, c.stream));
+    BRSVD_CUDA(cudaMemcpyAsync(idx, di.p, sizeof(int64_t) * l, cudaMemcpyDeviceToHost, c.stream));
+    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+    return (int)kOk;
+  });
+}
+
+int brsvd_scale_cols(brsvd_ctx* ctx, void* X, int64_t r, int64_t l, int64_t ldx, int dtype,
+                     const double* scale) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && X != nullptr && scale != nullptr, kErrArg, "NULL argument");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    esize(dtype);
+    DBuf<double> ds(c, l);
+    BRSVD_CUDA(cudaMemcpyAsync(ds.p, scale, sizeof(double) * l, cudaMemcpyHostToDevice,
+                               c.stream));
+    if (dtype == BRSVD_F64)
+      scale_cols_by_kernel<double, double><<<grid_for(r * l), 256, 0, c.stream>>>(
+          (double*)X, r, l, ldx, ds.p);
+    else
+      scale_cols_by_kernel<float, double><<<grid_for(r * l), 256, 0, c.stream>>>(
+          (float*)X, r, l, ldx, ds.p);
+    BRSVD_CHECK_LAUNCH();
+    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+    return (int)kOk;
+  });
+}
+
 }  // extern "C"

@@ -77,13 +77,15 @@ __global__ void chol_kernel(double* __restrict__ A, int n, int64_t ld, double sh
         const double dg = diag0[p0 + c];
         // a zero (dropped) column or a NaN pivot counts as a breakdown
         const double ratio = (dg > 0.0 && piv == piv) ? piv / dg : -1.0;
-        if (drop_ratio > 0.0 && !(ratio > drop_ratio)) {
-          s_d = 0.0;                       // dropped: zero column, unit diagonal
+        // dropped (rank-revealing mode) or broken down (non-positive pivot):
+        // zero column below a unit diagonal, so L stays finite and invertible
+        if ((drop_ratio > 0.0 && !(ratio > drop_ratio)) || !(piv > 0.0)) {
+          if (ratio < s_minr) s_minr = ratio;
+          s_d = 0.0;
           P[c * n + c] = 1.0;
           dropped[p0 + c] = 1;
         } else {
           if (ratio < s_minr) s_minr = ratio;
-          if (!(piv > 0.0)) piv = 1e-300;
           s_d = sqrt(piv);
           P[c * n + c] = s_d;
           dropped[p0 + c] = 0;

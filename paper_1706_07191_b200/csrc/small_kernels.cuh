@@ -184,6 +184,49 @@ __global__ void colsign_kernel(const T* __restrict__ U, int64_t rows,
   }
 }
 
+// Per column: max |U[i, j]| and the first row index attaining it (global
+// index = row_offset + i).  One block per column.
+template <typename T>
+__global__ void colmax_kernel(const T* __restrict__ U, int64_t rows, int64_t ldu,
+                              int64_t row_offset, double* __restrict__ vals,
+                              int64_t* __restrict__ idx) {
+  const int j = blockIdx.x;
+  double best = -1.0;
+  int64_t bidx = 0;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+    const double v = fabs((double)U[i + j * ldu]);
+    if (v > best) { best = v; bidx = i; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
+  }
+  __shared__ double sb[32];
+  __shared__ int64_t si[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { sb[warp] = best; si[warp] = bidx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (sb[w] > best || (sb[w] == best && si[w] < bidx)) { best = sb[w]; bidx = si[w]; }
+    vals[j] = best;
+    idx[j] = row_offset + bidx;
+  }
+}
+
+template <typename T, typename S>
+__global__ void scale_cols_by_kernel(T* __restrict__ X, int64_t rows, int64_t cols,
+                                     int64_t ld, const S* __restrict__ scale) {
+  const int64_t total = rows * cols;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = id % rows, j = id / rows;
+    X[i + j * ld] = (T)((S)X[i + j * ld] * scale[j]);
+  }
+}
+
 template <typename T>
 __global__ void scale_cols_kernel(T* __restrict__ X, int64_t rows, int64_t cols,
                                   int64_t ld, const T* __restrict__ sign) {

@@ -1,0 +1,334 @@
+"""Row-sharded randomized SVD over several GPUs (BASELINE config 4).
+
+The rows of A are split in contiguous panels, one per rank:
+rank g holds A[r0:r1, :], its rows of the sample Y, of the basis Q and of U.
+The global power iteration of ``rsvd_incore`` (rsvd.py:126-141) /
+``rsvd_naive_ooc`` (rsvd.py:218-284) then needs exactly these exchanges:
+
+  * Z = sum_g A_g^T Y_g            (n x l)   all-reduce, once per power pass
+  * G = sum_g Y_g^T Y_g            (l x l)   all-reduce, per CholQR pass
+  * C = sum_g Q_g^T W_g            (k x c)   all-reduce, completion (rare)
+  * B^T = sum_g A_g^T Q_g          (n x l)   all-reduce, once
+  * column argmax of U             (l)       all-gather, for the signs
+
+Everything else is local (the A-streaming products) or replicated and
+bit-identical on every rank (the l x l factorisations, the small SVD), so U
+stays row-sharded and sigma, Vt are replicated.  The stage operations come
+from an ``ops`` object: ``GpuOps`` calls the C ABI (tcgen05 products, fp64
+Gram/Cholesky kernels, Jacobi small SVD) on the local GPU; the tests run the
+same driver with numpy operations over the gloo backend.
+"""
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _lib
+from .kernels import SvdFactors
+
+_EPS = {np.dtype(np.float64): 2.220446049250313e-16,
+        np.dtype(np.float32): 1.1920928955078125e-07}
+
+
+# ---------------------------------------------------------------------------
+class TorchComm:
+    """Collectives over torch.distributed (NCCL for CUDA tensors; host
+    round-trip for gloo).  World size 1 needs no process group."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.active = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if self.active else 1
+        self.rank = dist.get_rank(group) if self.active else 0
+        self.backend = dist.get_backend(group) if self.active else None
+
+    def _as_tensor(self, x):
+        """A contiguous tensor sharing x's memory (column-major views are
+        transposed, which leaves the element-wise reductions unchanged)."""
+        import torch
+        if isinstance(x, np.ndarray):
+            return torch.from_numpy(x if x.flags.c_contiguous else x.T)
+        return x if x.is_contiguous() else x.t()
+
+    def allreduce_sum(self, x):
+        if self.world == 1:
+            return x
+        t = self._as_tensor(x)
+        if t.is_cuda and self.backend != "nccl":
+            h = t.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.all_reduce(t, group=self.group)
+        return x
+
+    def allreduce_max(self, value):
+        if self.world == 1:
+            return value
+        import torch
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        t = torch.tensor([value], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+    def allgather_obj(self, obj):
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+
+# ---------------------------------------------------------------------------
+def _cm_empty(rows, cols, dtype, device):
+    """Column-major (rows x cols) torch tensor (storage = (cols, rows))."""
+    import torch
+    return torch.empty((cols, rows), dtype=dtype, device=device).t()
+
+
+def _ld(t):
+    return max(t.stride(1), 1)
+
+
+def _code(t):
+    import torch
+    return _lib.F64 if t.dtype == torch.float64 else _lib.F32
+
+
+def _vp(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class GpuOps:
+    """Local stage operations on torch CUDA tensors through the C ABI.
+
+    Tall-skinny matrices are column-major torch views (shape (rows, cols),
+    stride (1, rows)); A may be row- or column-major.
+    """
+
+    def __init__(self, device=None):
+        import torch
+        from ._arrays import torch_stream_ptr  # noqa: F401
+        self.torch = torch
+        self.device = torch.device("cuda", torch.cuda.current_device()
+                                   if device is None else device)
+        self.ctx = _lib.context(self.device.index)
+        self.lib = _lib.load_library()
+
+    def _sync_stream(self):
+        self.ctx.set_stream(self.torch.cuda.current_stream(self.device).cuda_stream)
+
+    def asarray(self, x, dtype):
+        t = self.torch.as_tensor(np.asarray(x) if not hasattr(x, "data_ptr") else x,
+                                 device=self.device, dtype=dtype)
+        out = _cm_empty(t.shape[0], t.shape[1], dtype, self.device)
+        out.copy_(t)
+        return out
+
+    def dtype_of(self, A):
+        return A.dtype
+
+    def product(self, A, X, trans):
+        from ._arrays import DeviceMatrix
+        self._sync_stream()
+        mat = DeviceMatrix(A)
+        m, n = mat.shape
+        rows = n if trans else m
+        l = X.shape[1]
+        C = _cm_empty(rows, l, A.dtype, self.device)
+        _lib.check(self.lib.brsvd_sketch_product(
+            self.ctx.handle, mat.ptr, m, n, mat.ld, mat.code, mat.layout, int(trans),
+            _vp(X), _ld(X), l, _vp(C), rows))
+        return C
+
+    def gram(self, X, W=None):
+        self._sync_stream()
+        k1 = X.shape[1]
+        k2 = W.shape[1] if W is not None else k1
+        G = _cm_empty(k1, k2, self.torch.float64, self.device)
+        _lib.check(self.lib.brsvd_gram(
+            self.ctx.handle, _vp(X), X.shape[0], k1, _ld(X), _code(X),
+            _vp(W) if W is not None else None, k2, _ld(W) if W is not None else 1, _vp(G)))
+        return G
+
+    def chol_basis(self, G, shift=0.0, col_drop=0.0, rank_tol=0.0, drop_ratio=0.0):
+        self._sync_stream()
+        l = G.shape[0]
+        Gc = G.clone()
+        T = _cm_empty(l, l, self.torch.float64, self.device)
+        kept, rank = ctypes.c_int32(), ctypes.c_int32()
+        _lib.check(self.lib.brsvd_chol_basis(
+            self.ctx.handle, _vp(Gc), l, ctypes.c_double(shift), ctypes.c_double(col_drop),
+            ctypes.c_double(rank_tol), ctypes.c_double(drop_ratio), _vp(T),
+            ctypes.byref(kept), ctypes.byref(rank)))
+        return T, kept.value, rank.value
+
+    def apply(self, X, T, out_dtype, out=None, alpha=1.0, beta=0.0):
+        self._sync_stream()
+        r, k = X.shape
+        kt = T.shape[1]
+        if out is None:
+            out = _cm_empty(r, kt, out_dtype, self.device)
+        Tc = T if T.stride(0) == 1 and T.stride(1) == k else T.t().contiguous().t()
+        _lib.check(self.lib.brsvd_apply(
+            self.ctx.handle, _vp(X), r, k, _ld(X), _code(X), _vp(Tc), kt, _vp(out), _ld(out),
+            _code(out), ctypes.c_double(alpha), ctypes.c_double(beta)))
+        return out
+
+    def normalize(self, Z):
+        self._sync_stream()
+        out = _cm_empty(Z.shape[0], Z.shape[1], Z.dtype, self.device)
+        _lib.check(self.lib.brsvd_normalize(self.ctx.handle, _vp(Z), Z.shape[0], Z.shape[1],
+                                            _ld(Z), _code(Z), _vp(out), _ld(out)))
+        return out
+
+    def gaussian(self, rows, cols, seed, stream, row_offset, dtype):
+        self._sync_stream()
+        out = _cm_empty(rows, cols, dtype, self.device)
+        _lib.check(self.lib.brsvd_gaussian(
+            self.ctx.handle, _vp(out), rows, cols, rows, _code(out),
+            ctypes.c_uint64(seed & (2 ** 64 - 1)), ctypes.c_uint64(stream & (2 ** 64 - 1)),
+            int(row_offset)))
+        return out
+
+    def small_svd(self, Bt):
+        self._sync_stream()
+        n, l = Bt.shape
+        W = _cm_empty(l, l, Bt.dtype, self.device)
+        sigma = self.torch.empty(l, dtype=Bt.dtype, device=self.device)
+        Vt = self.torch.empty((l, n), dtype=Bt.dtype, device=self.device)
+        rank = ctypes.c_int32()
+        _lib.check(self.lib.brsvd_small_svd(
+            self.ctx.handle, _vp(Bt), n, l, _ld(Bt), _code(Bt), _lib.DEVICE, _vp(W),
+            _vp(sigma), _vp(Vt), ctypes.byref(rank)))
+        return W.double(), sigma, Vt, rank.value
+
+    def colmax(self, U, row_offset):
+        self._sync_stream()
+        l = U.shape[1]
+        vals = np.empty(l, dtype=np.float64)
+        idx = np.empty(l, dtype=np.int64)
+        _lib.check(self.lib.brsvd_colmax(self.ctx.handle, _vp(U), U.shape[0], l, _ld(U),
+                                         _code(U), int(row_offset),
+                                         ctypes.c_void_p(vals.ctypes.data),
+                                         ctypes.c_void_p(idx.ctypes.data)))
+        return vals, idx
+
+    def entry(self, U, i, j):
+        return float(U[i, j].item())
+
+    def scale_cols(self, X, scale):
+        self._sync_stream()
+        s = np.ascontiguousarray(scale, dtype=np.float64)
+        _lib.check(self.lib.brsvd_scale_cols(self.ctx.handle, _vp(X), X.shape[0], X.shape[1],
+                                             _ld(X), _code(X),
+                                             ctypes.c_void_p(s.ctypes.data)))
+        return X
+
+    def hstack(self, a, b):
+        out = _cm_empty(a.shape[0], a.shape[1] + b.shape[1], a.dtype, self.device)
+        out[:, :a.shape[1]] = a
+        out[:, a.shape[1]:] = b
+        return out
+
+    def cols(self, X, k):
+        return X[:, :k]
+
+    def cast(self, X, dtype):
+        out = _cm_empty(X.shape[0], X.shape[1], dtype, self.device)
+        out.copy_(X)
+        return out
+
+
+# ---------------------------------------------------------------------------
+def _orth_sharded(Y, ops, comm, eps_data, row_offset, m_total, seed):
+    """Rank-revealing CholQR2 of the row-sharded Y (runtime.cuh orth_full,
+    level 1 + completion) with all-reduced Grams."""
+    l = Y.shape[1]
+    G = comm.allreduce_sum(ops.gram(Y))
+    T, kept, rank_ref = ops.chol_basis(G, 0.0, 4.0 * l * eps_data, l * eps_data, 1e-12)
+    f64 = ops.torch.float64 if hasattr(ops, "torch") else np.float64
+    Q = None
+    if kept > 0:
+        Q1 = ops.apply(Y, ops.cols(T, kept), f64)
+        G2 = comm.allreduce_sum(ops.gram(Q1))
+        T2, _, _ = ops.chol_basis(G2)
+        Q = ops.apply(Q1, ops.cols(T2, kept), f64)
+    if kept < l:
+        cnt = l - kept
+        W = ops.gaussian(Y.shape[0], cnt, seed, 0x636f6d706c657465, row_offset, f64)
+        if Q is not None:
+            for _ in range(2):
+                C = comm.allreduce_sum(ops.gram(Q, W))
+                W = ops.apply(Q, C, f64, out=W, alpha=-1.0, beta=1.0)
+        for _ in range(2):
+            Gw = comm.allreduce_sum(ops.gram(W))
+            Tw, _, _ = ops.chol_basis(Gw)
+            W = ops.apply(W, Tw, f64)
+        Q = W if Q is None else ops.hstack(Q, W)
+    return Q, min(rank_ref, kept)
+
+
+def rsvd_sharded(A_local, cfg, row_offset, m_total, comm=None, ops=None, omega=None):
+    """Randomized SVD of the row-sharded matrix whose rows
+    [row_offset, row_offset + A_local.shape[0]) this rank holds.
+
+    Returns (factors, info): factors.U holds this rank's rows of U;
+    sigma and Vt are replicated.  Same semantics (global power iteration) and
+    validation as rsvd_incore (rsvd.py:126-141).
+    """
+    comm = comm or TorchComm()
+    ops = ops or GpuOps()
+    row_offset, m_total = int(row_offset), int(m_total)
+    m_loc, n = A_local.shape
+    cfg.validate(m_total, n)
+    k, p, q = cfg.target_rank, cfg.oversampling, cfg.power_exponent
+    l = k + p
+    dtype = ops.dtype_of(A_local)
+    npdt = np.dtype(np.float64) if str(dtype).endswith("float64") else np.dtype(np.float32)
+    eps_data = _EPS[npdt]
+    seed = int(cfg.master_seed)
+    X = ops.asarray(omega, dtype) if omega is not None else ops.gaussian(n, l, seed, 0, 0, dtype)
+    Y = ops.product(A_local, X, False)
+    vals, _ = ops.colmax(Y, row_offset)
+    bad = not np.all(np.isfinite(vals)) or np.any(vals < 0)
+    peak0 = comm.allreduce_max(float(np.max(vals)) if vals.size else 0.0)
+    bad = comm.allreduce_max(1.0 if bad else 0.0) > 0
+    if bad:
+        raise FloatingPointError("sample matrix is not finite; the overflow guard fires")
+    for _ in range(q):
+        Z = comm.allreduce_sum(ops.product(A_local, Y, True))
+        Y = ops.product(A_local, ops.normalize(Z), False)
+    Q, rank_y = _orth_sharded(Y, ops, comm, eps_data, row_offset, m_total, seed ^ 0x7153)
+    Qd = ops.cast(Q, dtype)
+    Bt = comm.allreduce_sum(ops.product(A_local, Qd, True))
+    W, sigma, Vt, rank_b = ops.small_svd(Bt)
+    U = ops.apply(Q, W, dtype)
+    # _fix_signs (rsvd.py:105-115) over the global rows
+    vals, idx = ops.colmax(U, row_offset)
+    entries = []
+    for j in range(l):
+        i_loc = int(idx[j]) - row_offset
+        entries.append((float(vals[j]), int(idx[j]), ops.entry(U, i_loc, j)))
+    gathered = comm.allgather_obj(entries)
+    signs = np.ones(l)
+    for j in range(l):
+        best = None
+        for ent in gathered:
+            v, i, e = ent[j]
+            if best is None or v > best[0] or (v == best[0] and i < best[1]):
+                best = (v, i, e)
+        signs[j] = -1.0 if best[2] < 0 else 1.0
+    ops.scale_cols(U, signs)
+    ops.scale_cols(Vt.t() if hasattr(Vt, "t") and not isinstance(Vt, np.ndarray) else Vt.T,
+                   signs)
+    s0 = float(sigma[0])
+    lim = math.log10(0.01 * np.finfo(npdt).max)
+    log_peak = (math.log10(peak0) + 2 * q * math.log10(s0)) if peak0 > 0 and s0 > 0 else -400.0
+    if log_peak > lim:
+        raise FloatingPointError("sample matrix magnitude exceeds the overflow guard")
+    info = {"rank_y": rank_y, "rank_b": rank_b, "max_abs_y0": peak0, "log10_peak": log_peak}
+    return SvdFactors(U=U, sigma=sigma, Vt=Vt, target_rank=k, effective_l=l), info

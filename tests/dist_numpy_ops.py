@@ -1,0 +1,99 @@
+"""numpy stage operations for the row-sharded driver (TEST INFRASTRUCTURE).
+
+Same interface as paper_1706_07191_b200.distributed.GpuOps, so the gloo tests
+exercise the driver's sharding and collective logic on CPU; each operation
+mirrors the semantics of the corresponding C ABI entry point.
+"""
+
+import numpy as np
+
+from oracle import ref_cpu
+
+F64 = np.float64
+
+
+class NumpyOps:
+    def dtype_of(self, A):
+        return A.dtype
+
+    def asarray(self, x, dtype):
+        return np.asfortranarray(np.asarray(x), dtype=dtype)
+
+    def product(self, A, X, trans):
+        return np.asfortranarray((A.T if trans else A) @ X)
+
+    def gram(self, X, W=None):
+        W = X if W is None else W
+        return np.asfortranarray(X.astype(F64).T @ W.astype(F64))
+
+    def chol_basis(self, G, shift=0.0, col_drop=0.0, rank_tol=0.0, drop_ratio=0.0):
+        """brsvd_chol_basis: scaled, column-order rank-revealing Cholesky."""
+        G = np.array(G, dtype=F64)
+        l = G.shape[0]
+        d = np.diag(G).copy()
+        dmax = d.max() if l else 0.0
+        s = np.where((d > col_drop * col_drop * dmax) & (d > 0), 1.0 / np.sqrt(np.maximum(d, 1e-300)), 0.0)
+        Gs = s[:, None] * (0.5 * (G + G.T)) * s[None, :] + shift * np.eye(l)
+        diag0 = np.diag(Gs).copy()
+        L = np.zeros((l, l))
+        kept = []
+        for j in range(l):
+            piv = Gs[j, j] - L[j, :j] @ L[j, :j]
+            ratio = piv / diag0[j] if diag0[j] > 0 and piv == piv else -1.0
+            if (drop_ratio > 0 and not ratio > drop_ratio) or not piv > 0:
+                L[j, j] = 1.0
+                continue
+            dj = np.sqrt(piv)
+            L[j, j] = dj
+            L[j + 1:, j] = (Gs[j + 1:, j] - L[j + 1:, :j] @ L[j, :j]) / dj
+            kept.append(j)
+        T = s[:, None] * np.linalg.inv(L).T
+        out = np.zeros((l, l))
+        out[:, :len(kept)] = T[:, kept]
+        colnorm = np.where(s > 0, 1.0 / np.where(s > 0, s, 1.0), 0.0)
+        cut = rank_tol * np.sqrt(np.sum(colnorm ** 2))
+        rank = sum(1 for j in kept if s[j] > 0 and L[j, j] * colnorm[j] > cut) if rank_tol > 0 else 0
+        return np.asfortranarray(out), len(kept), rank
+
+    def apply(self, X, T, out_dtype, out=None, alpha=1.0, beta=0.0):
+        r = alpha * (X.astype(F64) @ np.asarray(T, dtype=F64))
+        if out is not None:
+            if beta != 0.0:
+                r = r + beta * out.astype(F64)
+            out[...] = r.astype(out.dtype)
+            return out
+        return np.asfortranarray(r.astype(out_dtype))
+
+    def normalize(self, Z):
+        l = Z.shape[1]
+        T, _, _ = self.chol_basis(self.gram(Z), shift=16.0 * l * 2.220446049250313e-16)
+        return self.apply(Z, T, Z.dtype)
+
+    def gaussian(self, rows, cols, seed, stream, row_offset, dtype):
+        return ref_cpu.normal_sketch(int(rows), int(cols), seed % (2 ** 63), stream % (2 ** 63),
+                                     int(row_offset), dtype)
+
+    def small_svd(self, Bt):
+        w, s, vt, rank = ref_cpu.core_svd(np.ascontiguousarray(Bt.T))
+        return w.astype(F64), s, np.ascontiguousarray(vt), rank
+
+    def colmax(self, U, row_offset):
+        idx = np.argmax(np.abs(U), axis=0)
+        vals = np.abs(U[idx, np.arange(U.shape[1])]).astype(F64)
+        return vals, idx.astype(np.int64) + row_offset
+
+    def entry(self, U, i, j):
+        return float(U[i, j])
+
+    def scale_cols(self, X, scale):
+        X *= np.asarray(scale, dtype=X.dtype)[None, :]
+        return X
+
+    def hstack(self, a, b):
+        return np.asfortranarray(np.hstack([a, b]))
+
+    def cols(self, X, k):
+        return X[:, :k]
+
+    def cast(self, X, dtype):
+        return np.asfortranarray(X.astype(dtype))

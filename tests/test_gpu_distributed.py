@@ -1,0 +1,66 @@
+"""Row-sharded driver on the GPU: two ranks sharing cuda:0 over gloo (the
+box has one GPU), GPU stage operations through the C ABI, against the
+single-GPU pipeline with the same sketch."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, dtype_name, out_dir):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch
+    import torch.distributed as dist
+    from oracle import ref_cpu
+    from paper_1706_07191_b200 import RankDeficiencyWarning, SketchConfig
+    from paper_1706_07191_b200.distributed import GpuOps, TorchComm, rsvd_sharded
+    import warnings
+    warnings.simplefilter("ignore", RankDeficiencyWarning)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    dtype = np.float64 if dtype_name == "f64" else np.float32
+    A = ref_cpu.lowrank_plus_noise(3000, 800, 20, 1e-3, seed=9, dtype=dtype)
+    omega = ref_cpu.normal_sketch(800, 30, 0, dtype=dtype)
+    bounds = [0, 1500, 3000]
+    r0, r1 = bounds[rank], bounds[rank + 1]
+    A_loc = torch.as_tensor(A[r0:r1], device="cuda")
+    f, info = rsvd_sharded(A_loc, SketchConfig(20, 10, 2), r0, 3000, comm=TorchComm(),
+                           ops=GpuOps(0), omega=omega)
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), U=f.U.cpu().numpy(),
+             sigma=f.sigma.cpu().numpy(), Vt=f.Vt.cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dtype_name", ["f64", "f32"])
+def test_two_shards_match_single_gpu(dtype_name, tmp_path):
+    import torch.multiprocessing as mp
+    from oracle import ref_cpu
+    from paper_1706_07191_b200 import SketchConfig, rsvd_incore
+    mp.start_processes(_worker, args=(2, _free_port(), dtype_name, str(tmp_path)), nprocs=2,
+                       join=True, start_method="spawn")
+    parts = [np.load(tmp_path / f"r{r}.npz") for r in range(2)]
+    U = np.vstack([p["U"] for p in parts])
+    dtype = np.float64 if dtype_name == "f64" else np.float32
+    A = ref_cpu.lowrank_plus_noise(3000, 800, 20, 1e-3, seed=9, dtype=dtype)
+    omega = ref_cpu.normal_sketch(800, 30, 0, dtype=dtype)
+    f = rsvd_incore(A, SketchConfig(20, 10, 2), omega=omega)
+    fp64 = dtype == np.float64
+    np.testing.assert_allclose(parts[0]["sigma"][:20], f.sigma[:20],
+                               rtol=1e-10 if fp64 else 1e-5)
+    np.testing.assert_allclose(U[:, :20], f.U[:, :20], atol=1e-8 if fp64 else 1e-3)
+    np.testing.assert_allclose(parts[0]["Vt"][:20], f.Vt[:20], atol=1e-8 if fp64 else 1e-3)
+    np.testing.assert_array_equal(parts[0]["sigma"], parts[1]["sigma"])
