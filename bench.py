@@ -21,10 +21,10 @@ over A (m*n*4 bytes each) per decomposition / time, in GB/s, whole job.
             reference's numpy path) on a row sample of the same matrix, all
             host cores.
 
-With N > 1 each rank runs its own decomposition ("replicas", scaling weak):
-the in-core configuration has no cross-GPU exchange.  The row-sharded
-configuration with the NCCL all-reduce of Z is BASELINE config 4 (see
-DESIGN.md).
+With N > 1 (torchrun) the matrix is row-sharded over the ranks (BASELINE
+config 4 structure, weak scaling: every rank holds a 32768 x 32768 panel of
+an (N*32768) x 32768 rank-256 + noise matrix); the power passes all-reduce
+Z (n x l) over NCCL (paper_1706_07191_b200/distributed.py).
 """
 
 import argparse
@@ -92,19 +92,27 @@ def a_stream_gbs(seconds, m=M, n=N_COLS, elsize=4, passes=PASSES):
     return passes * m * n * elsize / seconds / 1e9
 
 
-def make_matrix(device, seed=1234):
-    """A = L R + 1e-3 N on the device (synthetic)."""
+def make_matrix(device, seed=1234, shard=0):
+    """A = L R + 1e-3 N on the device (synthetic).
+
+    ``shard`` selects a row panel of the multi-GPU matrix: the right factor R
+    is shared (same seed on every rank), the left factor rows and the noise
+    are per panel, so the panels stack to one rank-256 + noise matrix."""
     import torch
     g = torch.Generator(device=device).manual_seed(seed)
     prev = torch.backends.cuda.matmul.allow_tf32
     torch.backends.cuda.matmul.allow_tf32 = False
     L = torch.randn(M, RANK, generator=g, device=device, dtype=torch.float32)
     R = torch.randn(RANK, N_COLS, generator=g, device=device, dtype=torch.float32)
+    if shard:
+        gs = torch.Generator(device=device).manual_seed(seed + 7919 * shard)
+        L = torch.randn(M, RANK, generator=gs, device=device, dtype=torch.float32)
     A = L @ R
     torch.backends.cuda.matmul.allow_tf32 = prev
-    A.add_(torch.randn(M, N_COLS, generator=g, device=device, dtype=torch.float32),
-           alpha=NOISE)
-    del L, R
+    noise = torch.randn(M, N_COLS, generator=gs if shard else g, device=device,
+                        dtype=torch.float32)
+    A.add_(noise, alpha=NOISE)
+    del L, R, noise
     torch.cuda.synchronize(device)
     return A
 
@@ -250,12 +258,25 @@ def run_ours(args, world, rank, local):
     torch.cuda.set_device(dev)
     os.environ["BRSVD_DEVICE"] = str(local)
     cfg = SketchConfig(target_rank=K, oversampling=P, power_exponent=Q, master_seed=0)
-    A = make_matrix(dev)
+    A = make_matrix(dev, shard=rank)
     stream = torch.cuda.current_stream(dev)
+    sharded = world > 1
+    if sharded:
+        # config 4: A row-sharded over the ranks (weak scaling: each rank keeps
+        # its 32768-row panel), NCCL all-reduce of Z / Grams / B^T.
+        from paper_1706_07191_b200.distributed import GpuOps, TorchComm, rsvd_sharded
+        comm, ops = TorchComm(), GpuOps(local)
+
+        def one_step(a):
+            f, _ = rsvd_sharded(a, cfg, rank * M, world * M, comm=comm, ops=ops)
+            return f
+    else:
+        def one_step(a):
+            return run_rsvd(a, cfg, warn=False)
 
     # warm-up
     for _ in range(args.warmup):
-        run_rsvd(A, cfg, warn=False)
+        one_step(A)
     torch.cuda.synchronize(dev)
 
     # timed: device-resident A
@@ -265,7 +286,7 @@ def run_ours(args, world, rank, local):
     with ClockSampler(local) as clk, _lib.profile(local) as prof:
         start.record(stream)
         for _ in range(args.steps):
-            run = run_rsvd(A, cfg, warn=False)
+            run = one_step(A)
         stop.record(stream)
         torch.cuda.synchronize(dev)
     barrier(world)
@@ -273,7 +294,8 @@ def run_ours(args, world, rank, local):
     t_dev = max_over_ranks(t_dev, world)
     rep = prof.report
     value = world * a_stream_gbs(t_dev)
-    st = run.stats
+    st = None if sharded else run.stats
+    sigma_top = (run.sigma if sharded else run.factors.sigma)[:3]
 
     # roofline of the dominant kernel family
     peaks, basis = measured_peaks()
@@ -301,13 +323,20 @@ def run_ours(args, world, rank, local):
         a_host = pinned.numpy()
         del A
         torch.cuda.empty_cache()
+        def e2e_step():
+            if sharded:   # host panel in, U rows / sigma / Vt out
+                f = one_step(torch.as_tensor(a_host).to(dev, non_blocking=True))
+                return f.U.cpu(), f.sigma.cpu(), f.Vt.cpu()
+            r2 = run_rsvd(a_host, cfg, warn=False)
+            return r2.factors.U, r2.factors.sigma, r2.factors.Vt
+
         for _ in range(max(1, min(args.warmup, 2))):
-            run_rsvd(a_host, cfg, warn=False)
+            e2e_step()
         barrier(world)
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            r2 = run_rsvd(a_host, cfg, warn=False)
-            float(r2.factors.sigma[0])     # the result is on the host
+            out = e2e_step()
+            float(out[1][0])     # the result is on the host
         t_e2e = (time.perf_counter() - t0) / max(args.steps, 1)
         barrier(world)
         t_e2e = max_over_ranks(t_e2e, world)
@@ -331,16 +360,17 @@ def run_ours(args, world, rank, local):
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": "config2", "m": M, "n": N_COLS, "k": K, "p": P, "q": Q,
                        "rank": RANK, "noise": NOISE, "passes": PASSES,
-                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "parallelism": f"rowshard{world}" if world > 1 else "single",
                        "l2": "A (4.3 GB) exceeds L2; no flush needed"},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(rep.gpu_launches),
             "clocks": clk.summary(),
-            "stages_s": {"sketch": st.seconds_sketch, "orthonormalize": st.seconds_orthonormalize,
-                         "form_core": st.seconds_form_core, "svd": st.seconds_svd},
-            "sigma_top3": [float(x) for x in run.factors.sigma[:3].cpu()],
+            "stages_s": None if st is None else {
+                "sketch": st.seconds_sketch, "orthonormalize": st.seconds_orthonormalize,
+                "form_core": st.seconds_form_core, "svd": st.seconds_svd},
+            "sigma_top3": [float(x) for x in sigma_top.cpu()],
         }
         print(json.dumps(line), flush=True)
 

@@ -127,6 +127,19 @@ BRSVD_API int brsvd_sketch_product(brsvd_ctx* ctx, const void* A, int64_t m, int
                                    const void* X, int64_t ldx, int64_t l, void* C,
                                    int64_t ldc);
 
+/* Out-of-core randomized SVD of a host-resident A (brsvd_run /
+ * rsvd_naive_ooc, rsvd.py:188-284, global power iteration): A is streamed
+ * over PCIe in panels of `panel` rows (row-major A) or columns (column-major
+ * A) through `nbuf` device buffers, the copy of the next panel overlapping
+ * the products on the current one (pinned host memory for true overlap).
+ * Costs q + 2 passes over A; stats->words_read / passes report them.
+ * Other arguments as brsvd_rsvd. */
+BRSVD_API int brsvd_rsvd_stream(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n,
+                                int64_t lda, int dtype, int layout, int k, int p, int q,
+                                const void* omega, int omega_where, uint64_t seed, void* U,
+                                void* sigma, void* Vt, int out_where, int64_t panel, int nbuf,
+                                brsvd_stats* stats);
+
 /* Orthonormal basis of range(Y) (tsqr_factor, kernels.py:139-164).
  *   Y m x l column-major (ldy); Q m x l column-major; R (optional) l x l
  *   column-major with Y = Q R.  *detected_rank receives the numerical rank. */

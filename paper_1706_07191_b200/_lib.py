@@ -26,7 +26,7 @@ EXPORTED = (
     "brsvd_gaussian", "brsvd_profile_begin", "brsvd_profile_end",
     "brsvd_spectral_norm", "brsvd_ialm", "brsvd_sketch_product", "brsvd_gram",
     "brsvd_chol_basis", "brsvd_apply", "brsvd_normalize", "brsvd_colmax",
-    "brsvd_scale_cols",
+    "brsvd_scale_cols", "brsvd_rsvd_stream",
 )
 
 
@@ -94,6 +94,9 @@ def _declare(lib):
                                ctypes.POINTER(i32), ctypes.POINTER(i32), vp, vp, vp, vp]
     lib.brsvd_sketch_product.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, vp,
                                          i64, i64, vp, i64]
+    lib.brsvd_rsvd_stream.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, c_int, c_int,
+                                      vp, c_int, u64, vp, vp, vp, c_int, i64, c_int,
+                                      ctypes.POINTER(BrsvdStats)]
     lib.brsvd_gram.argtypes = [vp, vp, i64, i64, i64, c_int, vp, i64, i64, vp]
     lib.brsvd_chol_basis.argtypes = [vp, vp, i64, dbl, dbl, dbl, dbl, vp,
                                      ctypes.POINTER(i32), ctypes.POINTER(i32)]

@@ -8,6 +8,7 @@
 
 #include "pipeline.cuh"
 #include "rpca.cuh"
+#include "stream.cuh"
 
 using namespace brsvd;
 
@@ -94,6 +95,32 @@ struct OutView {
     if (host && dptr) cudaFreeAsync(dptr, s);
   }
 };
+
+void fill_stats(brsvd_stats* stats, const RsvdInfo& info, int64_t m, int64_t n, int l,
+                int q) {
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->words_read = info.words_read;
+    stats->block_reads = info.block_reads;
+    stats->passes_num = info.words_read;
+    stats->passes_den = m * n;
+    stats->flop_estimate = (int64_t)2 * m * n * l * (2 * q + 2) + (int64_t)4 * m * l * l +
+                           (int64_t)2 * n * l * l;
+    stats->detected_rank = info.rank_y;
+    stats->core_rank = info.rank_b;
+    stats->max_abs_y0 = info.max_abs_y0;
+    stats->log10_peak_est = info.log10_peak;
+    stats->overflow = info.overflow ? 1 : 0;
+    stats->seconds_sketch = info.ms_sketch * 1e-3;
+    stats->seconds_orthonormalize = info.ms_orth * 1e-3;
+    stats->seconds_form_core = info.ms_core * 1e-3;
+    stats->seconds_svd = info.ms_svd * 1e-3;
+  }
+  if (info.overflow)
+    throw Error(kErrOverflow,
+                "sample matrix magnitude exceeds the overflow guard; lower the power exponent "
+                "or rescale the input");
+}
 
 }  // namespace
 
@@ -232,29 +259,46 @@ int brsvd_rsvd(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda,
     so.flush();
     vo.flush();
     BRSVD_CUDA(cudaStreamSynchronize(c.stream));
-    if (stats) {
-      std::memset(stats, 0, sizeof(*stats));
-      stats->words_read = info.words_read;
-      stats->block_reads = info.block_reads;
-      stats->passes_num = info.words_read;
-      stats->passes_den = m * n;
-      stats->flop_estimate = (int64_t)2 * m * n * l * (2 * q + 2) +
-                             (int64_t)4 * m * l * l + (int64_t)2 * n * l * l;
-      stats->detected_rank = info.rank_y;
-      stats->core_rank = info.rank_b;
-      stats->max_abs_y0 = info.max_abs_y0;
-      stats->log10_peak_est = info.log10_peak;
-      stats->overflow = info.overflow ? 1 : 0;
-      stats->seconds_sketch = info.ms_sketch * 1e-3;
-      stats->seconds_orthonormalize = info.ms_orth * 1e-3;
-      stats->seconds_form_core = info.ms_core * 1e-3;
-      stats->seconds_svd = info.ms_svd * 1e-3;
-    }
-    if (info.overflow) {
-      throw Error(kErrOverflow,
-                  "sample matrix magnitude exceeds the overflow guard; lower the "
-                  "power exponent or rescale the input");
-    }
+    fill_stats(stats, info, m, n, l, q);
+    return (int)kOk;
+  });
+}
+
+int brsvd_rsvd_stream(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda,
+                      int dtype, int layout, int k, int p, int q, const void* omega,
+                      int omega_where, uint64_t seed, void* U, void* sigma, void* Vt,
+                      int out_where, int64_t panel, int nbuf, brsvd_stats* stats) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && A != nullptr, kErrArg, "NULL argument");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    const size_t es = esize(dtype);
+    BRSVD_REQUIRE(m >= 1 && n >= 1, kErrShape, "matrix must be non-empty");
+    BRSVD_REQUIRE(k >= 1 && p >= 0 && k + p <= std::min(m, n), kErrConfig,
+                  "k + p exceeds min(m, n)");
+    BRSVD_REQUIRE(q >= 0, kErrConfig, "power exponent must be non-negative");
+    BRSVD_REQUIRE(panel >= 1 && nbuf >= 1, kErrArg, "panel and nbuf must be positive");
+    const int l = k + p;
+    const bool row_major = layout == BRSVD_ROW_MAJOR;
+    BRSVD_REQUIRE(lda >= (row_major ? n : m), kErrShape, "lda too small");
+    InView ov(c, omega, n, l, n, es, omega ? omega_where : BRSVD_DEVICE);
+    OutView uo(c, U, (size_t)m * l * es, out_where);
+    OutView so(c, sigma, (size_t)l * es, out_where);
+    OutView vo(c, Vt, (size_t)n * l * es, out_where);
+    RsvdInfo info;
+    if (dtype == BRSVD_F64)
+      info = rsvd_stream<double>(c, (const double*)A, m, n, lda, row_major, k, p, q,
+                                 (const double*)ov.dptr, seed, (double*)uo.dptr,
+                                 (double*)so.dptr, (double*)vo.dptr, panel, nbuf);
+    else
+      info = rsvd_stream<float>(c, (const float*)A, m, n, lda, row_major, k, p, q,
+                                (const float*)ov.dptr, seed, (float*)uo.dptr,
+                                (float*)so.dptr, (float*)vo.dptr, panel, nbuf);
+    uo.flush();
+    so.flush();
+    vo.flush();
+    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+    fill_stats(stats, info, m, n, l, q);
     return (int)kOk;
   });
 }

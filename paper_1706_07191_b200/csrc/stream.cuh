@@ -1,0 +1,232 @@
+// Out-of-core randomized SVD: A stays in host memory and is streamed over
+// PCIe in panels (brsvd_run / rsvd_naive_ooc, rsvd.py:188-284, with the
+// global power iteration of rsvd_incore).
+//
+// Panels go through a ring of NB device buffers: a dedicated copy stream
+// issues cudaMemcpy2DAsync (pinned host memory makes it a true async DMA)
+// while the compute stream runs the products on the previous panel; events
+// order buffer reuse.  Each panel crosses PCIe once per pass and is read
+// twice from HBM when a pass needs both products:
+//   row panels (row-major A):   Y_i = A_i X,  Z += A_i^T Y_i
+//   column panels (col-major):  Z_J = A_J^T Yn, Y' += A_J Z_J
+// so the whole decomposition costs q + 2 passes over A: the
+// sketch pass (which also starts the first power step), q - 1 more power
+// passes, the pass that forms the final sample, and the B = Q^T A pass.
+#pragma once
+#include "pipeline.cuh"
+
+namespace brsvd {
+
+template <typename T>
+__global__ void axpy_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx,
+                            T* __restrict__ y, int64_t ldy) {
+  const int64_t total = rows * cols;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = id % rows, j = id / rows;
+    y[i + j * ldy] += x[i + j * ldx];
+  }
+}
+
+template <typename T>
+void axpy(Ctx& c, const T* x, int64_t rows, int64_t cols, int64_t ldx, T* y, int64_t ldy) {
+  axpy_kernel<T><<<grid_for(rows * cols), 256, 0, c.stream>>>(x, rows, cols, ldx, y, ldy);
+  BRSVD_CHECK_LAUNCH();
+}
+
+// Ring of device panel buffers fed from host memory on a side stream.
+template <typename T>
+struct PanelStreamer {
+  Ctx& c;
+  const T* host;
+  int64_t m, n, lda;
+  bool row_major;
+  int64_t panel;  // rows (row-major) or columns (column-major) per panel
+  int nb;
+  cudaStream_t copy = nullptr;
+  std::vector<cudaEvent_t> copied, consumed;
+  std::vector<DBuf<T>*> bufs;
+  int64_t panels_streamed = 0;
+
+  PanelStreamer(Ctx& c_, const T* host_, int64_t m_, int64_t n_, int64_t lda_, bool rm,
+                int64_t panel_, int nb_)
+      : c(c_), host(host_), m(m_), n(n_), lda(lda_), row_major(rm), panel(panel_), nb(nb_) {
+    BRSVD_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+    const int64_t inner = row_major ? n : m;
+    for (int b = 0; b < nb; ++b) {
+      cudaEvent_t e1, e2;
+      BRSVD_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+      BRSVD_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+      copied.push_back(e1);
+      consumed.push_back(e2);
+      bufs.push_back(new DBuf<T>(c, (size_t)(panel * inner)));
+    }
+    // buffers start "consumed"
+    for (int b = 0; b < nb; ++b) BRSVD_CUDA(cudaEventRecord(consumed[b], c.stream));
+  }
+  ~PanelStreamer() {
+    cudaStreamSynchronize(copy);
+    cudaStreamSynchronize(c.stream);
+    for (auto e : copied) cudaEventDestroy(e);
+    for (auto e : consumed) cudaEventDestroy(e);
+    for (auto b : bufs) delete b;
+    if (copy) cudaStreamDestroy(copy);
+  }
+  int64_t extent() const { return row_major ? m : n; }
+  int64_t count() const { return ceil_div(extent(), panel); }
+
+  // f(device panel pointer, ld, p0, p1) runs on the compute stream.
+  template <class F>
+  void pass(F&& f) {
+    const int64_t np = count();
+    const int64_t inner = row_major ? n : m;
+    for (int64_t i = 0; i < np; ++i) {
+      const int b = (int)(i % nb);
+      const int64_t p0 = i * panel, p1 = std::min(extent(), p0 + panel);
+      BRSVD_CUDA(cudaStreamWaitEvent(copy, consumed[b], 0));
+      BRSVD_CUDA(cudaMemcpy2DAsync(bufs[b]->p, inner * sizeof(T), host + p0 * lda,
+                                   lda * sizeof(T), inner * sizeof(T), p1 - p0,
+                                   cudaMemcpyHostToDevice, copy));
+      BRSVD_CUDA(cudaEventRecord(copied[b], copy));
+      BRSVD_CUDA(cudaStreamWaitEvent(c.stream, copied[b], 0));
+      f(bufs[b]->p, inner, p0, p1);
+      BRSVD_CUDA(cudaEventRecord(consumed[b], c.stream));
+      ++panels_streamed;
+    }
+  }
+};
+
+template <typename T>
+RsvdInfo rsvd_stream(Ctx& c, const T* Ah, int64_t m, int64_t n, int64_t lda, bool row_major,
+                     int k, int p, int q, const T* omega, uint64_t seed, T* U, T* sigma, T* V,
+                     int64_t panel, int nbuf) {
+  const int l = k + p;
+  RsvdInfo info;
+  StageEvents ev;
+  PanelStreamer<T> ps(c, Ah, m, n, lda, row_major, panel, nbuf);
+  ev.rec(0, c.stream);
+  DBuf<T> Xg;
+  const T* X = omega;
+  if (X == nullptr) {
+    Xg.alloc(c, (size_t)n * l);
+    gaussian_kernel<T><<<grid_for(n * ((l + 1) / 2)), 256, 0, c.stream>>>(Xg.p, n, l, n, seed,
+                                                                           0, 0);
+    BRSVD_CHECK_LAUNCH();
+    X = Xg.p;
+  }
+  DBuf<T> Y(c, (size_t)m * l), Z(c, (size_t)n * l), Zn(c, (size_t)n * l);
+  const int64_t pmax = panel;
+  DBuf<T> tmpZ(c, (size_t)(row_major ? n : pmax) * l);
+  DBuf<T> tmpY(c, row_major ? (size_t)1 : (size_t)m * l);
+  int passes = 0;
+  double peak0 = 0.0;
+  if (row_major) {
+    // pass 0: Y_i = A_i Omega (+ first power step Z = sum A_i^T Y_i)
+    for (int it = 0; it <= q; ++it) {
+      const T* Xin = it == 0 ? X : Zn.p;
+      const bool more = it < q;
+      if (more) BRSVD_CUDA(cudaMemsetAsync(Z.p, 0, sizeof(T) * n * l, c.stream));
+      ps.pass([&](const T* Ap, int64_t ld, int64_t r0, int64_t r1) {
+        big_nn<T>(c, Ap, r1 - r0, n, ld, true, Xin, n, l, Y.p + r0, m);
+        if (more) {
+          big_tn<T>(c, Ap, r1 - r0, n, ld, true, Y.p + r0, m, l, tmpZ.p, n);
+          axpy<T>(c, tmpZ.p, n, l, n, Z.p, n);
+        }
+      });
+      ++passes;
+      if (it == 0) {
+        const MaxAbs p0 = maxabs<T>(c, Y.p, m, l, m);
+        peak0 = p0.peak;
+        if (p0.nonfinite) {
+          info.overflow = true;
+          info.log10_peak = INFINITY;
+          return info;
+        }
+      }
+      if (more) normalize_sketch<T>(c, Z.p, n, l, n, Zn.p, n);
+    }
+  } else {
+    // column panels: Y = sum_J A_J Omega_J, then Y' = sum_J A_J (A_J^T Yn)
+    DBuf<T> Yn(c, (size_t)m * l), Ynew(c, (size_t)m * l);
+    for (int it = 0; it <= q; ++it) {
+      T* acc = it == 0 ? Y.p : Ynew.p;
+      BRSVD_CUDA(cudaMemsetAsync(acc, 0, sizeof(T) * m * l, c.stream));
+      if (it > 0) normalize_sketch<T>(c, Y.p, m, l, m, Yn.p, m);
+      ps.pass([&](const T* Ap, int64_t ld, int64_t j0, int64_t j1) {
+        const int64_t w = j1 - j0;
+        if (it == 0) {
+          big_nn<T>(c, Ap, m, w, ld, false, X + j0, n, l, tmpY.p, m);
+        } else {
+          big_tn<T>(c, Ap, m, w, ld, false, Yn.p, m, l, tmpZ.p, pmax);
+          big_nn<T>(c, Ap, m, w, ld, false, tmpZ.p, pmax, l, tmpY.p, m);
+        }
+        axpy<T>(c, tmpY.p, m, l, m, acc, m);
+      });
+      ++passes;
+      if (it > 0)
+        BRSVD_CUDA(cudaMemcpyAsync(Y.p, Ynew.p, sizeof(T) * m * l, cudaMemcpyDeviceToDevice,
+                                   c.stream));
+      if (it == 0) {
+        const MaxAbs p0 = maxabs<T>(c, Y.p, m, l, m);
+        peak0 = p0.peak;
+        if (p0.nonfinite) {
+          info.overflow = true;
+          info.log10_peak = INFINITY;
+          return info;
+        }
+      }
+    }
+  }
+  ev.rec(1, c.stream);
+  const int ns = sizeof(T) == 8 ? 2 : 1;
+  DBuf<double> Qw(c, (size_t)m * l);
+  info.rank_y = orth_full<T>(c, Y.p, m, l, m, Qw.p, seed ^ 0x7153ull, ns);
+  DBuf<T> Qt;
+  const T* Qop;
+  if (sizeof(T) == 8) {
+    Qop = reinterpret_cast<const T*>(Qw.p);
+  } else {
+    Qt.alloc(c, (size_t)m * l);
+    copy2d_kernel<double, T><<<grid_for(m * l), 256, 0, c.stream>>>(Qw.p, m, l, m, Qt.p, m);
+    BRSVD_CHECK_LAUNCH();
+    Qop = Qt.p;
+  }
+  ev.rec(2, c.stream);
+  DBuf<T> Bt(c, (size_t)n * l);
+  if (row_major) BRSVD_CUDA(cudaMemsetAsync(Bt.p, 0, sizeof(T) * n * l, c.stream));
+  ps.pass([&](const T* Ap, int64_t ld, int64_t p0, int64_t p1) {
+    if (row_major) {
+      big_tn<T>(c, Ap, p1 - p0, n, ld, true, Qop + p0, m, l, tmpZ.p, n);
+      axpy<T>(c, tmpZ.p, n, l, n, Bt.p, n);
+    } else {
+      big_tn<T>(c, Ap, m, p1 - p0, ld, false, Qop, m, l, Bt.p + p0, n);
+    }
+  });
+  ++passes;
+  ev.rec(3, c.stream);
+  Y.release();
+  DBuf<double> W(c, (size_t)l * l), sig(c, l);
+  info.rank_b = small_svd_device<T>(c, Bt.p, n, l, n, W.p, sig.p, V, n, ns);
+  gemm_nn_cm<double, double, T>(c, m, l, l, Qw.p, m, W.p, l, U, m);
+  fix_signs<T>(c, U, m, l, m, V, n, n);
+  copy2d_kernel<double, T><<<1, 256, 0, c.stream>>>(sig.p, l, 1, l, sigma, l);
+  BRSVD_CHECK_LAUNCH();
+  ev.rec(4, c.stream);
+  double s0 = 0.0;
+  readback(c, sig.p, &s0, sizeof(double));
+  info.max_abs_y0 = peak0;
+  info.words_read = (int64_t)passes * m * n;
+  info.block_reads = (int64_t)passes * ps.count();
+  info.ms_sketch = ev.ms(0, 1);
+  info.ms_orth = ev.ms(1, 2);
+  info.ms_core = ev.ms(2, 3);
+  info.ms_svd = ev.ms(3, 4);
+  const double lim = std::log10(0.01 * finfo_max<T>());
+  info.log10_peak = (peak0 > 0.0 && s0 > 0.0)
+                        ? std::log10(peak0) + 2.0 * q * std::log10(s0)
+                        : (peak0 > 0.0 ? std::log10(peak0) : -400.0);
+  info.overflow = !std::isfinite(s0) || info.log10_peak > lim;
+  return info;
+}
+
+}  // namespace brsvd

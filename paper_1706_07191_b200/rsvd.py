@@ -12,7 +12,9 @@ Intentional deltas:
     (same answer as s = 1), not the per-block iteration of rsvd.py:169-175.
   * A store is read across the boundary once per decomposition when it fits
     in HBM, so ``stats.full_passes`` is 1 (reference: 2 for brsvd_run,
-    2(q+1) for rsvd_naive_ooc).
+    2(q+1) for rsvd_naive_ooc).  With a ``memory_budget_bytes`` below the
+    payload, the budget's column blocks are streamed from host memory and a
+    decomposition costs q + 2 passes.
 """
 
 import ctypes
@@ -178,6 +180,52 @@ def _load_store_to_device(store, plan):
     return dev.t()   # m x n column-major view
 
 
+def run_rsvd_stream(a, cfg, panel=None, nbuf=3, omega=None, warn=True):
+    """Out-of-core decomposition of a host-resident matrix (C ABI
+    ``brsvd_rsvd_stream``): A is streamed over PCIe in panels of ``panel``
+    rows (C-ordered ``a``) or columns (Fortran-ordered ``a``) through ``nbuf``
+    device buffers; q + 2 passes.  Pinned host memory (e.g. a numpy view of a
+    ``torch.empty(..., pin_memory=True)`` tensor) overlaps copies with compute.
+    Returns RsvdRun with numpy factors."""
+    mat = HostMatrix(a)
+    m, n = mat.shape
+    cfg.validate(m, n)
+    k, p, q = cfg.target_rank, cfg.oversampling, cfg.power_exponent
+    l = k + p
+    inner = n if mat.layout == _lib.ROW_MAJOR else m
+    if panel is None:   # ~1 GiB panels
+        panel = max(1, (1 << 30) // max(1, inner * mat.a.itemsize))
+    ctx = _lib.context()
+    U = np.empty((m, l), dtype=mat.dtype, order="F")
+    sigma = np.empty(l, dtype=mat.dtype)
+    Vt = np.empty((l, n), dtype=mat.dtype, order="C")
+    keep, optr, owhere = _omega_arg(omega, n, l, mat.dtype, False)
+    stats = _lib.BrsvdStats()
+    t0 = time.perf_counter()
+    rc = _lib.load_library().brsvd_rsvd_stream(
+        ctx.handle, mat.ptr, m, n, mat.ld, mat.code, mat.layout, k, p, q, optr, owhere,
+        ctypes.c_uint64(int(cfg.master_seed) & (2 ** 64 - 1)),
+        ctypes.c_void_p(U.ctypes.data), ctypes.c_void_p(sigma.ctypes.data),
+        ctypes.c_void_p(Vt.ctypes.data), _lib.HOST, int(panel), int(nbuf),
+        ctypes.byref(stats))
+    wall = time.perf_counter() - t0
+    del keep
+    _lib.check(rc)
+    if warn:
+        warn_rank(stats.detected_rank, l)
+        warn_rank(stats.core_rank, l)
+    f = SvdFactors(U=U, sigma=sigma, Vt=Vt, target_rank=k, effective_l=l)
+    return RsvdRun(factors=f, stats=stats, wall_seconds=wall)
+
+
+def _store_payload(store):
+    """Read-only memory map of a store's column-major payload (m x n)."""
+    from .store import HEADER_SIZE
+    mm = np.memmap(store.path, dtype=store.dtype, mode="r", offset=HEADER_SIZE,
+                   shape=(store.n, store.m))
+    return mm.T   # m x n, Fortran-ordered view
+
+
 def _run_store(store, cfg, memory_budget_bytes, stage_names):
     m, n = store.m, store.n
     cfg.validate(m, n)
@@ -186,6 +234,24 @@ def _run_store(store, cfg, memory_budget_bytes, stage_names):
                        memory_budget_bytes=memory_budget_bytes, s=s)
     store.reset_stats()
     stats = store.stats
+    if memory_budget_bytes is not None and store.payload_bytes > memory_budget_bytes:
+        # Out of core: the budget's column blocks are the streamed panels;
+        # q + 2 passes over the store cross the boundary.
+        t0 = time.perf_counter()
+        run = run_rsvd_stream(_store_payload(store), cfg, panel=plan.n_prime, nbuf=3)
+        st = run.stats
+        passes = st.words_read // (m * n)
+        stats.words_read += int(st.words_read)
+        stats.block_reads += int(passes * plan.s)
+        stats.flop_estimate += int(st.flop_estimate)
+        seconds = {"sketch": st.seconds_sketch, "power": 0.0,
+                   "orthonormalize": st.seconds_orthonormalize,
+                   "form_core": st.seconds_form_core, "svd": st.seconds_svd}
+        words = {"sketch": (passes - 1) * m * n, "form_core": m * n}
+        for name in stage_names:
+            stats.log_stage(name, words.get(name, 0), 0, seconds[name])
+        del t0
+        return run.factors, stats, plan
     t0 = time.perf_counter()
     a_dev = _load_store_to_device(store, plan)
     load_s = time.perf_counter() - t0

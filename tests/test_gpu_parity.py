@@ -244,3 +244,44 @@ def test_f32_config2_shape_small_scale():
                                    ref["sigma"].astype(np.float64),
                                    ref["Vt"].astype(np.float64))
     assert abs(e_gpu - e_ref) <= 1e-4
+
+
+@pytest.mark.parametrize("order", ["C", "F"])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_streamed_out_of_core_matches_in_core(order, dtype):
+    """brsvd_rsvd_stream (host-resident A, panels over PCIe) == in-core."""
+    from paper_1706_07191_b200 import SketchConfig
+    from paper_1706_07191_b200.rsvd import run_rsvd, run_rsvd_stream
+    a = ref_cpu.lowrank_plus_noise(3000, 1200, 20, 1e-3, seed=21, dtype=dtype)
+    a = np.asarray(a, order=order)
+    omega = ref_cpu.normal_sketch(1200, 30, 0, dtype=dtype)
+    cfg = SketchConfig(20, 10, 2)
+    inc = run_rsvd(a, cfg, omega=omega, warn=False)
+    st = run_rsvd_stream(a, cfg, panel=257, nbuf=3, omega=omega, warn=False)
+    assert st.stats.words_read == (2 + 2) * a.size          # q + 2 passes
+    fp64 = dtype == np.float64
+    np.testing.assert_allclose(st.factors.sigma[:20], inc.factors.sigma[:20],
+                               rtol=1e-10 if fp64 else 1e-5)
+    assert sin_theta(st.factors.U[:, :20], inc.factors.U[:, :20]) <= (1e-8 if fp64 else 1e-4)
+    ref = ref_cpu.randomized_svd(a, 20, 10, 2, omega=omega)
+    np.testing.assert_allclose(st.factors.sigma[:20], ref["sigma"][:20],
+                               rtol=1e-10 if fp64 else 1e-5)
+
+
+def test_brsvd_run_budget_streams_store(tmp_path):
+    """brsvd_run with a budget below the payload streams the plan's blocks."""
+    from paper_1706_07191_b200 import MatrixStore, SketchConfig, brsvd_run, rsvd_incore
+    a = ref_cpu.lowrank_plus_noise(2000, 600, 8, 1e-4, seed=22)
+    st = MatrixStore.from_array(tmp_path / "a.oocm", a)
+    cfg = SketchConfig(target_rank=8, oversampling=8, power_exponent=1)
+    f, stats = brsvd_run(st, cfg, memory_budget_bytes=4 * 1024 * 1024)
+    assert stats.full_passes == 3                              # q + 2
+    assert stats.block_reads > 3
+    assert [e["stage"] for e in stats.stage_log] == ["sketch", "orthonormalize",
+                                                     "form_core", "svd"]
+    g = rsvd_incore(a, cfg)
+    np.testing.assert_allclose(f.sigma[:8], g.sigma[:8], rtol=1e-10)
+    f2, stats2 = brsvd_run(st, cfg)                            # fits: read once
+    assert stats2.full_passes == 1
+    np.testing.assert_allclose(f2.sigma[:8], g.sigma[:8], rtol=1e-10)
+    st.close()
