@@ -35,7 +35,7 @@ constexpr int BM = 128;
 constexpr int BK = 16;              // fp32 K elements per stage (64-byte rows)
 constexpr int STAGES = 6;
 constexpr int NPAD_MAX = 320;   // l <= 320: two CTAs of <= 160 columns
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kASlot = 320;    // TMEM columns [320, 512): six A staging slots
 constexpr uint32_t A_STAGE_BYTES = BM * BK * 4;
@@ -43,6 +43,7 @@ constexpr uint32_t A_STAGE_BYTES = BM * BK * 4;
 struct Params {
   int64_t M, K;
   int npad, nchunks, rows_c, n_out;
+  int ksplit;  // 1 or 2 K-halves per tile (2: atomicAdd of two partials)
   float* C;
   int64_t ldc;
 };
@@ -145,11 +146,43 @@ __device__ __forceinline__ uint32_t tf32_rna(float x) {
 // fp32 running sums held in the converter warps' registers.
 constexpr int kChunkKB = 8;
 
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                 "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr)
+               : "memory");
+}
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float lds32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+
+// Warp roles (384 threads): warp 0 TMA producer, warp 1 MMA issuer, warp 2
+// TMEM allocator, warps 4-11 converters/flushers.  Converter warp w owns TMEM
+// lane quadrant (w % 4) -- the rows 32(w%4)..+31 of the tile -- and half
+// h = (w - 4) / 4 of the work: k values [8h, 8h+8) of each A stage and the
+// accumulator columns [h nc/2, (h+1) nc/2) of every flush.
 template <bool A_KMAJOR, int NCMAX>
 __global__ void __launch_bounds__(kThreads, 1)
     tc3_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
                     const __grid_constant__ CUtensorMap mapBhi,
                     const __grid_constant__ CUtensorMap mapBlo, const Params p) {
+  constexpr int NH = NCMAX / 2;                          // running sums per thread
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_dyn + 1023) & ~(uintptr_t)1023);
   const int nc = p.rows_c;                               // columns of this CTA
@@ -163,21 +196,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accfree + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m0 = (int64_t)(blockIdx.x / p.nchunks) * BM;
-  const int nhalf = blockIdx.x % p.nchunks;
-  const int n0 = nhalf * nc;
-  const int nk = (int)((p.K + BK - 1) / BK);
+  const int tiles_n = p.nchunks;
+  const int ks = blockIdx.x % p.ksplit;
+  const int tile = blockIdx.x / p.ksplit;
+  const int64_t m0 = (int64_t)(tile / tiles_n) * BM;
+  const int n0 = (tile % tiles_n) * nc;
+  const int nk_all = (int)((p.K + BK - 1) / BK);
+  const int per = (nk_all + p.ksplit - 1) / p.ksplit;
+  const int kb_begin = ks * per;
+  const int nk = max(0, min(nk_all, kb_begin + per) - kb_begin);
   const int nchunk = (nk + kChunkKB - 1) / kChunkKB;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&freeb[s], 1);
-      mbar_init(&tfull[s], 4);
+      mbar_init(&tfull[s], 8);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accready[b], 1);
-      mbar_init(&accfree[b], 4);
+      mbar_init(&accfree[b], 8);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
@@ -204,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&freeb[s], ph ^ 1);
         uint8_t* st = smem + (size_t)s * stage_bytes;
         mbar_expect_tx(&full[s], stage_bytes);
-        const int k0 = kb * BK;
+        const int k0 = (kb_begin + kb) * BK;
         if (A_KMAJOR) {
           tma_load_2d(st, &mapA, &full[s], k0, (int)m0);
         } else {
@@ -248,63 +286,67 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {  // ---------------- converters + accumulator flushes
-    const int wq = warp - 4;
+    const int wq = warp & 3;
+    const int half = (warp - 4) >> 2;
     const int r = wq * 32 + lane;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-    float run[NCMAX];
+    const int hc = nc >> 1;                 // accumulator columns per half
+    const int c0 = half * hc;
+    float run[NH];
 #pragma unroll
-    for (int j = 0; j < NCMAX; ++j) run[j] = 0.f;
+    for (int j = 0; j < NH; ++j) run[j] = 0.f;
     auto flush = [&](int chunk) {
       const int buf = chunk & 1;
       mbar_wait(&accready[buf], (chunk >> 1) & 1);
       tc_after_sync();
 #pragma unroll
-      for (int j0 = 0; j0 < NCMAX; j0 += 16) {
-        if (j0 < nc) {
-          uint32_t acc[16];
-          tmem_ld16(tmem + lane_base + (uint32_t)(buf * nc + j0), acc);
+      for (int j0 = 0; j0 < NH; j0 += 8) {
+        if (j0 < hc) {
+          uint32_t acc[8];
+          tmem_ld8(tmem + lane_base + (uint32_t)(buf * nc + c0 + j0), acc);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int i = 0; i < 16; ++i) run[j0 + i] += __uint_as_float(acc[i]);
+          for (int i = 0; i < 8; ++i) run[j0 + i] += __uint_as_float(acc[i]);
         }
       }
       tc_before_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive(&accfree[buf]);
     };
+    const uint32_t smem_base = smem_u32(smem);
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % STAGES;
       const uint32_t ph = (kb / STAGES) & 1;
       mbar_wait(&full[s], ph);
-      const uint8_t* sa = smem + (size_t)s * stage_bytes;
-      float v[16];
+      const uint32_t sa = smem_base + (uint32_t)s * stage_bytes;
+      float v[8];
       if (A_KMAJOR) {
         // 64-byte rows; TMA 64B swizzle puts 16B chunk j of row r at j^((r>>1)&3)
-        const uint8_t* row = sa + r * 64;
+        const uint32_t row = sa + r * 64;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float4 x =
-              *reinterpret_cast<const float4*>(row + ((j ^ ((r >> 1) & 3)) << 4));
-          v[4 * j + 0] = x.x;
-          v[4 * j + 1] = x.y;
-          v[4 * j + 2] = x.z;
-          v[4 * j + 3] = x.w;
+        for (int jj = 0; jj < 2; ++jj) {
+          const int j = 2 * half + jj;
+          const float4 x = lds128(row + ((j ^ ((r >> 1) & 3)) << 4));
+          v[4 * jj + 0] = x.x;
+          v[4 * jj + 1] = x.y;
+          v[4 * jj + 2] = x.z;
+          v[4 * jj + 3] = x.w;
         }
       } else {
         // four (32 rows x 16 k) boxes, 32 consecutive rows per k
-        const float* box = reinterpret_cast<const float*>(sa + wq * (32 * BK * 4));
+        const uint32_t box = sa + wq * (32 * BK * 4) + lane * 4;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = box[k * 32 + lane];
+        for (int k = 0; k < 8; ++k) v[k] = lds32(box + (8 * half + k) * 128);
       }
-      uint32_t hi[16], lo[16];
+      uint32_t hi[8], lo[8];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
+      for (int i = 0; i < 8; ++i) {
         const uint32_t h = tf32_rna(v[i]);
         hi[i] = h;
         lo[i] = __float_as_uint(v[i] - __uint_as_float(h));
       }
-      tmem_st16(tmem + lane_base + kASlot + s * 32, hi);
-      tmem_st16(tmem + lane_base + kASlot + s * 32 + 16, lo);
+      tmem_st8(tmem + lane_base + kASlot + s * 32 + 8 * half, hi);
+      tmem_st8(tmem + lane_base + kASlot + s * 32 + 16 + 8 * half, lo);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_before_sync();
       __syncwarp();
@@ -312,13 +354,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       // the previous chunk's accumulator is complete once this chunk started
       if (kb > 0 && (kb % kChunkKB) == 0) flush(kb / kChunkKB - 1);
     }
-    flush(nchunk - 1);
+    if (nchunk > 0) flush(nchunk - 1);
     const int64_t row = m0 + r;
     if (row < p.M) {
 #pragma unroll
-      for (int j = 0; j < NCMAX; ++j) {
-        const int col = n0 + j;
-        if (j < nc && col < p.n_out) p.C[row + (int64_t)col * p.ldc] = run[j];
+      for (int j = 0; j < NH; ++j) {
+        const int col = n0 + c0 + j;
+        if (j < hc && col < p.n_out) {
+          float* dst = p.C + row + (int64_t)col * p.ldc;
+          if (p.ksplit > 1) atomicAdd(dst, run[j]);   // two partial sums: order-free
+          else *dst = run[j];
+        }
       }
     }
   }
@@ -458,8 +504,20 @@ inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, 
   p.n_out = l;
   p.C = C;
   p.ldc = ldc;
+  // Two K-halves per tile when the tile count leaves the last wave of CTAs
+  // (one per SM) badly filled: the two fp32 partial sums are combined with
+  // atomicAdd into a zeroed C, which is order-independent for two terms.
+  const int64_t tiles = ceil_div(M, BM) * g.nchunks;
+  const double waves = (double)tiles / c.num_sms;
+  p.ksplit = (K >= 8192 && waves > 1.0 && waves < 8.0 &&
+              waves - std::floor(waves) > 0.0 && waves - std::floor(waves) < 0.75)
+                 ? 2
+                 : 1;
+  if (p.ksplit > 1)
+    BRSVD_CUDA(cudaMemset2DAsync(C, (size_t)ldc * sizeof(float), 0, (size_t)M * sizeof(float),
+                                 (size_t)l, c.stream));
   const size_t smem = smem_bytes(g.rows_c);
-  const dim3 grid((unsigned)(ceil_div(M, BM) * g.nchunks));
+  const dim3 grid((unsigned)(tiles * p.ksplit));
 #define BRSVD_TC_LAUNCH(KM, NCM)                                                      \
   do {                                                                                \
     BRSVD_CUDA(cudaFuncSetAttribute(tc3_gemm_kernel<KM, NCM>,                         \
