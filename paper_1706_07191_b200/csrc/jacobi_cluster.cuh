@@ -1,0 +1,324 @@
+// One-sided Jacobi SVD of a square l x l matrix held entirely in the
+// distributed shared memory of ONE thread-block cluster (8 or 16 CTAs).
+//
+// Replaces, for the l-by-l core problems of the pipeline (np.linalg.svd(r.T)
+// in small_svd, kernels.py:173-188, and the Gram eigen-solves behind tsqr,
+// kernels.py:121-164), the cooperative-grid block Jacobi of jacobi.cuh whose
+// every tournament round went through global memory and a grid barrier.
+//
+// Layout: the columns of G (and of the accumulated rotation V) are grouped in
+// nb = 2 * cluster_size blocks of bw columns.  CTA c plays positions c and
+// nb-1-c of a round-robin ("circle method") tournament over the blocks, so in
+// every round each CTA owns one block pair in its shared memory:
+//   * the first round of a sweep orthogonalises all 2bw columns of the pair,
+//   * later rounds only the bw^2 cross pairs (block a column i against block
+//     b column (i + s) mod bw, s = 0..bw-1),
+// so every column pair meets exactly once per sweep.  Between rounds every CTA
+// PULLS its next two blocks from their current owners over DSMEM into the
+// other half of a ping-pong buffer; one cluster barrier per round orders the
+// pulls against the previous round's rotations (see the hazard note below).
+// A column rotation is one warp: the two columns stay in registers from the
+// dot products to the update (NP2 row pairs per lane, 8/16-byte shared-memory
+// accesses), the three reductions share one butterfly.
+#pragma once
+#include <cooperative_groups.h>
+#include "common.cuh"
+
+namespace brsvd {
+
+template <typename R>
+struct JacobiClusterArgs {
+  R* G;          // l x l, column-major, ld ldg  (overwritten by G V)
+  int64_t ldg;
+  R* V;          // l x l, column-major, ld ldv  (accumulated rotations; identity on entry)
+  int64_t ldv;
+  int l;         // matrix order
+  int bw;        // block width
+  int max_sweeps;
+  double tol;        // rotate while |x.y| > tol ||x|| ||y||
+  double floor_rel;  // columns below floor_rel * ||G||_F are numerically null
+  int* sweeps_done;  // optional
+};
+
+__device__ __forceinline__ int tourn_pos(int pos, int r, int n) {
+  return pos == 0 ? 0 : ((pos - 1 + r) % (n - 1)) + 1;
+}
+// Inverse of tourn_pos: the position block b sits at in round r.
+__device__ __forceinline__ int tourn_inv(int b, int r, int n) {
+  return b == 0 ? 0 : ((b - 1 - r) % (n - 1) + (n - 1)) % (n - 1) + 1;
+}
+
+template <typename R>
+__device__ __forceinline__ R jc_rsqrt(R x);
+template <>
+__device__ __forceinline__ float jc_rsqrt<float>(float x) { return rsqrtf(x); }
+template <>
+__device__ __forceinline__ double jc_rsqrt<double>(double x) { return 1.0 / sqrt(x); }
+
+template <typename R> struct Vec2;
+template <> struct Vec2<float> { using type = float2; };
+template <> struct Vec2<double> { using type = double2; };
+
+// Rotate columns (x, y) of G and (vx, vy) of V so that the G columns become
+// orthogonal.  One warp; columns are zero-padded to lp (a multiple of 4) and
+// each lane owns row pairs (2 lane + 64 k, +1), k < NP2, kept in registers
+// from the dot products to the update.  Returns true if rotated.
+template <typename R, int NP2>
+__device__ __forceinline__ bool jc_rotate(R* __restrict__ x, R* __restrict__ y,
+                                          R* __restrict__ vx, R* __restrict__ vy, int lp,
+                                          R tol2, R floor2, int lane) {
+  using V2 = typename Vec2<R>::type;
+  V2 xr[NP2], yr[NP2];
+  R a = 0, b = 0, g = 0;
+#pragma unroll
+  for (int k = 0; k < NP2; ++k) {
+    const int i = 2 * lane + 64 * k;
+    if (i < lp) {
+      xr[k] = *reinterpret_cast<const V2*>(x + i);
+      yr[k] = *reinterpret_cast<const V2*>(y + i);
+    } else {
+      xr[k].x = xr[k].y = yr[k].x = yr[k].y = R(0);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NP2; ++k) {
+    a = fma(xr[k].x, xr[k].x, a);
+    b = fma(yr[k].x, yr[k].x, b);
+    g = fma(xr[k].x, yr[k].x, g);
+    a = fma(xr[k].y, xr[k].y, a);
+    b = fma(yr[k].y, yr[k].y, b);
+    g = fma(xr[k].y, yr[k].y, g);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    g += __shfl_xor_sync(0xffffffffu, g, o);
+  }
+  if (!(a > floor2 && b > floor2)) return false;
+  if (!(g * g > tol2 * a * b)) return false;
+  R t;
+  if (sizeof(R) == 4) {
+    // fp32 phase (a preconditioner for the fp64 sweeps): approximate
+    // reciprocal / square root; c and s stay consistent through rsqrt.
+    const float zeta = __fdividef((float)(b - a), 2.0f * (float)g);
+    const float az = fabsf(zeta);
+    if (az > 1e18f) {
+      t = (R)__fdividef(0.5f, zeta);
+    } else {
+      const float w = fmaf(zeta, zeta, 1.0f);
+      t = (R)copysignf(__fdividef(1.0f, az + w * rsqrtf(w)), zeta);
+    }
+  } else {
+    const R zeta = (b - a) / (R(2) * g);
+    if (fabs(zeta) > R(1e150)) {
+      t = R(0.5) / zeta;
+    } else {
+      t = copysign(R(1), zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, R(1))));
+    }
+  }
+  if (t == R(0)) return false;
+  const R c = jc_rsqrt<R>(fma(t, t, R(1)));
+  const R s = c * t;
+#pragma unroll
+  for (int k = 0; k < NP2; ++k) {
+    const int i = 2 * lane + 64 * k;
+    if (i < lp) {
+      V2 nx, ny;
+      nx.x = c * xr[k].x - s * yr[k].x;
+      nx.y = c * xr[k].y - s * yr[k].y;
+      ny.x = s * xr[k].x + c * yr[k].x;
+      ny.y = s * xr[k].y + c * yr[k].y;
+      *reinterpret_cast<V2*>(x + i) = nx;
+      *reinterpret_cast<V2*>(y + i) = ny;
+      xr[k] = *reinterpret_cast<const V2*>(vx + i);
+      yr[k] = *reinterpret_cast<const V2*>(vy + i);
+      nx.x = c * xr[k].x - s * yr[k].x;
+      nx.y = c * xr[k].y - s * yr[k].y;
+      ny.x = s * xr[k].x + c * yr[k].x;
+      ny.y = s * xr[k].y + c * yr[k].y;
+      *reinterpret_cast<V2*>(vx + i) = nx;
+      *reinterpret_cast<V2*>(vy + i) = ny;
+    }
+  }
+  return true;
+}
+
+// Shared memory: buf[2][2 slots][bw columns][2 * lp] of R, where a column is
+// its G part (lp entries, lp = l rounded up to 4) followed by its V part.
+template <typename R>
+__host__ __device__ inline size_t jacobi_cluster_smem(int l, int bw) {
+  const int lp = (l + 3) & ~3;
+  return (size_t)2 * 2 * bw * 2 * lp * sizeof(R);
+}
+
+template <typename R, int NP2>
+__global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char jc_raw[];
+  R* buf = reinterpret_cast<R*>(jc_raw);
+  __shared__ int s_cnt[2];     // rotations of the current sweep, by sweep parity
+  __shared__ double s_red[32];
+  __shared__ int s_stop;
+
+  const int l = a.l, bw = a.bw;
+  const int lp = (l + 3) & ~3;
+  const int colsz = 2 * lp;                    // G part + V part
+  const size_t slotsz = (size_t)bw * colsz;    // one block
+  const size_t bufsz = 2 * slotsz;             // two blocks
+  const int C = (int)cluster.num_blocks();
+  const int me = (int)cluster.block_rank();
+  const int nb = 2 * C;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int tid = threadIdx.x, nt = blockDim.x;
+
+  // ||G||_F^2 is invariant under the rotations: fix the null floor once.
+  {
+    double f = 0.0;
+    for (int c = warp; c < l; c += nwarps)
+      for (int i = lane; i < l; i += 32) {
+        const double v = (double)a.G[c * a.ldg + i];
+        f = fma(v, v, f);
+      }
+    f = warp_sum(f);
+    if (lane == 0) s_red[warp] = f;
+    if (tid < 2) s_cnt[tid] = 0;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < nwarps; ++w) t += s_red[w];
+      s_red[0] = t;
+    }
+    __syncthreads();
+  }
+  const R floor2 = (R)(a.floor_rel * a.floor_rel * s_red[0]);
+  const R tol2 = (R)(a.tol * a.tol);
+
+  // Initial load of round 0's block pair from global memory into buf[0].
+  {
+    R* dst = buf;
+    for (int e = tid; e < 2 * bw * lp; e += nt) {
+      const int cl = e / lp, i = e % lp;         // local column, row
+      const int slot = cl / bw, j = cl % bw;
+      const int blk = tourn_pos(slot == 0 ? me : nb - 1 - me, 0, nb);
+      const int gc = blk * bw + j;
+      R* col = dst + slot * slotsz + (size_t)j * colsz;
+      const bool ok = gc < l && i < l;
+      col[i] = ok ? a.G[(int64_t)gc * a.ldg + i] : R(0);
+      col[lp + i] = ok ? a.V[(int64_t)gc * a.ldv + i] : R(0);
+    }
+  }
+  cluster.sync();
+
+  int r = 0;  // global round counter; tournament round = r % (nb - 1)
+  int sweep = 0;
+  int my_rot = 0;
+  for (;;) {
+    const int tr = r % (nb - 1);
+    R* cur = buf + (size_t)(r & 1) * bufsz;
+    const int ba = tourn_pos(me, tr, nb), bb = tourn_pos(nb - 1 - me, tr, nb);
+    // valid column counts of the two blocks (ragged last block)
+    const int va = max(0, min(bw, l - ba * bw)), vb = max(0, min(bw, l - bb * bw));
+    __syncthreads();
+    if (tr == 0) {
+      // all pairs of the 2bw columns: inner circle tournament over W = 2bw
+      const int W = 2 * bw;
+      for (int st = 0; st < W - 1; ++st) {
+        for (int p = warp; p < bw; p += nwarps) {
+          const int ca = tourn_pos(p, st, W), cb = tourn_pos(W - 1 - p, st, W);
+          const int ja = ca % bw, jb = cb % bw;
+          const bool oka = ca < bw ? ja < va : ja < vb;
+          const bool okb = cb < bw ? jb < va : jb < vb;
+          if (!oka || !okb) continue;
+          R* x = cur + (size_t)(ca / bw) * slotsz + (size_t)ja * colsz;
+          R* y = cur + (size_t)(cb / bw) * slotsz + (size_t)jb * colsz;
+          if (jc_rotate<R, NP2>(x, y, x + lp, y + lp, lp, tol2, floor2, lane)) ++my_rot;
+        }
+        __syncthreads();
+      }
+    } else {
+      for (int st = 0; st < bw; ++st) {
+        for (int p = warp; p < bw; p += nwarps) {
+          const int jb = p + st < bw ? p + st : p + st - bw;
+          if (p >= va || jb >= vb) continue;
+          R* x = cur + (size_t)p * colsz;
+          R* y = cur + slotsz + (size_t)jb * colsz;
+          if (jc_rotate<R, NP2>(x, y, x + lp, y + lp, lp, tol2, floor2, lane)) ++my_rot;
+        }
+        __syncthreads();
+      }
+    }
+    const bool sweep_end = (tr == nb - 2);
+    if (sweep_end && lane == 0 && my_rot) atomicAdd(&s_cnt[sweep & 1], my_rot);
+    if (sweep_end) my_rot = 0;
+    // Hazards: the pull below reads the peers' buf[r&1] (rotated in this
+    // round, before this barrier) and writes our buf[(r+1)&1], which the peers
+    // last read while pulling for round r (before this barrier).
+    cluster.sync();
+    if (sweep_end) {
+      if (tid == 0) {
+        int tot = 0;
+        for (int q = 0; q < C; ++q) tot += *cluster.map_shared_rank(&s_cnt[sweep & 1], q);
+        s_stop = (tot == 0) || (sweep + 1 >= a.max_sweeps);
+        s_cnt[(sweep + 1) & 1] = 0;
+      }
+      __syncthreads();
+      if (s_stop) break;
+      ++sweep;
+    }
+    // pull the blocks of round r+1 into buf[(r+1)&1]
+    const int tn = (r + 1) % (nb - 1);
+    R* nxt = buf + (size_t)((r + 1) & 1) * bufsz;
+    {
+      const int4* s4[2];
+      for (int slot = 0; slot < 2; ++slot) {
+        const int blk = tourn_pos(slot == 0 ? me : nb - 1 - me, tn, nb);
+        const int pos = tourn_inv(blk, tr, nb);         // where it sat this round
+        const int owner = pos < C ? pos : nb - 1 - pos;
+        const int oslot = pos < C ? 0 : 1;
+        s4[slot] = reinterpret_cast<const int4*>(
+            cluster.map_shared_rank(cur + oslot * slotsz, owner));
+      }
+      int4* d4 = reinterpret_cast<int4*>(nxt);
+      const int n4 = (int)(slotsz * sizeof(R) / 16);  // per slot
+      // DSMEM loads have ~200 cycles of latency: keep 8 in flight per thread
+      constexpr int U = 8;
+      for (int e0 = tid; e0 < 2 * n4; e0 += U * nt) {
+        int4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * nt;
+          if (e < 2 * n4) v[u] = e < n4 ? s4[0][e] : s4[1][e - n4];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * nt;
+          if (e < 2 * n4) d4[e] = v[u];
+        }
+      }
+    }
+    ++r;
+  }
+  // converged: our current pair is in buf[r&1]; write it back
+  {
+    const int tr = r % (nb - 1);
+    const R* cur = buf + (size_t)(r & 1) * bufsz;
+    for (int e = tid; e < 2 * bw * l; e += nt) {
+      const int cl = e / l, i = e % l;
+      const int slot = cl / bw, j = cl % bw;
+      const int blk = tourn_pos(slot == 0 ? me : nb - 1 - me, tr, nb);
+      const int gc = blk * bw + j;
+      if (gc >= l) continue;
+      const R* col = cur + slot * slotsz + (size_t)j * colsz;
+      a.G[(int64_t)gc * a.ldg + i] = col[i];
+      a.V[(int64_t)gc * a.ldv + i] = col[lp + i];
+    }
+  }
+  if (me == 0 && tid == 0 && a.sweeps_done) *a.sweeps_done = sweep + 1;
+  // keep the cluster alive until every peer finished reading our counters
+  cluster.sync();
+}
+
+}  // namespace brsvd

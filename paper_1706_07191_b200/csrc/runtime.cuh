@@ -20,6 +20,7 @@
 #include "gemm_simt.cuh"
 #include "chol.cuh"
 #include "jacobi.cuh"
+#include "jacobi_cluster.cuh"
 #include "small_kernels.cuh"
 
 namespace brsvd {
@@ -175,11 +176,96 @@ inline double jacobi_tol_tight(int nrow) {
 constexpr double kJacobiTolOrth = 1e-8;
 constexpr double kJacobiTolNormalize = 1e-4;
 
+// Cluster-resident Jacobi (jacobi_cluster.cuh) for square problems that are
+// too big for one CTA but fit the shared memory of an 8- or 16-CTA cluster.
+// Returns false (nothing launched) when the shape or the device does not fit.
+template <typename R, int NP2>
+bool jacobi_cluster_launch(Ctx& c, const JacobiClusterArgs<R>& args, int csize,
+                           size_t smem, int threads) {
+  auto kern = jacobi_cluster_kernel<R, NP2>;
+  BRSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+  if (csize > 8)
+    BRSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(csize);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = csize;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess ||
+      nclusters < 1) {
+    cudaGetLastError();
+    return false;
+  }
+  BRSVD_CUDA(cudaLaunchKernelEx(&cfg, kern, args));
+  BRSVD_CHECK_LAUNCH();
+  return true;
+}
+
+template <typename R>
+bool jacobi_cluster(Ctx& c, R* G, int l, int64_t ldg, R* V, int64_t ldv, double tol,
+                    double floor_rel, int max_sweeps, int* sweeps_done) {
+  if (l > 512 || l < 64 || std::getenv("BRSVD_NO_CLUSTER_JACOBI")) return false;
+  const size_t lim = c.max_smem_optin > 4096 ? c.max_smem_optin - 4096 : 0;
+  for (int csize : {16, 8}) {
+    const int bw = (int)ceil_div(l, 2 * csize);
+    const size_t smem = jacobi_cluster_smem<R>(l, bw);
+    if (smem > lim) continue;
+    JacobiClusterArgs<R> a;
+    a.G = G;
+    a.ldg = ldg;
+    a.V = V;
+    a.ldv = ldv;
+    a.l = l;
+    a.bw = bw;
+    a.max_sweeps = max_sweeps;
+    a.tol = tol;
+    a.floor_rel = floor_rel;
+    a.sweeps_done = sweeps_done;
+    const int threads = std::min(1024, std::max(256, 32 * bw));
+    const int np2 = (int)ceil_div((l + 3) & ~3, 64);  // row pairs per lane
+    bool ok;
+    if (np2 <= 2) ok = jacobi_cluster_launch<R, 2>(c, a, csize, smem, threads);
+    else if (np2 <= 3) ok = jacobi_cluster_launch<R, 3>(c, a, csize, smem, threads);
+    else if (np2 <= 4) ok = jacobi_cluster_launch<R, 4>(c, a, csize, smem, threads);
+    else if (np2 <= 5) ok = jacobi_cluster_launch<R, 5>(c, a, csize, smem, threads);
+    else if (np2 <= 6) ok = jacobi_cluster_launch<R, 6>(c, a, csize, smem, threads);
+    else ok = jacobi_cluster_launch<R, 8>(c, a, csize, smem, threads);
+    if (ok) return true;
+  }
+  return false;
+}
+
+// floor_rel < 0: the default null-column floor 16 nrow eps(R).  The fp32 phase
+// of the two-phase small SVD passes a lower one so that small but resolvable
+// columns (noise-level singular values of fp32 data) converge already in fp32.
 template <typename R = double>
 inline int jacobi(Ctx& c, R* G, int nrow, int ncol, int64_t ldg, R* V, int64_t ldv,
-                  double tol, int max_sweeps = 40) {
+                  double tol, int max_sweeps = 40, double floor_rel = -1.0) {
   BRSVD_REQUIRE(ncol >= 1 && ncol <= 1024 && nrow >= 1, kErrShape,
                 "jacobi: unsupported small-problem shape");
+  const double eps_r0 = sizeof(R) == 8 ? 2.220446049250313e-16 : 1.1920928955078125e-07;
+  const double tol_eff = std::max(tol, 8.0 * std::sqrt((double)nrow) * eps_r0);
+  const double floor_eff = floor_rel >= 0.0 ? floor_rel : 16.0 * nrow * eps_r0;
+  if (nrow == ncol) {
+    DBuf<int> sw(c, 1);
+    if (jacobi_cluster<R>(c, G, nrow, ldg, V, ldv, tol_eff, floor_eff, max_sweeps, sw.p)) {
+      if (std::getenv("BRSVD_DEBUG")) {
+        const int nsw = read_int(c, sw.p);
+        std::fprintf(stderr, "[brsvd] jacobi(cluster) %dx%d tol %.1e: %d sweeps\n", nrow,
+                     ncol, tol_eff, nsw);
+      }
+      return 0;
+    }
+  }
   const size_t budget = std::min<size_t>(c.max_smem_optin, 200 * 1024);
   const size_t per_col = (size_t)(nrow + ncol) * sizeof(R) + sizeof(int);
   int bw_fit = (int)(budget / (2 * per_col));
@@ -215,9 +301,8 @@ inline int jacobi(Ctx& c, R* G, int nrow, int ncol, int64_t ldg, R* V, int64_t l
   args.bw = bw;
   args.nb = nb;
   args.max_sweeps = max_sweeps;
-  const double eps_r = sizeof(R) == 8 ? 2.220446049250313e-16 : 1.1920928955078125e-07;
-  args.tol = std::max(tol, 8.0 * std::sqrt((double)nrow) * eps_r);
-  args.floor_rel = 16.0 * nrow * eps_r;
+  args.tol = tol_eff;
+  args.floor_rel = floor_eff;
   args.rot_count = counters.p;
   args.sweeps_done = counters.p + max_sweeps;
   if (single) {
@@ -551,7 +636,7 @@ int small_svd_device(Ctx& c, const T* Bt, int64_t n, int l, int64_t ldb, double*
                                                                                 M32.p, l);
     eye_kernel<float><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(V32.p, l);
     BRSVD_CHECK_LAUNCH();
-    jacobi<float>(c, M32.p, l, l, l, V32.p, l, 1e-5);
+    jacobi<float>(c, M32.p, l, l, l, V32.p, l, 1e-5, 40, 16.0 * l * 2.220446049250313e-16);
     copy2d_kernel<float, double><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(V32.p, l, l, l,
                                                                                 Vj.p, l);
     BRSVD_CHECK_LAUNCH();
