@@ -547,15 +547,10 @@ int brsvd_chol_basis(brsvd_ctx* ctx, double* G, int64_t l, double shift, double 
     BRSVD_REQUIRE(l >= 1 && l <= kCholMaxL, kErrShape, "chol_basis supports 1 <= l <= 384");
     set_chol_attrs(c);
     const int li = (int)l;
-    DBuf<double> Wd(c, (size_t)l * l), s(c, l), info(c, 3), Tm(c, (size_t)l * l);
+    DBuf<double> Wd(c, (size_t)l * l), info(c, 3), Tm(c, (size_t)l * l);
     DBuf<int> keep(c, l);
-    gram_prep_kernel<<<1, 1024, 0, c.stream>>>(G, li, s.p, Wd.p, 1, nullptr, col_drop);
-    BRSVD_CHECK_LAUNCH();
-    chol_kernel<<<1, 1024, chol_smem(li), c.stream>>>(G, li, li, shift, info.p,
-                                                      rank_tol > 0.0 ? s.p : nullptr,
-                                                      rank_tol, drop_ratio, keep.p);
-    BRSVD_CHECK_LAUNCH();
-    trinv_t_kernel<<<1, 1024, trinv_smem(li), c.stream>>>(G, li, li, s.p, Wd.p, Tm.p);
+    cholinv_launch(c.stream, c.max_smem_optin, G, li, li, 1, col_drop, shift, drop_ratio,
+                   rank_tol, Wd.p, Tm.p, nullptr, info.p, keep.p);
     BRSVD_CHECK_LAUNCH();
     BRSVD_CUDA(cudaMemsetAsync(T, 0, sizeof(double) * l * l, c.stream));
     compact_cols_kernel<<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(Tm.p, li, keep.p,

@@ -5,6 +5,10 @@
 // Householder QR of tsqr (kernels.py:121-164) and the Gram eigen-solves of the
 // Jacobi route, whose sequential depth is O(sweeps * l) against O(l / NB) here.
 #pragma once
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cooperative_groups.h>
 #include "common.cuh"
 
 namespace brsvd {
@@ -217,6 +221,416 @@ inline size_t chol_smem(int n) {
 }
 inline size_t trinv_smem(int n) {
   return ((size_t)n * kCholNB + kCholNB * kCholNB + (size_t)n * kCholNB) * sizeof(double);
+}
+
+
+}  // namespace brsvd
+
+namespace brsvd {
+
+// ---------------------------------------------------------------------------
+// Fused Cholesky basis change on one thread-block cluster: from a Gram matrix
+// G = X^T X (n x n, lower triangle read) to T = S L^-T, where
+//   s_j = 1/sqrt(G_jj) (column scaling; 0 for columns below col_drop of the
+//   largest), S G S + shift I = L L^T.
+// Replaces gram_prep + chol_kernel + trinv_t_kernel (three single-CTA
+// launches whose inner loops were latency-bound) by one launch:
+//   * blocked right-looking factorisation with 32-column panels.  Every CTA of
+//     the cluster redundantly factors the 32 x 32 diagonal block (one warp,
+//     rows in registers, column values broadcast by shuffles), inverts it (a
+//     column per lane) and solves the panel below against that inverse; the
+//     trailing SYRK update of the L2-resident matrix is split over the CTAs
+//     (4 x 4 register tiles fed by 16-byte shared loads of a k-major panel);
+//   * the inverse by block rows, X_IJ = -L_II^-1 sum_K L_IK X_KJ, columns
+//     split over the CTAs, with the diagonal-block inverses from the panels;
+//   * one cluster barrier per panel / block row orders the global updates.
+// Semantics (pivot drop, info[0..2], keep) are those of chol_kernel above.
+constexpr int kCiNB = 32;
+constexpr int kCiLd = 33;       // padded row stride of the shared panel
+constexpr int kCiThreads = 512;
+__device__ long long g_ci_t[64];
+#define CI_T(k) do { if (me == 0 && tid == 0) g_ci_t[(k)] = clock64(); } while (0)
+
+__host__ __device__ inline int cholinv_ldp(int n) { return (n + 3) & ~3; }
+__host__ __device__ inline size_t cholinv_big(int n) {
+  const size_t p1 = (size_t)n * kCiLd + (size_t)kCiNB * cholinv_ldp(n);  // phase 1 panels
+  const size_t p2 = (size_t)2 * kCiNB * n;                              // phase 2
+  return p1 > p2 ? p1 : p2;
+}
+inline size_t cholinv_smem(int n) {
+  return (cholinv_big(n) + (size_t)kCiNB * kCiLd + 4 * (size_t)n) * sizeof(double) +
+         (size_t)n * sizeof(int);
+}
+
+__global__ void __launch_bounds__(kCiThreads, 1)
+    cholinv_kernel(double* __restrict__ A, int n, int64_t ld, int scale, double col_drop,
+                   double shift, double drop_ratio, double rank_tol,
+                   double* __restrict__ X, double* __restrict__ T,
+                   double* __restrict__ s_out, double* __restrict__ info,
+                   int* __restrict__ keep) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) double cism[];
+  const size_t big = cholinv_big(n);
+  const int ldp = cholinv_ldp(n);
+  double* Lp = cism;                      // phase 1: panel, row-major rows x 33
+  double* PT = cism + (size_t)n * kCiLd;  // phase 1: L21 k-major, 32 x ldp
+  double* Di = cism + big;                // 32 x 33: inverse of the diagonal block
+  double* sc = Di + kCiNB * kCiLd;        // column scaling
+  double* d0 = sc + n;                    // scaled diagonal + shift
+  double* dL = d0 + n;                    // diagonal of L
+  double* Rat = dL + n;                   // pivots (for info[0] = min pivot / diagonal)
+  int* dropped = reinterpret_cast<int*>(Rat + n);
+  __shared__ double s_red[32];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int me = (int)cluster.block_rank(), C = (int)cluster.num_blocks();
+  const int gt = me * nt + tid, gnt = C * nt;      // cluster-wide thread index
+  const int gw = me * nw + warp, gnw = C * nw;     // cluster-wide warp index
+  const bool leader = (me == 0);
+
+  CI_T(0);
+  // ---- phase 0: scaling (redundant per CTA; the matrix write is split) ----
+  double dm = 0.0;
+  for (int j = tid; j < n; j += nt) dm = fmax(dm, A[(int64_t)j * ld + j]);
+  dm = warp_max(dm);
+  if (lane == 0) s_red[warp] = dm;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int w = 0; w < nw; ++w) m = fmax(m, s_red[w]);
+    s_red[0] = m;
+  }
+  __syncthreads();
+  const double fl2 = col_drop * col_drop * s_red[0];
+  for (int j = tid; j < n; j += nt) {
+    const double d = A[(int64_t)j * ld + j];
+    const double s = scale ? ((d > fl2 && d > 0.0) ? 1.0 / sqrt(d) : 0.0) : 1.0;
+    sc[j] = s;
+    d0[j] = s * s * d + shift;
+    if (s_out && leader) s_out[j] = s;
+  }
+  cluster.sync();  // every CTA has read the unscaled diagonal
+  for (int j = gw; j < n; j += gnw) {
+    const double sj = sc[j];
+    double* col = A + (int64_t)j * ld;
+    for (int i = j + lane; i < n; i += 32) col[i] = (i == j) ? d0[j] : col[i] * sc[i] * sj;
+  }
+  cluster.sync();
+
+  CI_T(1);
+  // ---- phase 1: blocked right-looking factorisation --------------------
+  for (int p0 = 0; p0 < n; p0 += kCiNB) {
+    const int pi = p0 / kCiNB;
+    const int nb = min(kCiNB, n - p0), rows = n - p0;
+    {
+      // batched loads (8 in flight per thread) before the shared stores
+      constexpr int U = 8;
+      const int tot = rows * nb;
+      for (int e0 = tid; e0 < tot; e0 += U * nt) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * nt;
+          const int i = e % rows, c = e / rows;
+          v[u] = (e < tot && i >= c) ? A[(int64_t)(p0 + c) * ld + (p0 + i)] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * nt;
+          if (e < tot) Lp[(e % rows) * kCiLd + e / rows] = v[u];
+        }
+      }
+    }
+    __syncthreads();
+    if (pi == 0) CI_T(2);
+    if (warp == 0) {
+      // factor the diagonal block in shared memory, lane r owning row r; the
+      // pivot test avoids divisions (piv/dg is only recorded for info[0]) and
+      // the factor uses rsqrt.  Loops stay rolled (instruction cache).
+      // Left-looking (Crout) column by column: lane r forms
+      // d_r = A[r][c] - L[r][:c] . L[c][:c] with independent loads (no
+      // stores in the dot), lane c's value is the pivot.
+      const int r = lane;
+      double* Lrow = Lp + r * kCiLd;
+      for (int c = 0; c < nb; ++c) {
+        const double* Lc = Lp + c * kCiLd;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if (r >= c && r < nb) {
+          int k = 0;
+#pragma unroll 2
+          for (; k + 3 < c; k += 4) {
+            s0 = fma(Lrow[k], Lc[k], s0);
+            s1 = fma(Lrow[k + 1], Lc[k + 1], s1);
+            s2 = fma(Lrow[k + 2], Lc[k + 2], s2);
+            s3 = fma(Lrow[k + 3], Lc[k + 3], s3);
+          }
+          for (; k < c; ++k) s0 = fma(Lrow[k], Lc[k], s0);
+        }
+        const double dr = (r >= c && r < nb) ? Lrow[c] - ((s0 + s1) + (s2 + s3)) : 0.0;
+        const double piv = __shfl_sync(0xffffffffu, dr, c);
+        const double dg = d0[p0 + c];
+        const bool drop = !(piv > 0.0) ||
+                          (drop_ratio > 0.0 && (!(dg > 0.0) || !(piv > drop_ratio * dg)));
+        const double inv = drop ? 0.0 : rsqrt(piv);
+        if (r == c) {
+          const double dsq = piv * inv;
+          Lrow[c] = drop ? 1.0 : dsq;
+          Di[kCiNB * kCiLd - kCiNB + c] = drop ? 1.0 : inv;  // scratch: 1 / L[c][c]
+          dropped[p0 + c] = drop ? 1 : 0;
+          dL[p0 + c] = drop ? 0.0 : dsq;
+          Rat[p0 + c] = piv;
+        } else if (r > c && r < nb) {
+          Lrow[c] = dr * inv;
+        }
+        __syncwarp();
+      }
+      // zero the strict upper triangle of the block
+      for (int j = r + 1; j < nb; ++j) Lrow[j] = 0.0;
+      __syncwarp();
+      if (pi == 0) CI_T(9);
+      // Di = L11^-1 (lower); lane c computes column c from its own earlier
+      // entries, two partial sums per row
+      const int c = lane;
+      double rinv[1];
+      for (int rr = 0; rr < nb; ++rr) {
+        rinv[0] = Di[kCiNB * kCiLd - kCiNB + rr];
+        double v0 = (rr == c) ? 1.0 : 0.0, v1 = 0.0;
+        if (rr > c) {
+          const double* lr = Lp + rr * kCiLd;
+          int k = c;
+#pragma unroll 4
+          for (; k + 1 < rr; k += 2) {
+            v0 = fma(-lr[k], Di[k * kCiLd + c], v0);
+            v1 = fma(-lr[k + 1], Di[(k + 1) * kCiLd + c], v1);
+          }
+          if (k < rr) v0 = fma(-lr[k], Di[k * kCiLd + c], v0);
+        }
+        const double x = (rr >= c && c < nb) ? (v0 + v1) * rinv[0] : 0.0;
+        __syncwarp();
+        Di[rr * kCiLd + c] = x;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (pi == 0) CI_T(3);
+    // TRSM: L21 = A21 L11^-T (rows nb..rows-1) into the k-major copy PT
+    // (zero-padded to a multiple of 4 rows); dropped columns are zero.
+    const int rpad = (rows + 3) & ~3;
+    {
+      // thread = (row i, group of 4 columns); one load of L[i][k] feeds four
+      // independent accumulator chains
+      const int nr = rpad - nb;
+      const int ng = (nb + 3) / 4;
+      for (int e = tid; e < nr * ng; e += nt) {
+        const int i = nb + e % nr, c0 = 4 * (e / nr);
+        double v[4] = {0.0, 0.0, 0.0, 0.0};
+        if (i < rows) {
+          const double* li = Lp + i * kCiLd;
+          const int kend = min(c0 + 3, nb - 1);
+#pragma unroll 4
+          for (int k = 0; k <= kend; ++k) {
+            const double lv = li[k];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (k <= c0 + q && c0 + q < nb) v[q] = fma(lv, Di[(c0 + q) * kCiLd + k], v[q]);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (c0 + q < nb) PT[(c0 + q) * ldp + i] = dropped[p0 + c0 + q] ? 0.0 : v[q];
+      }
+    }
+    __syncthreads();
+    if (leader) {
+      // write the panel (L) and the diagonal-block inverse (X) back
+      for (int e = tid; e < rows * nb; e += nt) {
+        const int i = e % rows, c = e / rows;
+        if (i >= c)
+          A[(int64_t)(p0 + c) * ld + (p0 + i)] = i < nb ? Lp[i * kCiLd + c] : PT[c * ldp + i];
+      }
+      for (int e = tid; e < nb * nb; e += nt) {
+        const int r = e % nb, c = e / nb;
+        X[(int64_t)(p0 + c) * n + (p0 + r)] = Di[r * kCiLd + c];
+      }
+    }
+    if (pi == 0) CI_T(4);
+    // trailing update: A22 -= L21 L21^T (lower), 4x4 register tiles, split
+    // over the cluster
+    const int R2 = rows - nb;
+    if (R2 > 0) {
+      const int nti = (R2 + 3) / 4;
+      const int ntiles = nti * (nti + 1) / 2;
+      for (int t = gt; t < ntiles; t += gnt) {
+        // t -> (ti, tj), tj <= ti, row-major over the lower triangle of tiles
+        int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+        while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+        while (ti * (ti + 1) / 2 > t) --ti;
+        const int tj = t - ti * (ti + 1) / 2;
+        const int i0 = nb + 4 * ti, j0 = nb + 4 * tj;
+        double acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+        double old[4][4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            const int gi = i0 + a, gj = j0 + b;
+            old[a][b] = (gi < rows && gj < rows && gi >= gj)
+                            ? A[(int64_t)(p0 + gj) * ld + (p0 + gi)] : 0.0;
+          }
+#pragma unroll 4
+        for (int k = 0; k < nb; ++k) {
+          const double2* pa = reinterpret_cast<const double2*>(PT + k * ldp + i0);
+          const double2* pb = reinterpret_cast<const double2*>(PT + k * ldp + j0);
+          const double2 a01 = pa[0], a23 = pa[1], b01 = pb[0], b23 = pb[1];
+          const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+          const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+        }
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int gj = j0 + b;
+          if (gj >= rows) continue;
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            const int gi = i0 + a;
+            if (gi >= rows || gi < gj) continue;
+            A[(int64_t)(p0 + gj) * ld + (p0 + gi)] = old[a][b] - acc[a][b];
+          }
+        }
+      }
+    }
+    if (pi == 0) CI_T(5);
+    cluster.sync();
+  }
+
+  CI_T(6);
+  // ---- phase 2: X = L^-1 by block rows ----------------------------------
+  double* Lr = cism;                      // Lr[k * 32 + r]: block row of L, k < i0
+  double* Rr = cism + (size_t)kCiNB * n;  // Rr[col * 32 + r]: rhs
+  for (int i0 = kCiNB; i0 < n; i0 += kCiNB) {
+    const int nbI = min(kCiNB, n - i0);
+    for (int e = tid; e < i0 * nbI; e += nt) {
+      const int r = e % nbI, k = e / nbI;
+      Lr[k * kCiNB + r] = A[(int64_t)k * ld + (i0 + r)];
+    }
+    for (int e = tid; e < nbI * nbI; e += nt) {
+      const int r = e % nbI, c = e / nbI;
+      Di[r * kCiLd + c] = X[(int64_t)(i0 + c) * n + (i0 + r)];
+    }
+    __syncthreads();
+    // a warp per column (lanes = rows r), columns split over the cluster:
+    // Rr[:, col] = sum_{k = col .. i0-1} L[i0 + r, k] X[k, col], then
+    // X[i0 + r, col] = -sum_j Di[r, j] Rr[j, col]
+    for (int col = gw; col < i0; col += gnw) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      const double* xc = X + (int64_t)col * n;
+      if (lane < nbI) {
+        int k = col;
+        for (; k + 3 < i0; k += 4) {
+          a0 = fma(Lr[k * kCiNB + lane], xc[k], a0);
+          a1 = fma(Lr[(k + 1) * kCiNB + lane], xc[k + 1], a1);
+          a2 = fma(Lr[(k + 2) * kCiNB + lane], xc[k + 2], a2);
+          a3 = fma(Lr[(k + 3) * kCiNB + lane], xc[k + 3], a3);
+        }
+        for (; k < i0; ++k) a0 = fma(Lr[k * kCiNB + lane], xc[k], a0);
+      }
+      const double rr = (a0 + a1) + (a2 + a3);
+      double v = 0.0;
+#pragma unroll
+      for (int j = 0; j < kCiNB; ++j) {
+        const double rj = __shfl_sync(0xffffffffu, rr, j);
+        if (j <= lane && j < nbI) v = fma(Di[lane * kCiLd + j], rj, v);
+      }
+      if (lane < nbI) X[(int64_t)col * n + (i0 + lane)] = -v;
+    }
+    cluster.sync();
+  }
+
+  CI_T(7);
+  // ---- phase 3: T = S X^T (upper triangular), info ------------------------
+  for (int e = gt; e < n * n; e += gnt) {
+    const int k = e % n, j = e / n;  // T[k, j]
+    T[(int64_t)j * n + k] = (k <= j) ? sc[k] * X[(int64_t)k * n + j] : 0.0;
+    if (k < j) A[(int64_t)j * ld + k] = 0.0;
+  }
+  if (leader && tid == 0 && info) {
+    double minr = 1.0;
+    for (int j = 0; j < n; ++j) {
+      const double rt = (d0[j] > 0.0 && Rat[j] == Rat[j]) ? Rat[j] / d0[j] : -1.0;
+      minr = fmin(minr, rt);
+    }
+    info[0] = minr;
+    int kept = 0;
+    for (int j = 0; j < n; ++j)
+      if (!dropped[j]) {
+        if (keep) keep[kept] = j;
+        ++kept;
+      }
+    info[2] = (double)kept;
+    CI_T(8);
+    if (rank_tol > 0.0) {
+      double fro2 = 0.0;
+      for (int j = 0; j < n; ++j)
+        if (sc[j] > 0.0) fro2 += 1.0 / (sc[j] * sc[j]);
+      const double cut = rank_tol * sqrt(fro2);
+      int rk = 0;
+      for (int j = 0; j < n; ++j)
+        if (!dropped[j] && sc[j] > 0.0 && dL[j] / sc[j] > cut) ++rk;
+      info[1] = (double)rk;
+    }
+  }
+}
+
+
+// Launch of cholinv_kernel on one cluster (8 CTAs for n > 96).
+inline void cholinv_launch(cudaStream_t st, size_t smem_limit, double* A, int n, int64_t ld,
+                           int scale, double col_drop, double shift, double drop_ratio,
+                           double rank_tol, double* X, double* T, double* s_out,
+                           double* info, int* keep) {
+  const size_t smem = cholinv_smem(n);
+  static size_t attr = 0;
+  if (attr < smem) {
+    const cudaError_t e = cudaFuncSetAttribute(
+        cholinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
+      throw Error(kErrCuda, std::string("cholinv smem attribute: ") + cudaGetErrorString(e));
+    attr = smem;
+  }
+  (void)smem_limit;
+  cudaLaunchConfig_t cfg = {};
+  const int csize = n > 96 ? 8 : 1;
+  cfg.gridDim = dim3(csize);
+  cfg.blockDim = dim3(kCiThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = csize;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, cholinv_kernel, A, n, ld, scale, col_drop,
+                                           shift, drop_ratio, rank_tol, X, T, s_out, info,
+                                           keep);
+  if (e != cudaSuccess)
+    throw Error(kErrCuda, std::string("cholinv launch: ") + cudaGetErrorString(e));
+  if (std::getenv("BRSVD_CI_TIMING")) {
+    long long t[10];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(t, g_ci_t, sizeof(t));
+    std::fprintf(stderr, "[cholinv n=%d] scale %lld | p0: load %lld diag %lld trsm %lld trail %lld | "
+                 "panels %lld | inverse %lld | out %lld | factor %lld (cycles)\n", n, t[1] - t[0], t[2] - t[1],
+                 t[3] - t[2], t[4] - t[3], t[5] - t[4], t[6] - t[1], t[7] - t[6], t[8] - t[7], t[9] - t[2]);
+  }
 }
 
 }  // namespace brsvd

@@ -380,20 +380,15 @@ CholInfo chol_basis(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double sh
                     double* Tm, bool sync, double col_drop = 0.0, double rank_tol = 0.0,
                     double drop_ratio = 0.0, int* keep = nullptr,
                     double* info_dev = nullptr) {
-  DBuf<double> G(c, (size_t)l * l), W(c, (size_t)l * l), s(c, l), infob;
+  DBuf<double> G(c, (size_t)l * l), W(c, (size_t)l * l), infob;
   double* info = info_dev;
   if (!info) {
     infob.alloc(c, 3);
     info = infob.p;
   }
   gemm_tn_cm<T, T, double>(c, l, l, r, X, ldx, X, ldx, G.p, l);
-  gram_prep_kernel<<<1, 1024, 0, c.stream>>>(G.p, l, s.p, W.p, 1, nullptr, col_drop);
-  BRSVD_CHECK_LAUNCH();
-  chol_kernel<<<1, 1024, chol_smem(l), c.stream>>>(G.p, l, l, shift, info,
-                                                   rank_tol > 0.0 ? s.p : nullptr, rank_tol,
-                                                   drop_ratio, keep);
-  BRSVD_CHECK_LAUNCH();
-  trinv_t_kernel<<<1, 1024, trinv_smem(l), c.stream>>>(G.p, l, l, s.p, W.p, Tm);
+  cholinv_launch(c.stream, c.max_smem_optin, G.p, l, l, 1, col_drop, shift, drop_ratio,
+                 rank_tol, W.p, Tm, nullptr, info, keep);
   BRSVD_CHECK_LAUNCH();
   CholInfo ci;
   if (sync) {
@@ -559,6 +554,27 @@ int orth_full(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* Q,
     const CholInfo ci = chol_basis<T>(c, X, r, l, ldx, 0.0, Tm.p, true, drop, l * eps_data,
                                       1e-12, keep.p, info.p);
     const int k1 = ci.kept;
+    if (sizeof(T) == 4 && k1 < l) {
+      // fp32 data: the dropped directions are below the data's resolution.
+      // Complete in the same second CholQR pass: [Q1 | Gaussian columns] is
+      // well conditioned, so one pass returns l orthonormal columns whose
+      // first k1 span the kept part of range(X) (kernels.py:142-144, "columns
+      // of Q remain orthonormal").
+      DBuf<double> Q1(c, (size_t)r * l);
+      if (k1 > 0) {
+        compact_cols_kernel<<<grid_for((int64_t)l * k1), 256, 0, c.stream>>>(
+            Tm.p, l, keep.p, info.p, Tc.p);
+        BRSVD_CHECK_LAUNCH();
+        gemm_nn_cm<T, double, double>(c, r, k1, l, X, ldx, Tc.p, l, Q1.p, r);
+      }
+      const int cnt = l - k1;
+      gaussian_kernel<double><<<grid_for(r * ((cnt + 1) / 2)), 256, 0, c.stream>>>(
+          Q1.p + (int64_t)k1 * r, r, cnt, r, seed, 0x636f6d706c657465ull, 0);
+      BRSVD_CHECK_LAUNCH();
+      chol_basis<double>(c, Q1.p, r, l, r, 0.0, Tm.p, false);
+      gemm_nn_cm<double, double, double>(c, r, l, l, Q1.p, r, Tm.p, l, Q, r);
+      return std::min(ci.rank_ref, k1);
+    }
     if (k1 > 0) {
       const double* Tk = Tm.p;
       if (k1 < l) {
