@@ -345,9 +345,9 @@ int brsvd_tsqr(brsvd_ctx* ctx, const void* Y, int64_t m, int64_t l, int64_t ldy,
     InView yv(c, Y, m, l, ldy, es, where);
     OutView qo(c, Q, (size_t)m * l * es, where);
     OutView ro(c, R, (size_t)l * l * es, where);
-    DBuf<double> Qw(c, (size_t)m * l);
     int rank;
     if (dtype == BRSVD_F64) {
+      DBuf<double> Qw(c, (size_t)m * l);
       rank = orth_full<double>(c, (const double*)yv.dptr, m, (int)l, yv.ld, Qw.p,
                                0x75717221ull, 2);
       BRSVD_CUDA(cudaMemcpyAsync(qo.dptr, Qw.p, (size_t)m * l * 8,
@@ -356,14 +356,14 @@ int brsvd_tsqr(brsvd_ctx* ctx, const void* Y, int64_t m, int64_t l, int64_t ldy,
         gemm_tn_cm<double, double, double>(c, l, l, m, Qw.p, m, (const double*)yv.dptr,
                                            yv.ld, (double*)ro.dptr, l);
     } else {
+      DBuf<float> Qw(c, (size_t)m * l);
       rank = orth_full<float>(c, (const float*)yv.dptr, m, (int)l, yv.ld, Qw.p,
                               0x75717221ull, 1);
-      copy2d_kernel<double, float><<<grid_for(m * l), 256, 0, c.stream>>>(
-          Qw.p, m, l, m, (float*)qo.dptr, m);
-      BRSVD_CHECK_LAUNCH();
+      BRSVD_CUDA(cudaMemcpyAsync(qo.dptr, Qw.p, (size_t)m * l * 4,
+                                 cudaMemcpyDeviceToDevice, c.stream));
       if (ro.dptr)
-        gemm_tn_cm<double, float, float>(c, l, l, m, Qw.p, m, (const float*)yv.dptr,
-                                         yv.ld, (float*)ro.dptr, l);
+        gemm_tn_cm<float, float, float>(c, l, l, m, Qw.p, m, (const float*)yv.dptr,
+                                        yv.ld, (float*)ro.dptr, l);
     }
     qo.flush();
     ro.flush();

@@ -1,0 +1,156 @@
+// Tall-skinny Gram products in fp64: C (a x b) = X^T Y for column-major
+// X (r x a), Y (r x b) of fp32 or fp64 data, r >> a, b.
+//
+// These are the fp64 Grams of the Cholesky QR passes (the Cholesky factor of
+// X^T X is the R of tsqr, kernels.py:121-164) and the core M = B Q_b of
+// small_svd (kernels.py:173-188).  fp32 inputs are exact in fp64 and every
+// product is exact, so the only rounding is the fp64 accumulation.
+//
+// 96 x 96 or 128 x 128 output tiles (the one that pads l least; symmetric
+// case: lower-triangle tiles only), 8 x 4 register tiles per thread fed by 16-byte shared loads of k-major
+// slabs, register-prefetched double buffering, and a deterministic split-K:
+// every split writes its partial tile, a second kernel sums the partials in a
+// fixed order (bitwise reproducible, tests/test_gpu_parity.py::test_deterministic).
+#pragma once
+#include "common.cuh"
+
+namespace brsvd {
+namespace gram {
+
+constexpr int BK = 16;  // k slab
+template <int BT> struct Cfg {
+  static constexpr int LDS = BT + 4;                       // padded k-major row (doubles)
+  static constexpr int TY = BT / 8, TX = BT / 4;           // 8 x 4 outputs per thread
+  static constexpr int NT = TX * TY;
+  static constexpr int PER = (BT * BK + NT - 1) / NT;      // loader elements per thread
+  static constexpr size_t SMEM = (size_t)2 * 2 * BK * LDS * sizeof(double);
+};
+
+template <typename TX, typename TY, int BT>
+__global__ void __launch_bounds__(Cfg<BT>::NT, Cfg<BT>::NT <= 288 ? 2 : 1)
+    gram_tile_kernel(int64_t r, int a, int b, const TX* __restrict__ X, int64_t ldx,
+                     const TY* __restrict__ Y, int64_t ldy, int sym, int ntj, int64_t kchunk,
+                     double* __restrict__ part) {
+  using C = Cfg<BT>;
+  constexpr int LDS = C::LDS, NTX = C::TX, NT = C::NT, PER = C::PER, H = BT / 2;
+  extern __shared__ __align__(16) double gsm[];
+  double(*As)[BK][LDS] = reinterpret_cast<double(*)[BK][LDS]>(gsm);
+  double(*Bs)[BK][LDS] = reinterpret_cast<double(*)[BK][LDS]>(gsm + 2 * BK * LDS);
+  const int tid = threadIdx.x;
+  const int tx = tid % NTX, ty = tid / NTX;
+  // tile index -> (ti, tj)
+  int ti, tj;
+  const int t = blockIdx.x;
+  if (sym) {
+    ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+    while (ti * (ti + 1) / 2 > t) --ti;
+    tj = t - ti * (ti + 1) / 2;
+  } else {
+    ti = t / ntj;
+    tj = t % ntj;
+  }
+  const int i0 = ti * BT, j0 = tj * BT;
+  const int64_t kb = (int64_t)blockIdx.y * kchunk;
+  const int64_t ke = min(r, kb + kchunk);
+
+  // loader: element e -> column e / BK, k e % BK (consecutive threads read
+  // consecutive rows of one column: coalesced)
+  // raw (unconverted) prefetch registers: the fp64 conversion happens at the
+  // shared store, after the compute of the current slab, so the global load
+  // latency stays hidden
+  TX ra[PER];
+  TY rb[PER];
+  auto load = [&](int64_t k0) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = tid + q * NT;
+      const int lc = e / BK, lk = e % BK;
+      const int64_t k = k0 + lk;
+      const bool ok = e < BT * BK && k < ke;
+      ra[q] = (ok && i0 + lc < a) ? X[k + (int64_t)(i0 + lc) * ldx] : TX(0);
+      rb[q] = (ok && j0 + lc < b) ? Y[k + (int64_t)(j0 + lc) * ldy] : TY(0);
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = tid + q * NT;
+      if (e < BT * BK) {
+        As[buf][e % BK][e / BK] = (double)ra[q];
+        Bs[buf][e % BK][e / BK] = (double)rb[q];
+      }
+    }
+  };
+  double acc[8][4];
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+
+  int buf = 0;
+  if (kb < ke) {
+    load(kb);
+    store(0);
+  }
+  __syncthreads();
+  for (int64_t k0 = kb; k0 < ke; k0 += BK) {
+    const bool more = k0 + BK < ke;
+    if (more) load(k0 + BK);
+#pragma unroll 4
+    for (int kk = 0; kk < BK; ++kk) {
+      // rows ty*4 .. +3 and BT/2 + ty*4 .. +3 (about two distinct row groups
+      // per warp: broadcasts); columns tx*2, +1 and BT/2 + tx*2, +1 (each
+      // 16-byte load spans contiguous bytes across the warp)
+      const double2* pa = reinterpret_cast<const double2*>(&As[buf][kk][ty * 4]);
+      const double2* pb = reinterpret_cast<const double2*>(&Bs[buf][kk][tx * 2]);
+      const double2 a01 = pa[0], a23 = pa[1], a45 = pa[H / 2], a67 = pa[H / 2 + 1];
+      const double2 b01 = pb[0], b23 = pb[H / 2];
+      const double av[8] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y};
+      const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
+    }
+    if (more) {
+      store(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  // partial tile -> part[split][a x b] (column-major, ld a)
+  double* P = part + (int64_t)blockIdx.y * a * b;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int i = i0 + (u < 4 ? ty * 4 + u : H + ty * 4 + u - 4);
+    if (i >= a) continue;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int j = j0 + (v < 2 ? tx * 2 + v : H + tx * 2 + v - 2);
+      if (j < b) P[i + (int64_t)j * a] = acc[u][v];
+    }
+  }
+}
+
+// C = sum over splits (fixed order); sym: mirror the lower-triangle tiles.
+__global__ void gram_reduce_kernel(const double* __restrict__ part, int a, int b, int splits,
+                                   int sym, int BT, double* __restrict__ C, int64_t ldc) {
+  const int64_t total = (int64_t)a * b;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(idx % a), j = (int)(idx / a);
+    int si = i, sj = j;
+    if (sym && (i / BT) < (j / BT)) {  // upper tile: read the mirrored lower entry
+      si = j;
+      sj = i;
+    }
+    const int64_t src = si + (int64_t)sj * a;
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += part[(int64_t)z * total + src];
+    C[i + (int64_t)j * ldc] = s;
+  }
+}
+
+}  // namespace gram
+}  // namespace brsvd

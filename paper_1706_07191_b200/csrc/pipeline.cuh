@@ -7,8 +7,7 @@
 // match the reference's to rounding while the sketch never overflows or loses
 // rank to cancellation.
 #pragma once
-#include "runtime.cuh"
-#include "big_gemm.cuh"
+#include "orth.cuh"
 
 namespace brsvd {
 
@@ -88,30 +87,19 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
   Zn.release();
   Z.release();
   const int ns = sizeof(T) == 8 ? 2 : 1;
-  DBuf<double> Qw(c, (size_t)m * l);
+  DBuf<T> Qw(c, (size_t)m * l);
   info.rank_y = orth_full<T>(c, Y.p, m, l, m, Qw.p, seed ^ 0x7153ull, ns);
   Y.release();
-  DBuf<T> Qt;
-  const T* Qop;
-  if (sizeof(T) == 8) {
-    Qop = reinterpret_cast<const T*>(Qw.p);
-  } else {
-    Qt.alloc(c, (size_t)m * l);
-    copy2d_kernel<double, T><<<grid_for(m * l), 256, 0, c.stream>>>(Qw.p, m, l, m,
-                                                                   Qt.p, m);
-    BRSVD_CHECK_LAUNCH();
-    Qop = Qt.p;
-  }
+  const T* Qop = Qw.p;
   ev.rec(2, c.stream);
   DBuf<T> Bt(c, (size_t)n * l);
   big_tn<T>(c, A, m, n, lda, row_major, Qop, m, l, Bt.p, n);
   info.words_read += m * n;
   info.block_reads += 1;
   ev.rec(3, c.stream);
-  Qt.release();
   DBuf<double> W(c, (size_t)l * l), sig(c, l);
   info.rank_b = small_svd_device<T>(c, Bt.p, n, l, n, W.p, sig.p, V, n, ns);
-  gemm_nn_cm<double, double, T>(c, m, l, l, Qw.p, m, W.p, l, U, m);
+  apply_basis<T>(c, Qw.p, m, l, m, W.p, l, l, U, m);
   fix_signs<T>(c, U, m, l, m, V, n, n);
   copy2d_kernel<double, T><<<1, 256, 0, c.stream>>>(sig.p, l, 1, l, sigma, l);
   BRSVD_CHECK_LAUNCH();

@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "gemm_simt.cuh"
+#include "gram_simt.cuh"
 #include "chol.cuh"
 #include "jacobi.cuh"
 #include "jacobi_cluster.cuh"
@@ -135,11 +136,60 @@ void gemm(Ctx& c, int64_t M, int64_t N, int64_t K, const TA* A, int64_t sam,
   }
 }
 
+// Tall-skinny fp64 Gram C (a x b) = X^T Y (gram_simt.cuh), deterministic
+// split-K; symmetric when X is Y.
+template <typename TX, typename TY, int BT>
+void gram_fp64_bt(Ctx& c, int64_t a, int64_t b, int64_t r, const TX* X, int64_t ldx,
+                  const TY* Y, int64_t ldy, double* C, int64_t ldc, bool sym) {
+  using namespace gram;
+  const int nti = (int)ceil_div(a, BT), ntj = (int)ceil_div(b, BT);
+  const int tiles = sym ? nti * (nti + 1) / 2 : nti * ntj;
+  const int per_sm = Cfg<BT>::NT <= 288 ? 2 : 1;
+  int64_t splits = std::max<int64_t>(1, ceil_div((int64_t)per_sm * c.num_sms, tiles));
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, r / (4 * BK)));
+  int64_t kchunk = ceil_div(ceil_div(r, splits), BK) * BK;
+  splits = ceil_div(r, kchunk);
+  DBuf<double> part(c, (size_t)(splits * a * b));
+  static bool attr = false;
+  if (!attr) {
+    BRSVD_CUDA(cudaFuncSetAttribute(gram_tile_kernel<TX, TY, BT>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)Cfg<BT>::SMEM));
+    attr = true;
+  }
+  gram_tile_kernel<TX, TY, BT><<<dim3(tiles, (unsigned)splits), Cfg<BT>::NT, Cfg<BT>::SMEM,
+                                 c.stream>>>(r, (int)a, (int)b, X, ldx, Y, ldy, sym ? 1 : 0,
+                                             ntj, kchunk, part.p);
+  BRSVD_CHECK_LAUNCH();
+  gram_reduce_kernel<<<grid_for(a * b), 256, 0, c.stream>>>(part.p, (int)a, (int)b,
+                                                            (int)splits, sym ? 1 : 0, BT, C,
+                                                            ldc);
+  BRSVD_CHECK_LAUNCH();
+}
+
+// Tall-skinny fp64 Gram C (a x b) = X^T Y (gram_simt.cuh), deterministic
+// split-K; symmetric when X is Y.  The tile size pads a, b least.
+template <typename TX, typename TY>
+void gram_fp64(Ctx& c, int64_t a, int64_t b, int64_t r, const TX* X, int64_t ldx,
+               const TY* Y, int64_t ldy, double* C, int64_t ldc) {
+  const bool sym = (a == b) && ((const void*)X == (const void*)Y) && ldx == ldy;
+  const int64_t w96 = ceil_div(a, 96) * ceil_div(b, 96) * 96 * 96;
+  const int64_t w128 = ceil_div(a, 128) * ceil_div(b, 128) * 128 * 128;
+  if (w96 < w128)
+    gram_fp64_bt<TX, TY, 96>(c, a, b, r, X, ldx, Y, ldy, C, ldc, sym);
+  else
+    gram_fp64_bt<TX, TY, 128>(c, a, b, r, X, ldx, Y, ldy, C, ldc, sym);
+}
+
 // Column-major helpers: C = op(X)... written out for readability.
 //   XtY:  C (a x b) = X(r x a)^T Y(r x b)
 template <typename TX, typename TY, typename TC>
 void gemm_tn_cm(Ctx& c, int64_t a, int64_t b, int64_t r, const TX* X, int64_t ldx,
                 const TY* Y, int64_t ldy, TC* C, int64_t ldc) {
+  if (sizeof(TC) == 8 && r >= 2048 && a >= 32 && b >= 32) {
+    gram_fp64<TX, TY>(c, a, b, r, X, ldx, Y, ldy, reinterpret_cast<double*>(C), ldc);
+    return;
+  }
   gemm<TX, TY, double, TC>(c, a, b, r, X, ldx, 1, Y, 1, ldy, C, 1, ldc);
 }
 //   XT:  C (r x b) = alpha X(r x a) T(a x b) + beta C0
@@ -356,325 +406,6 @@ void gram_eig(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* E,
 
 inline double orth_tau(int64_t r, int l) {
   return 8.0 * (double)std::max<int64_t>(r, l) * 2.220446049250313e-16;
-}
-
-constexpr int kCholMaxL = 384;  // chol_kernel shared-memory limit (~197 KB)
-
-// Cholesky basis change of X (r x l): with s_j = 1/||x_j|| and the scaled Gram
-// G~ = S X^T X S, factor G~ + shift I = L L^T and return T = S L^-T in Tm
-// (l x l, column-major).  Returns min pivot / diagonal (1 = orthogonal
-// columns, ~1/cond^2 otherwise, <= 0 on breakdown) when `ratio` is requested.
-struct CholInfo {
-  double min_ratio = 0.0;  // min pivot / diagonal over the kept columns
-  int rank_ref = 0;        // reference-style |diag R| rank (kernels.py:155-157)
-  int kept = 0;            // columns kept by the rank-revealing pass
-};
-
-// Cholesky basis change of X (r x l): with s_j = 1/||x_j|| and the scaled Gram
-// G~ = S X^T X S, factor G~ + shift I = L L^T and return T = S L^-T in Tm
-// (l x l, column-major).  drop_ratio > 0 drops (in column order) the columns
-// whose pivot falls below it; `keep` (device, l ints) then lists the kept
-// columns.  Host-visible diagnostics only when `sync` is set.
-template <typename T>
-CholInfo chol_basis(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double shift,
-                    double* Tm, bool sync, double col_drop = 0.0, double rank_tol = 0.0,
-                    double drop_ratio = 0.0, int* keep = nullptr,
-                    double* info_dev = nullptr) {
-  DBuf<double> G(c, (size_t)l * l), W(c, (size_t)l * l), infob;
-  double* info = info_dev;
-  if (!info) {
-    infob.alloc(c, 3);
-    info = infob.p;
-  }
-  gemm_tn_cm<T, T, double>(c, l, l, r, X, ldx, X, ldx, G.p, l);
-  cholinv_launch(c.stream, c.max_smem_optin, G.p, l, l, 1, col_drop, shift, drop_ratio,
-                 rank_tol, W.p, Tm, nullptr, info, keep);
-  BRSVD_CHECK_LAUNCH();
-  CholInfo ci;
-  if (sync) {
-    double h[3];
-    readback(c, info, h, sizeof(h));
-    ci.min_ratio = h[0];
-    ci.rank_ref = (int)h[1];
-    ci.kept = (int)h[2];
-  }
-  return ci;
-}
-
-inline void set_chol_attrs(Ctx& c) {
-  static bool done = false;
-  if (done) return;
-  const int lim = (int)c.max_smem_optin - 2048;  // leave room for static smem
-  BRSVD_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
-  BRSVD_CUDA(cudaFuncSetAttribute(trinv_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  lim));
-  done = true;
-}
-
-// Basis change for the power iteration: Xout spans range(X) with restored
-// conditioning.  Shifted Cholesky QR (shift ~ l*eps of the unit diagonal,
-// never breaks down) when l fits the Cholesky kernel, else the regularised
-// Gram-eigen basis X S E Lam^-1/2 (eigenvalues floored at tau*lam_0).  No
-// host synchronisation either way.
-template <typename T>
-void normalize_sketch(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, T* Xout,
-                      int64_t ldo) {
-  DBuf<double> Tm(c, (size_t)l * l);
-  if (l <= kCholMaxL) {
-    set_chol_attrs(c);
-    chol_basis<T>(c, X, r, l, ldx, 16.0 * l * 2.220446049250313e-16, Tm.p, false);
-  } else {
-    DBuf<double> E(c, (size_t)l * l), lam(c, l), s(c, l);
-    gram_eig<T>(c, X, r, l, ldx, E.p, lam.p, s.p, kJacobiTolNormalize);
-    build_basis_kernel<<<1, 1024, 0, c.stream>>>(E.p, lam.p, s.p, l, orth_tau(r, l), 0,
-                                                 Tm.p, nullptr);
-    BRSVD_CHECK_LAUNCH();
-  }
-  gemm_nn_cm<T, double, T>(c, r, l, l, X, ldx, Tm.p, l, Xout, ldo);
-}
-
-// Block projection X <- X - Qb (Qb^T X), applied twice ("twice is enough").
-inline void project_out(Ctx& c, const double* Qb, int64_t r, int kq, double* X,
-                        int cols) {
-  if (kq <= 0 || cols <= 0) return;
-  DBuf<double> Cm(c, (size_t)kq * cols);
-  for (int pass = 0; pass < 2; ++pass) {
-    gemm_tn_cm<double, double, double>(c, kq, cols, r, Qb, r, X, r, Cm.p, kq);
-    gemm_nn_cm<double, double, double>(c, r, cols, kq, Qb, r, Cm.p, kq, X, r, -1.0,
-                                       1.0, X, r);
-  }
-}
-
-// Newton-Schulz polar refinement of the r x k block Q: Q <- Q (1.5 I - 0.5 Q^T Q).
-inline void ns_refine(Ctx& c, double* Q, int64_t r, int k, int iters) {
-  if (k <= 0 || iters <= 0) return;
-  DBuf<double> G2(c, (size_t)k * k), T2(c, (size_t)k * k), Qt(c, (size_t)r * k);
-  for (int it = 0; it < iters; ++it) {
-    gemm_tn_cm<double, double, double>(c, k, k, r, Q, r, Q, r, G2.p, k);
-    ns_matrix_kernel<<<grid_for((int64_t)k * k), 256, 0, c.stream>>>(G2.p, k, T2.p);
-    BRSVD_CHECK_LAUNCH();
-    gemm_nn_cm<double, double, double>(c, r, k, k, Q, r, T2.p, k, Qt.p, r);
-    BRSVD_CUDA(cudaMemcpyAsync(Q, Qt.p, sizeof(double) * r * k,
-                               cudaMemcpyDeviceToDevice, c.stream));
-  }
-}
-
-// Deflation levels: the part of X that level 1 left unresolved,
-// R = (I - Q Q^T) X, is re-factored with an unscaled Gram (eigen route, so the
-// threshold is relative to R's own scale) while ||R||_F^2 > stop2.  A Gram
-// resolves directions down to ~sqrt(tau) of its largest, Householder QR (the
-// reference's tsqr, kernels.py:121-164) down to eps; each level buys another
-// factor sqrt(tau).  Appends columns to Q and to the reported rank.
-template <typename T>
-void deflate_levels(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* Q,
-                    int& total, int& rank, double stop2, double tau, int ns_iters) {
-  if (total >= l || !(stop2 > 0.0)) return;
-  DBuf<double> E(c, (size_t)l * l), lam(c, l), s(c, l), Tm(c, (size_t)l * l);
-  DBuf<double> scal(c, 4);
-  DBuf<int> drank(c, 1);
-  DBuf<double> R(c, (size_t)r * l);
-  copy2d_kernel<T, double><<<grid_for(r * l), 256, 0, c.stream>>>(X, r, l, ldx, R.p, r);
-  BRSVD_CHECK_LAUNCH();
-  DBuf<double> G(c, (size_t)l * l), V(c, (size_t)l * l);
-  for (int level = 0; level < 4 && total < l; ++level) {
-    project_out(c, Q, r, total, R.p, l);
-    // ||R||_F^2 first: most calls stop here without an eigen-solve
-    gemm_tn_cm<double, double, double>(c, l, l, r, R.p, r, R.p, r, G.p, l);
-    gram_prep_kernel<<<1, 1024, 0, c.stream>>>(G.p, l, s.p, V.p, 0, scal.p, 0.0);
-    BRSVD_CHECK_LAUNCH();
-    double nr2;
-    readback(c, scal.p, &nr2, sizeof(double));
-    if (!(nr2 > stop2)) break;
-    jacobi(c, G.p, l, l, l, V.p, l, kJacobiTolOrth);
-    jacobi_finish(c, G.p, l, l, l, V.p, l, lam.p, nullptr, 0, E.p, l);
-    build_basis_kernel<<<1, 1024, 0, c.stream>>>(E.p, lam.p, s.p, l, tau, 1, Tm.p,
-                                                 drank.p);
-    BRSVD_CHECK_LAUNCH();
-    int rk2 = read_int(c, drank.p);
-    if (rk2 <= 0) break;
-    rk2 = std::min(rk2, l - total);
-    double* Qn = Q + (int64_t)total * r;
-    gemm_nn_cm<double, double, double>(c, r, rk2, l, R.p, r, Tm.p, l, Qn, r);
-    project_out(c, Q, r, total, Qn, rk2);
-    ns_refine(c, Qn, r, rk2, std::max(ns_iters, 1));
-    total += rk2;
-    rank += rk2;
-  }
-}
-
-template <typename T>
-int orth_full(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* Q,
-              uint64_t seed, int ns_iters);
-
-// Numerically null directions: Gaussian columns projected out twice and
-// orthonormalised (kernels.py:142-144, "columns of Q remain orthonormal").
-inline void complete_basis(Ctx& c, double* Q, int64_t r, int l, int total, uint64_t seed,
-                           int ns_iters) {
-  if (total >= l) return;
-  const int cnt = l - total;
-  double* W = Q + (int64_t)total * r;
-  gaussian_kernel<double><<<grid_for(r * ((cnt + 1) / 2)), 256, 0, c.stream>>>(
-      W, r, cnt, r, seed, 0x636f6d706c657465ull, 0);
-  BRSVD_CHECK_LAUNCH();
-  project_out(c, Q, r, total, W, cnt);
-  DBuf<double> Wq(c, (size_t)r * cnt);
-  orth_full<double>(c, W, r, cnt, r, Wq.p, seed * 0x9E3779B97F4A7C15ull + 1,
-                    std::max(ns_iters, 1));
-  BRSVD_CUDA(cudaMemcpyAsync(W, Wq.p, sizeof(double) * r * cnt, cudaMemcpyDeviceToDevice,
-                             c.stream));
-  project_out(c, Q, r, total, W, cnt);
-  ns_refine(c, W, r, cnt, 1);
-}
-
-// Rank-revealing orthonormal basis of range(X), X (r x l), r >= l
-// (tsqr / tsqr_factor, kernels.py:139-170).  Returns the detected numerical
-// rank; Q is r x l, fp64, ld r, always with l orthonormal columns.
-//
-// Level 1 (l <= kCholMaxL): rank-revealing Cholesky QR in column order.
-// Columns whose pivot falls below 1e-12 of their norm lie numerically in the
-// span of the earlier ones and are set aside; the kept ones get a second
-// CholQR pass (orthonormal to rounding).  The reported rank is the
-// reference's |diag R| > l eps ||X||_F cut, since the Cholesky factor of the
-// Gram is the R of an unpivoted QR (kernels.py:155-157).
-// Level 1 (larger l): Gram eigenpairs by Jacobi, keep lam > tau lam_0.
-// Then deflation levels for what is still resolvable in the data's precision
-// and a Gaussian completion of the null directions.
-template <typename T>
-int orth_full(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* Q,
-              uint64_t seed, int ns_iters) {
-  const double eps_data = sizeof(T) == 8 ? 2.220446049250313e-16 : 1.1920928955078125e-07;
-  const double tau = orth_tau(r, l);
-  const double drop = 4.0 * l * eps_data;  // the reference's rank cut, kernels.py:155-157
-  int total = 0, rank = 0;
-  double normx2 = 0.0;
-  if (l <= kCholMaxL) {
-    set_chol_attrs(c);
-    DBuf<int> keep(c, l);
-    DBuf<double> info(c, 3), Tm(c, (size_t)l * l), Tc(c, (size_t)l * l);
-    const CholInfo ci = chol_basis<T>(c, X, r, l, ldx, 0.0, Tm.p, true, drop, l * eps_data,
-                                      1e-12, keep.p, info.p);
-    const int k1 = ci.kept;
-    if (sizeof(T) == 4 && k1 < l) {
-      // fp32 data: the dropped directions are below the data's resolution.
-      // Complete in the same second CholQR pass: [Q1 | Gaussian columns] is
-      // well conditioned, so one pass returns l orthonormal columns whose
-      // first k1 span the kept part of range(X) (kernels.py:142-144, "columns
-      // of Q remain orthonormal").
-      DBuf<double> Q1(c, (size_t)r * l);
-      if (k1 > 0) {
-        compact_cols_kernel<<<grid_for((int64_t)l * k1), 256, 0, c.stream>>>(
-            Tm.p, l, keep.p, info.p, Tc.p);
-        BRSVD_CHECK_LAUNCH();
-        gemm_nn_cm<T, double, double>(c, r, k1, l, X, ldx, Tc.p, l, Q1.p, r);
-      }
-      const int cnt = l - k1;
-      gaussian_kernel<double><<<grid_for(r * ((cnt + 1) / 2)), 256, 0, c.stream>>>(
-          Q1.p + (int64_t)k1 * r, r, cnt, r, seed, 0x636f6d706c657465ull, 0);
-      BRSVD_CHECK_LAUNCH();
-      chol_basis<double>(c, Q1.p, r, l, r, 0.0, Tm.p, false);
-      gemm_nn_cm<double, double, double>(c, r, l, l, Q1.p, r, Tm.p, l, Q, r);
-      return std::min(ci.rank_ref, k1);
-    }
-    if (k1 > 0) {
-      const double* Tk = Tm.p;
-      if (k1 < l) {
-        compact_cols_kernel<<<grid_for((int64_t)l * k1), 256, 0, c.stream>>>(
-            Tm.p, l, keep.p, info.p, Tc.p);
-        BRSVD_CHECK_LAUNCH();
-        Tk = Tc.p;
-      }
-      DBuf<double> Q1(c, (size_t)r * k1);
-      gemm_nn_cm<T, double, double>(c, r, k1, l, X, ldx, Tk, l, Q1.p, r);
-      chol_basis<double>(c, Q1.p, r, k1, r, 0.0, Tm.p, false);
-      gemm_nn_cm<double, double, double>(c, r, k1, k1, Q1.p, r, Tm.p, k1, Q, r);
-      if (ns_iters > 1) ns_refine(c, Q, r, k1, 1);
-    }
-    total = k1;
-    rank = std::min(ci.rank_ref, k1);
-    if (total == l) return rank;
-    if (sizeof(T) == 4) {
-      complete_basis(c, Q, r, l, total, seed, ns_iters);
-      return rank;
-    }
-    // ||X||_F^2 for the deflation stop rule
-    DBuf<double> nf(c, 1);
-    DBuf<double> G(c, (size_t)l * l), Wd(c, (size_t)l * l), sd(c, l);
-    gemm_tn_cm<T, T, double>(c, l, l, r, X, ldx, X, ldx, G.p, l);
-    gram_prep_kernel<<<1, 1024, 0, c.stream>>>(G.p, l, sd.p, Wd.p, 0, nf.p, 0.0);
-    BRSVD_CHECK_LAUNCH();
-    readback(c, nf.p, &normx2, sizeof(double));
-  } else {
-    DBuf<double> E(c, (size_t)l * l), lam(c, l), s(c, l), Tm(c, (size_t)l * l);
-    DBuf<double> scal(c, 4);
-    DBuf<int> drank(c, 1);
-    gram_eig<T>(c, X, r, l, ldx, E.p, lam.p, s.p, kJacobiTolOrth, true, scal.p, drop);
-    build_basis_kernel<<<1, 1024, 0, c.stream>>>(E.p, lam.p, s.p, l, tau, 1, Tm.p, drank.p);
-    BRSVD_CHECK_LAUNCH();
-    BRSVD_CUDA(cudaMemcpyAsync(scal.p + 1, drank.p, sizeof(int), cudaMemcpyDeviceToDevice,
-                               c.stream));
-    double hs[2];
-    readback(c, scal.p, hs, sizeof(hs));
-    normx2 = hs[0];
-    std::memcpy(&total, &hs[1], sizeof(int));
-    rank = total;
-    if (total > 0) {
-      gemm_nn_cm<T, double, double>(c, r, total, l, X, ldx, Tm.p, l, Q, r);
-      ns_refine(c, Q, r, total, ns_iters);
-    }
-  }
-  // fp64 data only: for fp32 data the level-1 cut (1e-6 of a column's norm)
-  // is already below the reference's own rank cut (l eps32 ||X||_F).
-  if (sizeof(T) == 8 && total < l && normx2 > 0.0)
-    deflate_levels<T>(c, X, r, l, ldx, Q, total, rank, drop * drop * normx2, tau, ns_iters);
-  complete_basis(c, Q, r, l, total, seed, ns_iters);
-  return rank;
-}
-
-// ---------------------------------------------------------------------------
-// small_svd (kernels.py:173-188): B^T (n x l, given as Bt) = Qb R,
-// R^T = W diag(sigma) Zj^T  (one-sided Jacobi),  V = Qb Zj.
-// Outputs: W (l x l fp64, ld l), sigma (fp64), Vout (n x l, T, ld ldv).
-template <typename T>
-int small_svd_device(Ctx& c, const T* Bt, int64_t n, int l, int64_t ldb, double* W,
-                     double* sigma, T* Vout, int64_t ldv, int ns_iters) {
-  DBuf<double> Qb(c, (size_t)n * l), M(c, (size_t)l * l), Vj(c, (size_t)l * l),
-      Zj(c, (size_t)l * l);
-  const int rank = orth_full<T>(c, Bt, n, l, ldb, Qb.p, 0x5eedb5ull, ns_iters);
-  // M = Bt^T Qb = R^T
-  gemm_tn_cm<T, double, double>(c, l, l, n, Bt, ldb, Qb.p, n, M.p, l);
-  if (l > 64) {
-    // Two-phase Jacobi: sweeps in fp32 (native rsqrt/rcp, half the shuffles
-    // and shared memory) down to ~1e-5 orthogonality, then the fp64 sweeps
-    // start from M V0 with V0 polished to an fp64-orthogonal matrix; the
-    // quadratic convergence leaves only ~2 fp64 sweeps.
-    DBuf<float> M32(c, (size_t)l * l), V32(c, (size_t)l * l);
-    copy2d_kernel<double, float><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(M.p, l, l, l,
-                                                                                M32.p, l);
-    eye_kernel<float><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(V32.p, l);
-    BRSVD_CHECK_LAUNCH();
-    jacobi<float>(c, M32.p, l, l, l, V32.p, l, 1e-5, 40, 16.0 * l * 2.220446049250313e-16);
-    copy2d_kernel<float, double><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(V32.p, l, l, l,
-                                                                                Vj.p, l);
-    BRSVD_CHECK_LAUNCH();
-    ns_refine(c, Vj.p, l, l, 2);
-    DBuf<double> M1(c, (size_t)l * l);
-    gemm_nn_cm<double, double, double>(c, l, l, l, M.p, l, Vj.p, l, M1.p, l);
-    BRSVD_CUDA(cudaMemcpyAsync(M.p, M1.p, sizeof(double) * l * l, cudaMemcpyDeviceToDevice,
-                               c.stream));
-  } else {
-    eye_kernel<double><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(Vj.p, l);
-    BRSVD_CHECK_LAUNCH();
-  }
-  // fp32 data: singular vectors orthogonal to 1e-7 (the output precision) and
-  // singular values to ~1e-14 relative; fp64 data: tight.
-  const double tol = sizeof(T) == 8 ? jacobi_tol_tight(l) : 1e-7;
-  jacobi(c, M.p, l, l, l, Vj.p, l, tol);
-  jacobi_finish(c, M.p, l, l, l, Vj.p, l, sigma, W, l, Zj.p, l);
-  complete_null_columns_kernel<<<1, 1024, (size_t)l * sizeof(double), c.stream>>>(
-      W, l, l, l, sigma, 16.0 * l * 2.220446049250313e-16);
-  BRSVD_CHECK_LAUNCH();
-  gemm_nn_cm<double, double, T>(c, n, l, l, Qb.p, n, Zj.p, l, Vout, ldv);
-  return rank;
 }
 
 template <typename T>

@@ -179,18 +179,9 @@ RsvdInfo rsvd_stream(Ctx& c, const T* Ah, int64_t m, int64_t n, int64_t lda, boo
   }
   ev.rec(1, c.stream);
   const int ns = sizeof(T) == 8 ? 2 : 1;
-  DBuf<double> Qw(c, (size_t)m * l);
+  DBuf<T> Qw(c, (size_t)m * l);
   info.rank_y = orth_full<T>(c, Y.p, m, l, m, Qw.p, seed ^ 0x7153ull, ns);
-  DBuf<T> Qt;
-  const T* Qop;
-  if (sizeof(T) == 8) {
-    Qop = reinterpret_cast<const T*>(Qw.p);
-  } else {
-    Qt.alloc(c, (size_t)m * l);
-    copy2d_kernel<double, T><<<grid_for(m * l), 256, 0, c.stream>>>(Qw.p, m, l, m, Qt.p, m);
-    BRSVD_CHECK_LAUNCH();
-    Qop = Qt.p;
-  }
+  const T* Qop = Qw.p;
   ev.rec(2, c.stream);
   DBuf<T> Bt(c, (size_t)n * l);
   if (row_major) BRSVD_CUDA(cudaMemsetAsync(Bt.p, 0, sizeof(T) * n * l, c.stream));
@@ -207,7 +198,7 @@ RsvdInfo rsvd_stream(Ctx& c, const T* Ah, int64_t m, int64_t n, int64_t lda, boo
   Y.release();
   DBuf<double> W(c, (size_t)l * l), sig(c, l);
   info.rank_b = small_svd_device<T>(c, Bt.p, n, l, n, W.p, sig.p, V, n, ns);
-  gemm_nn_cm<double, double, T>(c, m, l, l, Qw.p, m, W.p, l, U, m);
+  apply_basis<T>(c, Qw.p, m, l, m, W.p, l, l, U, m);
   fix_signs<T>(c, U, m, l, m, V, n, n);
   copy2d_kernel<double, T><<<1, 256, 0, c.stream>>>(sig.p, l, 1, l, sigma, l);
   BRSVD_CHECK_LAUNCH();

@@ -43,9 +43,10 @@ constexpr uint32_t A_STAGE_BYTES = BM * BK * 4;
 struct Params {
   int64_t M, K;
   int npad, nchunks, rows_c, n_out;
-  int ksplit;  // 1 or 2 K-halves per tile (2: atomicAdd of two partials)
+  int ksplit;  // K-splits per tile (part == nullptr: 1 or 2, atomicAdd of two partials)
   float* C;
   int64_t ldc;
+  float* part;  // split-K workspace: split s writes its partial to part + s * M * n_out
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -361,9 +362,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < NH; ++j) {
         const int col = n0 + c0 + j;
         if (j < hc && col < p.n_out) {
-          float* dst = p.C + row + (int64_t)col * p.ldc;
-          if (p.ksplit > 1) atomicAdd(dst, run[j]);   // two partial sums: order-free
-          else *dst = run[j];
+          if (p.part != nullptr) {
+            p.part[(int64_t)ks * p.M * p.n_out + row + (int64_t)col * p.M] = run[j];
+          } else {
+            float* dst = p.C + row + (int64_t)col * p.ldc;
+            if (p.ksplit > 1) atomicAdd(dst, run[j]);   // two partial sums: order-free
+            else *dst = run[j];
+          }
         }
       }
     }
@@ -470,12 +475,13 @@ bool tc_gemm_supported(Ctx& c, const T* A, int64_t lda, int64_t m, int64_t n, in
 
 template <typename T>
 void tc_gemm_launch(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool row_major,
-                    bool trans, const T* X, int64_t ldx, int l, T* C, int64_t ldc);
+                    bool trans, const T* X, int64_t ldx, int l, T* C, int64_t ldc,
+                    int splits = 0, float* part = nullptr);
 
 template <>
 inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, int64_t lda,
                                   bool row_major, bool trans, const float* X, int64_t ldx,
-                                  int l, float* C, int64_t ldc) {
+                                  int l, float* C, int64_t ldc, int splits, float* part) {
   using namespace tc;
   const int64_t M = trans ? n : m, K = trans ? m : n;
   const bool kmajor = row_major != trans;
@@ -509,11 +515,13 @@ inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, 
   // atomicAdd into a zeroed C, which is order-independent for two terms.
   const int64_t tiles = ceil_div(M, BM) * g.nchunks;
   const double waves = (double)tiles / c.num_sms;
+  p.part = part;
   p.ksplit = (K >= 8192 && waves > 1.0 && waves < 8.0 &&
               waves - std::floor(waves) > 0.0 && waves - std::floor(waves) < 0.75)
                  ? 2
                  : 1;
-  if (p.ksplit > 1)
+  if (part != nullptr) p.ksplit = splits;
+  else if (p.ksplit > 1)
     BRSVD_CUDA(cudaMemset2DAsync(C, (size_t)ldc * sizeof(float), 0, (size_t)M * sizeof(float),
                                  (size_t)l, c.stream));
   const size_t smem = smem_bytes(g.rows_c);
@@ -543,8 +551,41 @@ inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, 
 
 template <>
 inline void tc_gemm_launch<double>(Ctx&, const double*, int64_t, int64_t, int64_t, bool, bool,
-                                   const double*, int64_t, int, double*, int64_t) {
+                                   const double*, int64_t, int, double*, int64_t, int, float*) {
   throw Error(kErrArg, "tcgen05 path is fp32-only");
+}
+
+// Fixed-order sum of the split-K partials (deterministic), fp64 output.
+__global__ void splitk_sum_kernel(const float* __restrict__ part, int64_t M, int64_t N,
+                                  int splits, double* __restrict__ C, int64_t ldc) {
+  const int64_t total = M * N;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += (double)part[(int64_t)z * total + idx];
+    C[(idx % M) + (idx / M) * ldc] = s;
+  }
+}
+
+// C (a x b, fp64) = X^T Y for tall-skinny fp32 X (r x a), Y (r x b): the
+// tcgen05 3xTF32 product with the long K = r split over CTAs (fp32 partial
+// sums of <= r / splits terms, summed in fp64 in a fixed order).  fp32-level
+// accuracy: for Grams of well-conditioned bases only.
+inline bool tc_gram(Ctx& c, const float* X, int64_t r, int a, int64_t ldx, const float* Y,
+                    int64_t ldy, int b, double* C, int64_t ldc) {
+  if (!tc_gemm_supported<float>(c, X, ldx, r, a, b) || r < 1024) return false;
+  const tc::Geometry g = tc::geometry(b);
+  const int64_t tiles = ceil_div(a, tc::BM) * g.nchunks;
+  int splits = (int)std::max<int64_t>(1, ceil_div(2 * c.num_sms, tiles));
+  splits = (int)std::min<int64_t>(splits, ceil_div(r, 512));
+  DBuf<float> part(c, (size_t)splits * a * b);
+  // Z = A^T Y with A = X (r x a, column-major): trans=true
+  tc_gemm_launch<float>(c, X, r, a, ldx, /*row_major=*/false, /*trans=*/true, Y, ldy, b,
+                        nullptr, 0, splits, part.p);
+  splitk_sum_kernel<<<grid_for((int64_t)a * b), 256, 0, c.stream>>>(part.p, a, b, splits, C,
+                                                                    ldc);
+  BRSVD_CHECK_LAUNCH();
+  return true;
 }
 
 }  // namespace brsvd
