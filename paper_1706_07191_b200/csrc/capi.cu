@@ -240,20 +240,35 @@ int brsvd_rsvd(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda,
     // A as a column-major (rows x cols) array: row-major A is A^T col-major.
     const int64_t a_rows = row_major ? n : m, a_cols = row_major ? m : n;
     BRSVD_REQUIRE(lda >= a_rows, kErrShape, "lda too small");
-    InView av(c, A, a_rows, a_cols, lda, es, a_where);
+    // host input: the pipeline streams A in (H2D overlapped with the sample
+    // pass, HostFeed); device input is used in place
+    const bool on_host = a_where != BRSVD_DEVICE;
+    InView av(c, on_host ? nullptr : A, a_rows, a_cols, lda, es, BRSVD_DEVICE);
+    DBuf<unsigned char> adev;
+    HostFeed feed;
+    const void* aptr = av.dptr;
+    int64_t ald = av.ld;
+    if (on_host) {
+      adev.alloc(c, (size_t)a_rows * a_cols * es);
+      aptr = adev.p;
+      ald = a_rows;
+      feed.host = A;
+      feed.ldh = lda;
+    }
     InView ov(c, omega, n, l, n, es, omega ? omega_where : BRSVD_DEVICE);
     OutView uo(c, U, (size_t)m * l * es, out_where);
     OutView so(c, sigma, (size_t)l * es, out_where);
     OutView vo(c, Vt, (size_t)n * l * es, out_where);
     RsvdInfo info;
     if (dtype == BRSVD_F64) {
-      info = rsvd_device<double>(c, (const double*)av.dptr, m, n, av.ld, row_major, k,
-                                 p, q, (const double*)ov.dptr, seed, (double*)uo.dptr,
-                                 (double*)so.dptr, (double*)vo.dptr);
+      info = rsvd_device<double>(c, (const double*)aptr, m, n, ald, row_major, k, p, q,
+                                 (const double*)ov.dptr, seed, (double*)uo.dptr,
+                                 (double*)so.dptr, (double*)vo.dptr,
+                                 on_host ? &feed : nullptr);
     } else {
-      info = rsvd_device<float>(c, (const float*)av.dptr, m, n, av.ld, row_major, k, p,
-                                q, (const float*)ov.dptr, seed, (float*)uo.dptr,
-                                (float*)so.dptr, (float*)vo.dptr);
+      info = rsvd_device<float>(c, (const float*)aptr, m, n, ald, row_major, k, p, q,
+                                (const float*)ov.dptr, seed, (float*)uo.dptr,
+                                (float*)so.dptr, (float*)vo.dptr, on_host ? &feed : nullptr);
     }
     uo.flush();
     so.flush();

@@ -7,6 +7,7 @@
 // match the reference's to rounding while the sketch never overflows or loses
 // rank to cancellation.
 #pragma once
+#include <vector>
 #include "orth.cuh"
 
 namespace brsvd {
@@ -41,10 +42,86 @@ struct StageEvents {
   }
 };
 
+// Host-resident input: A (device, ld lda, allocated by the caller) is filled
+// from host memory by the pipeline itself so that the H2D transfer overlaps
+// the sample pass.  Row-major A arrives in row panels on a copy stream and
+// Y[rows] = A[rows, :] X is computed per panel as soon as it lands (the
+// remaining passes need all of A); column-major A is copied whole first.
+struct HostFeed {
+  const void* host = nullptr;
+  int64_t ldh = 0;   // host leading dimension (elements)
+  int panels = 8;
+};
+
+template <typename T>
+__global__ void sum_slices_kernel(const T* __restrict__ parts, int64_t count, int slices,
+                                  T* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    T s = T(0);
+    for (int z = 0; z < slices; ++z) s += parts[(int64_t)z * count + i];
+    out[i] = s;
+  }
+}
+
+// Returns true when Z = A^T Y (n x l) was also formed panel by panel
+// (Z += A_i^T Y_i, the fused power step of the north star: each panel is used
+// for both products while it is fresh), so the first transpose pass is done
+// by the time the transfer completes.
+template <typename T>
+bool feed_and_sample(Ctx& c, T* A, int64_t m, int64_t n, int64_t lda, bool row_major,
+                     const HostFeed& f, const T* X, int l, T* Y, T* Z) {
+  const int64_t a_rows = row_major ? n : m, a_cols = row_major ? m : n;
+  if (!row_major) {
+    BRSVD_CUDA(cudaMemcpy2DAsync(A, lda * sizeof(T), f.host, f.ldh * sizeof(T),
+                                 a_rows * sizeof(T), a_cols, cudaMemcpyHostToDevice,
+                                 c.stream));
+    big_nn<T>(c, A, m, n, lda, row_major, X, n, l, Y, m);
+    return false;
+  }
+  cudaStream_t cs;
+  BRSVD_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaEvent_t ready;
+  BRSVD_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  // the copy stream must not overwrite A before earlier work on it finished
+  BRSVD_CUDA(cudaEventRecord(ready, c.stream));
+  BRSVD_CUDA(cudaStreamWaitEvent(cs, ready, 0));
+  const int P = (int)std::max<int64_t>(1, std::min<int64_t>(f.panels, m / 128));
+  const int64_t step = ceil_div(ceil_div(m, P), 128) * 128;
+  const int npan = (int)ceil_div(m, step);
+  DBuf<T> Zp;
+  if (Z != nullptr) Zp.alloc(c, (size_t)npan * n * l);
+  std::vector<cudaEvent_t> evs;
+  int pi = 0;
+  for (int64_t r0 = 0; r0 < m; r0 += step, ++pi) {
+    const int64_t r1 = std::min(m, r0 + step);
+    const T* src = reinterpret_cast<const T*>(f.host) + r0 * f.ldh;
+    BRSVD_CUDA(cudaMemcpy2DAsync(A + r0 * lda, lda * sizeof(T), src, f.ldh * sizeof(T),
+                                 n * sizeof(T), r1 - r0, cudaMemcpyHostToDevice, cs));
+    cudaEvent_t e;
+    BRSVD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    BRSVD_CUDA(cudaEventRecord(e, cs));
+    evs.push_back(e);
+    BRSVD_CUDA(cudaStreamWaitEvent(c.stream, e, 0));
+    big_nn<T>(c, A + r0 * lda, r1 - r0, n, lda, true, X, n, l, Y + r0, m);
+    if (Z != nullptr)
+      big_tn<T>(c, A + r0 * lda, r1 - r0, n, lda, true, Y + r0, m, l,
+                Zp.p + (int64_t)pi * n * l, n);
+  }
+  if (Z != nullptr) {
+    sum_slices_kernel<T><<<grid_for(n * l), 256, 0, c.stream>>>(Zp.p, n * l, npan, Z);
+    BRSVD_CHECK_LAUNCH();
+  }
+  for (auto e : evs) cudaEventDestroy(e);
+  cudaEventDestroy(ready);
+  cudaStreamDestroy(cs);  // returns at once; the stream is released when its work is done
+  return Z != nullptr;
+}
+
 template <typename T>
 RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
                      bool row_major, int k, int p, int q, const T* omega,
-                     uint64_t seed, T* U, T* sigma, T* V) {
+                     uint64_t seed, T* U, T* sigma, T* V, const HostFeed* feed = nullptr) {
   const int l = k + p;
   RsvdInfo info;
   StageEvents ev;
@@ -59,7 +136,12 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
     X = Xg.p;
   }
   DBuf<T> Y(c, (size_t)m * l), Z(c, (size_t)n * l), Zn(c, (size_t)n * l);
-  big_nn<T>(c, A, m, n, lda, row_major, X, n, l, Y.p, m);
+  bool z_ready = false;
+  if (feed != nullptr)
+    z_ready = feed_and_sample<T>(c, const_cast<T*>(A), m, n, lda, row_major, *feed, X, l, Y.p,
+                                 q > 0 ? Z.p : nullptr);
+  else
+    big_nn<T>(c, A, m, n, lda, row_major, X, n, l, Y.p, m);
   const MaxAbs p0 = maxabs<T>(c, Y.p, m, l, m);
   info.max_abs_y0 = p0.peak;
   bool nonfinite = p0.nonfinite;
@@ -69,7 +151,7 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
     return info;
   }
   for (int it = 0; it < q; ++it) {
-    big_tn<T>(c, A, m, n, lda, row_major, Y.p, m, l, Z.p, n);
+    if (!(it == 0 && z_ready)) big_tn<T>(c, A, m, n, lda, row_major, Y.p, m, l, Z.p, n);
     normalize_sketch<T>(c, Z.p, n, l, n, Zn.p, n);
     big_nn<T>(c, A, m, n, lda, row_major, Zn.p, n, l, Y.p, m);
   }

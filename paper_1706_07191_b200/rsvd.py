@@ -103,6 +103,22 @@ def _omega_arg(omega, n, l, dtype, device):
     return o, ctypes.c_void_p(o.ctypes.data), _lib.HOST
 
 
+def host_outputs(m, n, l, npdt):
+    """U (m x l, Fortran order) and Vt (l x n) as numpy arrays backed by
+    page-locked host memory (torch's caching host allocator), so the D2H copies
+    of the factors run at full PCIe rate instead of faulting in fresh pageable
+    pages; plain numpy arrays when pinning is unavailable."""
+    try:
+        import torch
+        tdt = torch.float64 if npdt == np.float64 else torch.float32
+        U = torch.empty((l, m), dtype=tdt, pin_memory=True).numpy().T
+        Vt = torch.empty((l, n), dtype=tdt, pin_memory=True).numpy()
+        return U, Vt
+    except (RuntimeError, ImportError):
+        return (np.empty((m, l), dtype=npdt, order="F"),
+                np.empty((l, n), dtype=npdt, order="C"))
+
+
 def run_rsvd(a, cfg, omega=None, warn=True):
     """One GPU decomposition; returns RsvdRun (factors + stats).
 
@@ -130,9 +146,8 @@ def run_rsvd(a, cfg, omega=None, warn=True):
     else:
         ctx = _lib.context()
         npdt = mat.dtype
-        U = np.empty((m, l), dtype=npdt, order="F")
+        U, Vt = host_outputs(m, n, l, npdt)
         sigma = np.empty(l, dtype=npdt)
-        Vt = np.empty((l, n), dtype=npdt, order="C")
         ptrs = [ctypes.c_void_p(x.ctypes.data) for x in (U, sigma, Vt)]
         where = _lib.HOST
     keep, optr, owhere = _omega_arg(omega, n, l, npdt, device)
@@ -196,9 +211,8 @@ def run_rsvd_stream(a, cfg, panel=None, nbuf=3, omega=None, warn=True):
     if panel is None:   # ~1 GiB panels
         panel = max(1, (1 << 30) // max(1, inner * mat.a.itemsize))
     ctx = _lib.context()
-    U = np.empty((m, l), dtype=mat.dtype, order="F")
+    U, Vt = host_outputs(m, n, l, mat.dtype)
     sigma = np.empty(l, dtype=mat.dtype)
-    Vt = np.empty((l, n), dtype=mat.dtype, order="C")
     keep, optr, owhere = _omega_arg(omega, n, l, mat.dtype, False)
     stats = _lib.BrsvdStats()
     t0 = time.perf_counter()
