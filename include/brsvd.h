@@ -127,6 +127,17 @@ BRSVD_API int brsvd_sketch_product(brsvd_ctx* ctx, const void* A, int64_t m, int
                                    const void* X, int64_t ldx, int64_t l, void* C,
                                    int64_t ldc);
 
+/* Fused residual of a rank-l factorisation, one pass over A
+ * (relative_frobenius_error, rsvd.py:396-432):
+ *   out[0] = ||A - U diag(sigma) Vt||_F^2,   out[1] = ||A||_F^2   (fp64, host)
+ * A (m x n, lda, layout), U (m x l column-major, ldu), sigma (l), Vt (l x n
+ * row-major, ldv): device pointers of `dtype`.  A column block of a larger
+ * matrix is handled by passing Vt + j0 with the full ldv. */
+BRSVD_API int brsvd_residual(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda,
+                             int dtype, int layout, const void* U, int64_t ldu,
+                             const void* sigma, const void* Vt, int64_t ldv, int64_t l,
+                             double* out);
+
 /* Out-of-core randomized SVD of a host-resident A (brsvd_run /
  * rsvd_naive_ooc, rsvd.py:188-284, global power iteration): A is streamed
  * over PCIe in panels of `panel` rows (row-major A) or columns (column-major

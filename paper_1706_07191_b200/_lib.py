@@ -26,7 +26,7 @@ EXPORTED = (
     "brsvd_gaussian", "brsvd_profile_begin", "brsvd_profile_end",
     "brsvd_spectral_norm", "brsvd_ialm", "brsvd_sketch_product", "brsvd_gram",
     "brsvd_chol_basis", "brsvd_apply", "brsvd_normalize", "brsvd_colmax",
-    "brsvd_scale_cols", "brsvd_rsvd_stream",
+    "brsvd_scale_cols", "brsvd_rsvd_stream", "brsvd_residual",
 )
 
 
@@ -98,6 +98,8 @@ def _declare(lib):
                                       vp, c_int, u64, vp, vp, vp, c_int, i64, c_int,
                                       ctypes.POINTER(BrsvdStats)]
     lib.brsvd_gram.argtypes = [vp, vp, i64, i64, i64, c_int, vp, i64, i64, vp]
+    lib.brsvd_residual.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, vp, i64, vp, vp, i64,
+                                   i64, ctypes.POINTER(dbl)]
     lib.brsvd_chol_basis.argtypes = [vp, vp, i64, dbl, dbl, dbl, dbl, vp,
                                      ctypes.POINTER(i32), ctypes.POINTER(i32)]
     lib.brsvd_apply.argtypes = [vp, vp, i64, i64, i64, c_int, vp, i64, vp, i64, c_int, dbl,

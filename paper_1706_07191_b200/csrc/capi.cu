@@ -9,6 +9,7 @@
 #include "pipeline.cuh"
 #include "rpca.cuh"
 #include "stream.cuh"
+#include "residual.cuh"
 
 using namespace brsvd;
 
@@ -314,6 +315,26 @@ int brsvd_rsvd_stream(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64
     vo.flush();
     BRSVD_CUDA(cudaStreamSynchronize(c.stream));
     fill_stats(stats, info, m, n, l, q);
+    return (int)kOk;
+  });
+}
+
+int brsvd_residual(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda, int dtype,
+                   int layout, const void* U, int64_t ldu, const void* sigma, const void* Vt,
+                   int64_t ldv, int64_t l, double* out) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && out != nullptr, kErrArg, "NULL argument");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    esize(dtype);
+    BRSVD_REQUIRE(m >= 0 && n >= 0 && l >= 0, kErrShape, "bad shape");
+    const bool row_major = layout == BRSVD_ROW_MAJOR;
+    if (dtype == BRSVD_F64)
+      residual_device<double>(c, (const double*)A, m, n, lda, row_major, (const double*)U, ldu,
+                              (const double*)sigma, (const double*)Vt, ldv, (int)l, out);
+    else
+      residual_device<float>(c, (const float*)A, m, n, lda, row_major, (const float*)U, ldu,
+                             (const float*)sigma, (const float*)Vt, ldv, (int)l, out);
     return (int)kOk;
   });
 }

@@ -323,48 +323,72 @@ def block_range_finder(store, cfg, memory_budget_bytes=None, plan=None):
     return factors.U, (plan if plan is not None else plan_used)
 
 
+def _residual_sums(a_dev, U_col, sig, Vt, j0=0):
+    """(||A - U diag(s) Vt[:, j0:j0+n]||^2, ||A||^2) of a device block through
+    the fused C-ABI kernel (brsvd_residual)."""
+    import torch
+    mat = DeviceMatrix(a_dev)
+    m, n = mat.shape
+    l = U_col.shape[1]
+    lib = _lib.load_library()
+    ctx = _lib.context(mat.device)
+    ctx.set_stream(torch_stream_ptr(mat.t))
+    esz = U_col.element_size()
+    out = (ctypes.c_double * 2)()
+    rc = lib.brsvd_residual(ctx.handle, mat.ptr, m, n, mat.ld, mat.code, mat.layout,
+                            ctypes.c_void_p(U_col.data_ptr()), U_col.stride(1),
+                            ctypes.c_void_p(sig.data_ptr()),
+                            ctypes.c_void_p(Vt.data_ptr() + j0 * esz), Vt.stride(0), l, out)
+    _lib.check(rc)
+    return out[0], out[1]
+
+
 def relative_frobenius_error(source, factors, block_width=None):
     """||A - U diag(sigma) Vt||_F / ||A||_F (rsvd.py:396-432), on the GPU.
 
-    Streams column blocks of a store (one extra pass) or takes an in-memory
-    matrix; sums of squares accumulate in fp64.
+    One fused pass over A (brsvd_residual: the rank-l reconstruction is formed
+    tile by tile in registers and subtracted as A is read; sums of squares in
+    fp64).  A store is streamed in column blocks (one extra pass, like the
+    reference); an in-memory matrix is used as is.
     """
     import torch
-    us = factors.U
-    vt = factors.Vt
-    sig = factors.sigma
     dev = f"cuda:{_lib.context().device}"
 
-    def T(x):
-        return x.to(dev) if is_torch(x) else torch.as_tensor(np.asarray(x), device=dev)
+    def T(x, dt):
+        t = x.to(dev) if is_torch(x) else torch.as_tensor(np.asarray(x), device=dev)
+        return t.to(dt)
 
-    U_d, s_d, Vt_d = T(us), T(sig), T(vt)
-    us_d = U_d * s_d
     if isinstance(source, MatrixStore):
         m, n = source.m, source.n
-        if us_d.shape[0] != m or Vt_d.shape[1] != n:
-            raise ValueError(f"factor shapes {us_d.shape[0]}x{Vt_d.shape[1]} do not "
-                             f"match source {m}x{n}")
-        if block_width is None:
-            block_width = max(1, min(n, (64 << 20) // (m * source.element_size)))
-        num = torch.zeros((), dtype=torch.float64, device=dev)
-        den = torch.zeros((), dtype=torch.float64, device=dev)
-        for j0 in range(0, n, block_width):
-            j1 = min(j0 + block_width, n)
-            blk = T(source.read_block(j0, j1))
-            diff = blk - us_d.to(blk.dtype) @ Vt_d[:, j0:j1].to(blk.dtype)
-            num += (diff.double() ** 2).sum()
-            den += (blk.double() ** 2).sum()
+        tdt = torch.float64 if source.dtype == np.float64 else torch.float32
     else:
         a = source if is_torch(source) else np.asarray(source)
-        a_d = T(a)
-        if us_d.shape[0] != a_d.shape[0] or Vt_d.shape[1] != a_d.shape[1]:
-            raise ValueError(f"factor shapes {us_d.shape[0]}x{Vt_d.shape[1]} do not "
-                             f"match source {a_d.shape[0]}x{a_d.shape[1]}")
-        diff = a_d - us_d.to(a_d.dtype) @ Vt_d.to(a_d.dtype)
-        num = (diff.double() ** 2).sum()
-        den = (a_d.double() ** 2).sum()
-    num, den = float(num), float(den)
+        m, n = a.shape
+        tdt = (a.dtype if is_torch(a) else
+               (torch.float64 if a.dtype == np.float64 else torch.float32))
+        if tdt not in (torch.float32, torch.float64):
+            tdt = torch.float64
+    U_d = T(factors.U, tdt)
+    Vt_d = T(factors.Vt, tdt).contiguous()
+    s_d = T(factors.sigma, tdt).contiguous()
+    if U_d.shape[0] != m or Vt_d.shape[1] != n:
+        raise ValueError(f"factor shapes {U_d.shape[0]}x{Vt_d.shape[1]} do not "
+                         f"match source {m}x{n}")
+    U_col = U_d.t().contiguous().t()    # column-major m x l
+    num = den = 0.0
+    if isinstance(source, MatrixStore):
+        if block_width is None:
+            block_width = max(1, min(n, (256 << 20) // max(1, m * source.element_size)))
+        for j0 in range(0, n, block_width):
+            j1 = min(j0 + block_width, n)
+            blk = torch.as_tensor(source.read_block(j0, j1), device=dev).to(tdt)
+            blk = blk.t().contiguous().t() if not blk.t().is_contiguous() else blk
+            a_, b_ = _residual_sums(blk, U_col, s_d, Vt_d, j0)
+            num += a_
+            den += b_
+    else:
+        a_d = T(a, tdt)
+        num, den = _residual_sums(a_d, U_col, s_d, Vt_d)
     if den == 0.0:
         return 0.0 if num == 0.0 else float("inf")
     return float(np.sqrt(num) / np.sqrt(den))
