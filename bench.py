@@ -302,12 +302,16 @@ def run_ours(args, world, rank, local):
     big_ms_per_launch = rep.big_ms / max(rep.big_launches, 1)
     flops_per_launch = rep.big_flops / max(rep.big_launches, 1)
     achieved_tflops = flops_per_launch / (big_ms_per_launch * 1e-3) / 1e12
-    peak = peaks["bf16_tflops_sustained"] / 6.0
+    h16 = os.environ.get("BRSVD_TC_H16", "1") != "0"
+    # fp16-split products: 3 kind::f16 MMAs per product term at the bf16/f16
+    # dense rate; 3xTF32 (BRSVD_TC_H16=0): 3 kind::tf32 MMAs at half that rate
+    peak = peaks["bf16_tflops_sustained"] / (3.0 if h16 else 6.0)
     roofline = {
         "bound": "tensor", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
         "frac": achieved_tflops / peak, "traffic": None,
         "kernel": "A-streaming products Y=A X / Z=A^T Y (2*m*n*l flops per launch)",
-        "peak_basis": f"{basis} bf16_tflops_sustained / 2 (TF32 rate) / 3 (3xTF32 split)",
+        "peak_basis": (f"{basis} bf16_tflops_sustained / 3 (3 fp16-split tcgen05 MMAs)" if h16
+                       else f"{basis} bf16_tflops_sustained / 2 (TF32 rate) / 3 (3xTF32)"),
         "launch_ms": big_ms_per_launch, "launches_per_step": rep.big_launches / args.steps,
         "share_of_step": rep.big_ms / (t_dev * 1e3 * args.steps),
         "hbm_gbs_achieved": (rep.big_bytes / max(rep.big_launches, 1))

@@ -68,15 +68,25 @@ __global__ void sum_slices_kernel(const T* __restrict__ parts, int64_t count, in
 // (Z += A_i^T Y_i, the fused power step of the north star: each panel is used
 // for both products while it is fresh), so the first transpose pass is done
 // by the time the transfer completes.
+// Row / column maxima of |A| for the fp16-split products (fp32 data only).
+template <typename T>
+bool want_amax(Ctx& c, const T* A, int64_t lda, int64_t m, int64_t n, int l) {
+  return sizeof(T) == 4 && tc::h16_enabled() && tc_gemm_supported<T>(c, A, lda, m, n, l);
+}
+
 template <typename T>
 bool feed_and_sample(Ctx& c, T* A, int64_t m, int64_t n, int64_t lda, bool row_major,
-                     const HostFeed& f, const T* X, int l, T* Y, T* Z) {
+                     const HostFeed& f, const T* X, int l, T* Y, T* Z, float* arow,
+                     float* acol) {
   const int64_t a_rows = row_major ? n : m, a_cols = row_major ? m : n;
   if (!row_major) {
     BRSVD_CUDA(cudaMemcpy2DAsync(A, lda * sizeof(T), f.host, f.ldh * sizeof(T),
                                  a_rows * sizeof(T), a_cols, cudaMemcpyHostToDevice,
                                  c.stream));
-    big_nn<T>(c, A, m, n, lda, row_major, X, n, l, Y, m);
+    if (arow)
+      absmax_rows_cols(c, reinterpret_cast<const float*>(A), m, n, lda, row_major, arow, acol,
+                       /*init=*/false);
+    big_nn<T>(c, A, m, n, lda, row_major, X, n, l, Y, m, arow);
     return false;
   }
   cudaStream_t cs;
@@ -103,10 +113,15 @@ bool feed_and_sample(Ctx& c, T* A, int64_t m, int64_t n, int64_t lda, bool row_m
     BRSVD_CUDA(cudaEventRecord(e, cs));
     evs.push_back(e);
     BRSVD_CUDA(cudaStreamWaitEvent(c.stream, e, 0));
-    big_nn<T>(c, A + r0 * lda, r1 - r0, n, lda, true, X, n, l, Y + r0, m);
+    // panel maxima: rows land in arow[r0:r1], columns accumulate over panels
+    if (arow)
+      absmax_rows_cols(c, reinterpret_cast<const float*>(A + r0 * lda), r1 - r0, n, lda, true,
+                       arow + r0, acol, /*init=*/false);
+    big_nn<T>(c, A + r0 * lda, r1 - r0, n, lda, true, X, n, l, Y + r0, m,
+              arow ? arow + r0 : nullptr);
     if (Z != nullptr)
       big_tn<T>(c, A + r0 * lda, r1 - r0, n, lda, true, Y + r0, m, l,
-                Zp.p + (int64_t)pi * n * l, n);
+                Zp.p + (int64_t)pi * n * l, n, acol);
   }
   if (Z != nullptr) {
     sum_slices_kernel<T><<<grid_for(n * l), 256, 0, c.stream>>>(Zp.p, n * l, npan, Z);
@@ -136,12 +151,25 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
     X = Xg.p;
   }
   DBuf<T> Y(c, (size_t)m * l), Z(c, (size_t)n * l), Zn(c, (size_t)n * l);
+  // per-row / per-column maxima of |A| (one pass, reused by every product)
+  DBuf<float> arow, acol;
+  if (want_amax<T>(c, A, lda, m, n, l)) {
+    arow.alloc(c, (size_t)m);
+    acol.alloc(c, (size_t)n);
+    if (feed == nullptr) {
+      absmax_rows_cols(c, reinterpret_cast<const float*>(A), m, n, lda, row_major, arow.p,
+                       acol.p);
+    } else {  // the feed accumulates panel by panel
+      BRSVD_CUDA(cudaMemsetAsync(arow.p, 0, sizeof(float) * m, c.stream));
+      BRSVD_CUDA(cudaMemsetAsync(acol.p, 0, sizeof(float) * n, c.stream));
+    }
+  }
   bool z_ready = false;
   if (feed != nullptr)
     z_ready = feed_and_sample<T>(c, const_cast<T*>(A), m, n, lda, row_major, *feed, X, l, Y.p,
-                                 q > 0 ? Z.p : nullptr);
+                                 q > 0 ? Z.p : nullptr, arow.p, acol.p);
   else
-    big_nn<T>(c, A, m, n, lda, row_major, X, n, l, Y.p, m);
+    big_nn<T>(c, A, m, n, lda, row_major, X, n, l, Y.p, m, arow.p);
   const MaxAbs p0 = maxabs<T>(c, Y.p, m, l, m);
   info.max_abs_y0 = p0.peak;
   bool nonfinite = p0.nonfinite;
@@ -151,9 +179,10 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
     return info;
   }
   for (int it = 0; it < q; ++it) {
-    if (!(it == 0 && z_ready)) big_tn<T>(c, A, m, n, lda, row_major, Y.p, m, l, Z.p, n);
+    if (!(it == 0 && z_ready))
+      big_tn<T>(c, A, m, n, lda, row_major, Y.p, m, l, Z.p, n, acol.p);
     normalize_sketch<T>(c, Z.p, n, l, n, Zn.p, n);
-    big_nn<T>(c, A, m, n, lda, row_major, Zn.p, n, l, Y.p, m);
+    big_nn<T>(c, A, m, n, lda, row_major, Zn.p, n, l, Y.p, m, arow.p);
   }
   info.words_read += (int64_t)(2 * q + 1) * m * n;
   info.block_reads += 2 * q + 1;
@@ -175,7 +204,7 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
   const T* Qop = Qw.p;
   ev.rec(2, c.stream);
   DBuf<T> Bt(c, (size_t)n * l);
-  big_tn<T>(c, A, m, n, lda, row_major, Qop, m, l, Bt.p, n);
+  big_tn<T>(c, A, m, n, lda, row_major, Qop, m, l, Bt.p, n, acol.p);
   info.words_read += m * n;
   info.block_reads += 1;
   ev.rec(3, c.stream);

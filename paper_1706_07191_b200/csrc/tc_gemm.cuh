@@ -23,6 +23,7 @@
 // stay L2-resident across the M tiles.
 #pragma once
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include <cstdlib>
 
@@ -35,7 +36,7 @@ constexpr int BM = 128;
 constexpr int BK = 16;              // fp32 K elements per stage (64-byte rows)
 constexpr int STAGES = 6;
 constexpr int NPAD_MAX = 320;   // l <= 320: two CTAs of <= 160 columns
-constexpr int kThreads = 384;
+constexpr int kThreads = 640;   // 4 role warps + 16 converter warps
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kASlot = 320;    // TMEM columns [320, 512): six A staging slots
 constexpr uint32_t A_STAGE_BYTES = BM * BK * 4;
@@ -47,6 +48,11 @@ struct Params {
   float* C;
   int64_t ldc;
   float* part;  // split-K workspace: split s writes its partial to part + s * M * n_out
+  // fp16 split (H16 kernels): row_max[M] = max |opA(row, :)| (power-of-two
+  // row scale 2^(14 - ceil(log2 max)) applied before the split, undone in the
+  // epilogue), col_inv[npad] = inverse power-of-two scales of the B columns
+  const float* row_max;
+  const float* col_inv;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -100,6 +106,50 @@ __device__ __forceinline__ uint64_t desc_kmajor_sw64(uint32_t saddr) {
   d |= (uint64_t)4 << 61;            // SWIZZLE_64B
   return d;
 }
+// K-major operand, 32-byte swizzle (16 fp16 per row): 8-row groups 256 B apart.
+__device__ __forceinline__ uint64_t desc_kmajor_sw32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;            // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(256 >> 4) << 32;   // SBO
+  d |= (uint64_t)1 << 46;            // descriptor version (sm100)
+  d |= (uint64_t)6 << 61;            // SWIZZLE_32B
+  return d;
+}
+__device__ __forceinline__ void mma_f16_ts(uint32_t d, uint32_t a, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&v)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+// Power-of-two scale mapping max |x| to <= 2^14 (fp16 split without overflow).
+__host__ __device__ __forceinline__ float h16_scale(float mx) {
+  if (!(mx > 0.f) || !(mx < 3.0e38f)) return 1.f;
+  int e;
+  frexpf(mx, &e);  // mx = f * 2^e, f in [0.5, 1)
+  return ldexpf(1.f, 14 - e);
+}
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  // a -> low half (lower k), b -> high half
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
+__device__ __forceinline__ float2 unpack_h2(uint32_t h) {
+  float lo, hi;
+  asm("{\n.reg .f16 l, h;\nmov.b32 {l, h}, %2;\ncvt.f32.f16 %0, l;\ncvt.f32.f16 %1, h;\n}"
+      : "=f"(lo), "=f"(hi)
+      : "r"(h));
+  return make_float2(lo, hi);
+}
+
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a, uint64_t bdesc,
                                             uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -178,16 +228,20 @@ __device__ __forceinline__ float lds32(uint32_t addr) {
 // lane quadrant (w % 4) -- the rows 32(w%4)..+31 of the tile -- and half
 // h = (w - 4) / 4 of the work: k values [8h, 8h+8) of each A stage and the
 // accumulator columns [h nc/2, (h+1) nc/2) of every flush.
-template <bool A_KMAJOR, int NCMAX>
+// H16: the split uses fp16 (hi, lo) pairs and kind::f16 MMAs (twice the
+// tf32 rate): with a power-of-two scale per row of opA and per column of B,
+// hi + lo carries 22 significant bits like the tf32 pair, and the three
+// products are exact in the fp32 accumulator.
+template <bool A_KMAJOR, int NCMAX, bool H16>
 __global__ void __launch_bounds__(kThreads, 1)
     tc3_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
                     const __grid_constant__ CUtensorMap mapBhi,
                     const __grid_constant__ CUtensorMap mapBlo, const Params p) {
-  constexpr int NH = NCMAX / 2;                          // running sums per thread
+  constexpr int NH = NCMAX / 4;                          // running sums per thread
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_dyn + 1023) & ~(uintptr_t)1023);
   const int nc = p.rows_c;                               // columns of this CTA
-  const uint32_t b_bytes = (uint32_t)nc * BK * 4;        // one of hi / lo
+  const uint32_t b_bytes = (uint32_t)nc * BK * (H16 ? 2 : 4);  // one of hi / lo
   const uint32_t stage_bytes = A_STAGE_BYTES + 2 * b_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * stage_bytes);
   uint64_t* freeb = full + STAGES;
@@ -216,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accready[b], 1);
-      mbar_init(&accfree[b], 8);
+      mbar_init(&accfree[b], 16);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
@@ -257,7 +311,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
+      // c_format f32; a/b format tf32 (2) or f16 (0); K-major A and B
+      const uint32_t fmt = H16 ? 0u : 2u;
+      const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) |
                              ((uint32_t)(nc >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % STAGES;
@@ -271,28 +327,44 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_after_sync();
         const uint32_t bh = smem_u32(smem + (size_t)s * stage_bytes + A_STAGE_BYTES);
         const uint32_t bl = bh + b_bytes;
-        const uint32_t a_hi = tmem + kASlot + s * 32, a_lo = a_hi + 16;
         const uint32_t d = tmem + (uint32_t)(buf * nc);
+        if constexpr (H16) {
+          // one K=16 step: A hi/lo in 8 TMEM columns each (fp16 pairs)
+          const uint32_t a_hi = tmem + kASlot + s * 16, a_lo = a_hi + 8;
+          const uint64_t dh = desc_kmajor_sw32(bh), dl = desc_kmajor_sw32(bl);
+          const uint32_t acc = chunk_start ? 0u : 1u;
+          mma_f16_ts(d, a_lo, dh, idesc, acc);
+          mma_f16_ts(d, a_hi, dl, idesc, 1u);
+          mma_f16_ts(d, a_hi, dh, idesc, 1u);
+        } else {
+          const uint32_t a_hi = tmem + kASlot + s * 32, a_lo = a_hi + 16;
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          const uint64_t dh = desc_kmajor_sw64(bh + kk * 32);
-          const uint64_t dl = desc_kmajor_sw64(bl + kk * 32);
-          const uint32_t acc = (chunk_start && kk == 0) ? 0u : 1u;
-          mma_tf32_ts(d, a_lo + kk * 8, dh, idesc, acc);
-          mma_tf32_ts(d, a_hi + kk * 8, dl, idesc, 1u);
-          mma_tf32_ts(d, a_hi + kk * 8, dh, idesc, 1u);
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t dh = desc_kmajor_sw64(bh + kk * 32);
+            const uint64_t dl = desc_kmajor_sw64(bl + kk * 32);
+            const uint32_t acc = (chunk_start && kk == 0) ? 0u : 1u;
+            mma_tf32_ts(d, a_lo + kk * 8, dh, idesc, acc);
+            mma_tf32_ts(d, a_hi + kk * 8, dl, idesc, 1u);
+            mma_tf32_ts(d, a_hi + kk * 8, dh, idesc, 1u);
+          }
         }
         mma_commit(&freeb[s]);
         if ((kb % kChunkKB) == kChunkKB - 1 || kb == nk - 1) mma_commit(&accready[buf]);
       }
     }
   } else if (warp >= 4) {  // ---------------- converters + accumulator flushes
-    const int wq = warp & 3;
-    const int half = (warp - 4) >> 2;
+    // 16 warps: lane quadrant wq (TMEM lanes / tile rows 32 wq ..), k half of
+    // each stage, stage parity par (even / odd k-blocks, so each warp's
+    // split -> tcgen05.st -> wait chain has two stages of MMA time), and a
+    // quarter of the accumulator columns for the flushes and the epilogue.
+    const int idx = warp - 4;
+    const int wq = idx & 3;
+    const int half = (idx >> 2) & 1;
+    const int par = idx >> 3;
     const int r = wq * 32 + lane;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-    const int hc = nc >> 1;                 // accumulator columns per half
-    const int c0 = half * hc;
+    const int hc = nc >> 2;                 // accumulator columns per warp
+    const int c0 = (2 * par + half) * hc;
     float run[NH];
 #pragma unroll
     for (int j = 0; j < NH; ++j) run[j] = 0.f;
@@ -315,7 +387,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&accfree[buf]);
     };
     const uint32_t smem_base = smem_u32(smem);
-    for (int kb = 0; kb < nk; ++kb) {
+    float rscale = 1.f;
+    if constexpr (H16) {
+      const int64_t grow = m0 + r;
+      rscale = (p.row_max != nullptr && grow < p.M) ? h16_scale(p.row_max[grow]) : 1.f;
+    }
+    int flushed = 0;
+    for (int kb = par; kb < nk; kb += 2) {
       const int s = kb % STAGES;
       const uint32_t ph = (kb / STAGES) & 1;
       mbar_wait(&full[s], ph);
@@ -339,24 +417,45 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[k] = lds32(box + (8 * half + k) * 128);
       }
-      uint32_t hi[8], lo[8];
+      if constexpr (H16) {
+        uint32_t hi[4], lo[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint32_t h = tf32_rna(v[i]);
-        hi[i] = h;
-        lo[i] = __float_as_uint(v[i] - __uint_as_float(h));
+        for (int i = 0; i < 4; ++i) {
+          const float x0 = v[2 * i] * rscale, x1 = v[2 * i + 1] * rscale;
+          hi[i] = pack_h2(x0, x1);
+          const float2 hf = unpack_h2(hi[i]);
+          lo[i] = pack_h2(x0 - hf.x, x1 - hf.y);
+        }
+        tmem_st4(tmem + lane_base + kASlot + s * 16 + 4 * half, hi);
+        tmem_st4(tmem + lane_base + kASlot + s * 16 + 8 + 4 * half, lo);
+      } else {
+        uint32_t hi[8], lo[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t h = tf32_rna(v[i]);
+          hi[i] = h;
+          lo[i] = __float_as_uint(v[i] - __uint_as_float(h));
+        }
+        tmem_st8(tmem + lane_base + kASlot + s * 32 + 8 * half, hi);
+        tmem_st8(tmem + lane_base + kASlot + s * 32 + 16 + 8 * half, lo);
       }
-      tmem_st8(tmem + lane_base + kASlot + s * 32 + 8 * half, hi);
-      tmem_st8(tmem + lane_base + kASlot + s * 32 + 16 + 8 * half, lo);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_before_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tfull[s]);
-      // the previous chunk's accumulator is complete once this chunk started
-      if (kb > 0 && (kb % kChunkKB) == 0) flush(kb / kChunkKB - 1);
+      // earlier chunks' accumulators are complete once this chunk started
+      while (flushed < kb / kChunkKB) flush(flushed++);
     }
-    if (nchunk > 0) flush(nchunk - 1);
+    while (flushed < nchunk) flush(flushed++);
     const int64_t row = m0 + r;
+    if constexpr (H16) {
+      const float rinv = 1.f / rscale;
+#pragma unroll
+      for (int j = 0; j < NH; ++j) {
+        const int col = n0 + c0 + j;
+        if (j < hc && col < p.n_out) run[j] *= rinv * p.col_inv[col];
+      }
+    }
     if (row < p.M) {
 #pragma unroll
       for (int j = 0; j < NH; ++j) {
@@ -399,6 +498,70 @@ __global__ void tc_split_kernel(const float* __restrict__ X, int64_t K, int n_sr
   }
 }
 
+// fp16 split of the sketch: per column j a power-of-two scale s_j from
+// max |X[:, j]| (colmax, 32-bit patterns of |x|), hi = f16(s_j x),
+// lo = f16(s_j x - hi); col_inv[j] = 1 / s_j (1 for padding columns).
+__global__ void tc_colmax_kernel(const float* __restrict__ X, int64_t K, int n_src,
+                                 int64_t ldx, unsigned* __restrict__ cmax) {
+  const int j = blockIdx.y;
+  unsigned m = 0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K;
+       k += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, __float_as_uint(fabsf(X[k + j * ldx])));
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(&cmax[j], m);
+}
+
+__global__ void tc_split16_kernel(const float* __restrict__ X, int64_t K, int n_src,
+                                  int64_t ldx, int npad, int64_t kld,
+                                  const unsigned* __restrict__ cmax,
+                                  uint16_t* __restrict__ hi, uint16_t* __restrict__ lo,
+                                  float* __restrict__ col_inv) {
+  const int64_t total = (int64_t)npad * kld;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = idx % kld, j = idx / kld;
+    const float sc = j < n_src ? h16_scale(__uint_as_float(cmax[j])) : 1.f;
+    const float x = (j < n_src && k < K) ? X[k + j * ldx] * sc : 0.f;
+    const __half h = __float2half_rn(x);
+    hi[idx] = __half_as_ushort(h);
+    lo[idx] = __half_as_ushort(__float2half_rn(x - __half2float(h)));
+    if (k == 0) col_inv[j] = 1.f / sc;
+  }
+}
+
+// max |S[i, :]| (rmax) and max |S[:, j]| (cmax) of a column-major S (sr x sc,
+// ld), accumulated with atomicMax on the 32-bit patterns of |x| (monotone for
+// non-negative floats; NaN propagates).  CTA tile: 256 rows (one per thread,
+// coalesced) x 128 columns.
+__global__ void __launch_bounds__(256)
+    absmax_rc_kernel(const float* __restrict__ S, int64_t sr, int64_t sc, int64_t ld,
+                     unsigned* __restrict__ rmax, unsigned* __restrict__ cmax) {
+  __shared__ unsigned wmax[8][128];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int64_t j0 = (int64_t)blockIdx.y * 128;
+  const bool ok = row < sr;
+  unsigned rm = 0;
+#pragma unroll 8
+  for (int jj = 0; jj < 128; ++jj) {
+    const int64_t j = j0 + jj;
+    const unsigned v = (ok && j < sc) ? __float_as_uint(fabsf(S[row + j * ld])) : 0u;
+    rm = max(rm, v);
+    const unsigned cm = __reduce_max_sync(0xffffffffu, v);
+    if (lane == 0) wmax[warp][jj] = cm;
+  }
+  if (ok) atomicMax(&rmax[row], rm);
+  __syncthreads();
+  if (threadIdx.x < 128) {
+    const int64_t j = j0 + threadIdx.x;
+    unsigned m = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) m = max(m, wmax[w][threadIdx.x]);
+    if (j < sc && m) atomicMax(&cmax[j], m);
+  }
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                   const cuuint32_t*, CUtensorMapInterleave,
@@ -422,13 +585,14 @@ inline EncodeTiledFn encode_fn() {
 // `row_bytes` stride; box (box_inner x box_outer).
 inline CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer,
                             uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
-                            CUtensorMapSwizzle swz) {
+                            CUtensorMapSwizzle swz,
+                            CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {inner, outer};
   const cuuint64_t strides[1] = {row_bytes};
   const cuuint32_t box[2] = {box_inner, box_outer};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base),
+  const CUresult r = encode_fn()(&m, dt, 2, const_cast<void*>(base),
                                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -450,12 +614,19 @@ inline Geometry geometry(int l) {
   return g;
 }
 
-inline size_t smem_bytes(int rows_c) {
-  return (size_t)STAGES * (A_STAGE_BYTES + 2u * (uint32_t)rows_c * BK * 4) + 128 + 1024;
+inline size_t smem_bytes(int rows_c, bool h16 = false) {
+  return (size_t)STAGES * (A_STAGE_BYTES + 2u * (uint32_t)rows_c * BK * (h16 ? 2 : 4)) + 128 +
+         1024;
 }
 
 inline bool env_enabled() {
   const char* e = std::getenv("BRSVD_TC");
+  return !(e && e[0] == '0');
+}
+
+// fp16-split products (2x the tf32 MMA rate) unless BRSVD_TC_H16=0.
+inline bool h16_enabled() {
+  const char* e = std::getenv("BRSVD_TC_H16");
   return !(e && e[0] == '0');
 }
 
@@ -473,34 +644,57 @@ bool tc_gemm_supported(Ctx& c, const T* A, int64_t lda, int64_t m, int64_t n, in
   return m >= 1 && n >= 1;
 }
 
+// Row and column maxima |A| of the big operand (one pass), as floats:
+// amax_rows[m], amax_cols[n] (either may be NULL).  Used for the power-of-two
+// scales of the fp16-split products; computed once per decomposition.
+inline void absmax_rows_cols(Ctx& c, const float* A, int64_t m, int64_t n, int64_t lda,
+                             bool row_major, float* amax_rows, float* amax_cols,
+                             bool init = true) {
+  const int64_t sr = row_major ? n : m, sc = row_major ? m : n;
+  DBuf<unsigned> rbuf, cbuf;
+  unsigned* S_r = reinterpret_cast<unsigned*>(row_major ? amax_cols : amax_rows);
+  unsigned* S_c = reinterpret_cast<unsigned*>(row_major ? amax_rows : amax_cols);
+  if (!S_r) {
+    rbuf.alloc(c, (size_t)sr);
+    S_r = rbuf.p;
+    BRSVD_CUDA(cudaMemsetAsync(S_r, 0, sizeof(unsigned) * sr, c.stream));
+  } else if (init) {
+    BRSVD_CUDA(cudaMemsetAsync(S_r, 0, sizeof(unsigned) * sr, c.stream));
+  }
+  if (!S_c) {
+    cbuf.alloc(c, (size_t)sc);
+    S_c = cbuf.p;
+    BRSVD_CUDA(cudaMemsetAsync(S_c, 0, sizeof(unsigned) * sc, c.stream));
+  } else if (init) {
+    BRSVD_CUDA(cudaMemsetAsync(S_c, 0, sizeof(unsigned) * sc, c.stream));
+  }
+  if (sr < 1 || sc < 1) return;
+  const dim3 grid((unsigned)ceil_div(sr, 256), (unsigned)ceil_div(sc, 128));
+  tc::absmax_rc_kernel<<<grid, 256, 0, c.stream>>>(A, sr, sc, lda, S_r, S_c);
+  BRSVD_CHECK_LAUNCH();
+}
+
 template <typename T>
 void tc_gemm_launch(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool row_major,
                     bool trans, const T* X, int64_t ldx, int l, T* C, int64_t ldc,
-                    int splits = 0, float* part = nullptr);
+                    int splits = 0, float* part = nullptr, const float* opa_max = nullptr);
 
 template <>
 inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, int64_t lda,
                                   bool row_major, bool trans, const float* X, int64_t ldx,
-                                  int l, float* C, int64_t ldc, int splits, float* part) {
+                                  int l, float* C, int64_t ldc, int splits, float* part,
+                                  const float* opa_max) {
   using namespace tc;
   const int64_t M = trans ? n : m, K = trans ? m : n;
   const bool kmajor = row_major != trans;
   const Geometry g = geometry(l);
-  const int64_t kld = ceil_div(K, 4) * 4;
-  DBuf<float> hi(c, (size_t)g.npad * kld), lo(c, (size_t)g.npad * kld);
-  tc_split_kernel<<<grid_for((int64_t)g.npad * kld), 256, 0, c.stream>>>(
-      X, K, l, ldx, g.npad, kld, hi.p, lo.p);
-  BRSVD_CHECK_LAUNCH();
+  const bool h16 = h16_enabled();
   // A as stored: row-major (m x n) has n contiguous; column-major has m contiguous.
   const uint64_t inner = row_major ? (uint64_t)n : (uint64_t)m;
   const uint64_t outer = row_major ? (uint64_t)m : (uint64_t)n;
   const CUtensorMap mapA =
       kmajor ? make_map(A, inner, outer, (uint64_t)lda * 4, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B)
              : make_map(A, inner, outer, (uint64_t)lda * 4, 32, BK, CU_TENSOR_MAP_SWIZZLE_NONE);
-  const CUtensorMap mapBhi = make_map(hi.p, (uint64_t)kld, (uint64_t)g.npad, (uint64_t)kld * 4,
-                                      BK, (uint32_t)g.rows_c, CU_TENSOR_MAP_SWIZZLE_64B);
-  const CUtensorMap mapBlo = make_map(lo.p, (uint64_t)kld, (uint64_t)g.npad, (uint64_t)kld * 4,
-                                      BK, (uint32_t)g.rows_c, CU_TENSOR_MAP_SWIZZLE_64B);
   Params p;
   p.M = M;
   p.K = K;
@@ -510,12 +704,59 @@ inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, 
   p.n_out = l;
   p.C = C;
   p.ldc = ldc;
+  p.part = part;
+  p.row_max = nullptr;
+  p.col_inv = nullptr;
+  DBuf<float> hi, lo, opmax, cinv;
+  DBuf<unsigned> bmax;
+  CUtensorMap mapBhi, mapBlo;
+  if (h16) {
+    const int64_t kld = ceil_div(K, 8) * 8;
+    if (opa_max == nullptr) {
+      opmax.alloc(c, (size_t)M);
+      if (trans)
+        absmax_rows_cols(c, A, m, n, lda, row_major, nullptr, opmax.p);
+      else
+        absmax_rows_cols(c, A, m, n, lda, row_major, opmax.p, nullptr);
+      opa_max = opmax.p;
+    }
+    bmax.alloc(c, (size_t)g.npad);
+    cinv.alloc(c, (size_t)g.npad);
+    hi.alloc(c, (size_t)g.npad * kld / 2 + 8);
+    lo.alloc(c, (size_t)g.npad * kld / 2 + 8);
+    BRSVD_CUDA(cudaMemsetAsync(bmax.p, 0, sizeof(unsigned) * g.npad, c.stream));
+    tc_colmax_kernel<<<dim3((unsigned)std::min<int64_t>(ceil_div(K, 256), 64), (unsigned)l), 256,
+                       0, c.stream>>>(X, K, l, ldx, bmax.p);
+    BRSVD_CHECK_LAUNCH();
+    tc_split16_kernel<<<grid_for((int64_t)g.npad * kld), 256, 0, c.stream>>>(
+        X, K, l, ldx, g.npad, kld, bmax.p, reinterpret_cast<uint16_t*>(hi.p),
+        reinterpret_cast<uint16_t*>(lo.p), cinv.p);
+    BRSVD_CHECK_LAUNCH();
+    mapBhi = make_map(hi.p, (uint64_t)kld, (uint64_t)g.npad, (uint64_t)kld * 2, BK,
+                      (uint32_t)g.rows_c, CU_TENSOR_MAP_SWIZZLE_32B,
+                      CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    mapBlo = make_map(lo.p, (uint64_t)kld, (uint64_t)g.npad, (uint64_t)kld * 2, BK,
+                      (uint32_t)g.rows_c, CU_TENSOR_MAP_SWIZZLE_32B,
+                      CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    p.row_max = opa_max;
+    p.col_inv = cinv.p;
+  } else {
+    const int64_t kld = ceil_div(K, 4) * 4;
+    hi.alloc(c, (size_t)g.npad * kld);
+    lo.alloc(c, (size_t)g.npad * kld);
+    tc_split_kernel<<<grid_for((int64_t)g.npad * kld), 256, 0, c.stream>>>(
+        X, K, l, ldx, g.npad, kld, hi.p, lo.p);
+    BRSVD_CHECK_LAUNCH();
+    mapBhi = make_map(hi.p, (uint64_t)kld, (uint64_t)g.npad, (uint64_t)kld * 4, BK,
+                      (uint32_t)g.rows_c, CU_TENSOR_MAP_SWIZZLE_64B);
+    mapBlo = make_map(lo.p, (uint64_t)kld, (uint64_t)g.npad, (uint64_t)kld * 4, BK,
+                      (uint32_t)g.rows_c, CU_TENSOR_MAP_SWIZZLE_64B);
+  }
   // Two K-halves per tile when the tile count leaves the last wave of CTAs
   // (one per SM) badly filled: the two fp32 partial sums are combined with
   // atomicAdd into a zeroed C, which is order-independent for two terms.
   const int64_t tiles = ceil_div(M, BM) * g.nchunks;
   const double waves = (double)tiles / c.num_sms;
-  p.part = part;
   p.ksplit = (K >= 8192 && waves > 1.0 && waves < 8.0 &&
               waves - std::floor(waves) > 0.0 && waves - std::floor(waves) < 0.75)
                  ? 2
@@ -524,26 +765,31 @@ inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, 
   else if (p.ksplit > 1)
     BRSVD_CUDA(cudaMemset2DAsync(C, (size_t)ldc * sizeof(float), 0, (size_t)M * sizeof(float),
                                  (size_t)l, c.stream));
-  const size_t smem = smem_bytes(g.rows_c);
+  const size_t smem = smem_bytes(g.rows_c, h16);
   const dim3 grid((unsigned)(tiles * p.ksplit));
-#define BRSVD_TC_LAUNCH(KM, NCM)                                                      \
-  do {                                                                                \
-    BRSVD_CUDA(cudaFuncSetAttribute(tc3_gemm_kernel<KM, NCM>,                         \
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,      \
-                                    (int)smem));                                      \
-    tc3_gemm_kernel<KM, NCM><<<grid, kThreads, smem, c.stream>>>(mapA, mapBhi, mapBlo, \
-                                                                 p);                  \
+#define BRSVD_TC_LAUNCH(KM, NCM, H)                                                      \
+  do {                                                                                   \
+    BRSVD_CUDA(cudaFuncSetAttribute(tc3_gemm_kernel<KM, NCM, H>,                         \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                                    (int)smem));                                         \
+    tc3_gemm_kernel<KM, NCM, H><<<grid, kThreads, smem, c.stream>>>(mapA, mapBhi, mapBlo, \
+                                                                    p);                  \
   } while (0)
-#define BRSVD_TC_NC(KM)                                          \
+#define BRSVD_TC_NC(KM, H)                                       \
   do {                                                           \
-    if (g.rows_c <= 32) BRSVD_TC_LAUNCH(KM, 32);                 \
-    else if (g.rows_c <= 64) BRSVD_TC_LAUNCH(KM, 64);            \
-    else if (g.rows_c <= 96) BRSVD_TC_LAUNCH(KM, 96);            \
-    else if (g.rows_c <= 128) BRSVD_TC_LAUNCH(KM, 128);          \
-    else BRSVD_TC_LAUNCH(KM, 160);                               \
+    if (g.rows_c <= 32) BRSVD_TC_LAUNCH(KM, 32, H);              \
+    else if (g.rows_c <= 64) BRSVD_TC_LAUNCH(KM, 64, H);         \
+    else if (g.rows_c <= 96) BRSVD_TC_LAUNCH(KM, 96, H);         \
+    else if (g.rows_c <= 128) BRSVD_TC_LAUNCH(KM, 128, H);       \
+    else BRSVD_TC_LAUNCH(KM, 160, H);                            \
   } while (0)
-  if (kmajor) BRSVD_TC_NC(true);
-  else BRSVD_TC_NC(false);
+  if (h16) {
+    if (kmajor) BRSVD_TC_NC(true, true);
+    else BRSVD_TC_NC(false, true);
+  } else {
+    if (kmajor) BRSVD_TC_NC(true, false);
+    else BRSVD_TC_NC(false, false);
+  }
 #undef BRSVD_TC_NC
 #undef BRSVD_TC_LAUNCH
   BRSVD_CHECK_LAUNCH();
@@ -551,7 +797,8 @@ inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, 
 
 template <>
 inline void tc_gemm_launch<double>(Ctx&, const double*, int64_t, int64_t, int64_t, bool, bool,
-                                   const double*, int64_t, int, double*, int64_t, int, float*) {
+                                   const double*, int64_t, int, double*, int64_t, int, float*,
+                                   const float*) {
   throw Error(kErrArg, "tcgen05 path is fp32-only");
 }
 
