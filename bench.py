@@ -306,9 +306,17 @@ def run_ours(args, world, rank, local):
     # fp16-split products: 3 kind::f16 MMAs per product term at the bf16/f16
     # dense rate; 3xTF32 (BRSVD_TC_H16=0): 3 kind::tf32 MMAs at half that rate
     peak = peaks["bf16_tflops_sustained"] / (3.0 if h16 else 6.0)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):   # dram bytes of one launch, from the committed ncu capture
+        with open(tpath) as f:
+            tj = json.load(f)
+        traffic = tj["dram_bytes_read"] + tj["dram_bytes_write"]
     roofline = {
         "bound": "tensor", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
-        "frac": achieved_tflops / peak, "traffic": None,
+        "frac": achieved_tflops / peak, "traffic": traffic,
+        "traffic_unit": "bytes per launch (ncu dram read+write, profiles/traffic.json)",
+        "algorithmic_bytes": M * N_COLS * 4,
         "kernel": "A-streaming products Y=A X / Z=A^T Y (2*m*n*l flops per launch)",
         "peak_basis": (f"{basis} bf16_tflops_sustained / 3 (3 fp16-split tcgen05 MMAs)" if h16
                        else f"{basis} bf16_tflops_sustained / 2 (TF32 rate) / 3 (3xTF32)"),
