@@ -116,6 +116,19 @@ BRSVD_API int brsvd_rsvd(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, in
                const void* omega, int omega_where, uint64_t seed, void* U,
                void* sigma, void* Vt, int out_where, brsvd_stats* stats);
 
+/* Paper-literal block randomized SVD (block_range_finder + brsvd_run,
+ * rsvd.py:150-215; Alg. 2): the sample is the sum over the column
+ * blocks [col_bounds[b], col_bounds[b+1]) of (A_J A_J^T)^q A_J Omega_J, each
+ * block's power iteration unnormalised and complete before the next block.
+ * nblocks + 1 bounds, col_bounds[0] = 0, col_bounds[nblocks] = n.  With
+ * nblocks <= 1 or q = 0 this is brsvd_rsvd.  Other arguments as brsvd_rsvd. */
+BRSVD_API int brsvd_rsvd_blocked(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n,
+                                 int64_t lda, int dtype, int layout, int a_where, int k,
+                                 int p, int q, const void* omega, int omega_where,
+                                 uint64_t seed, const int64_t* col_bounds, int nblocks,
+                                 void* U, void* sigma, void* Vt, int out_where,
+                                 brsvd_stats* stats);
+
 /* One pass over A -- the A-streaming product of the power iteration and of
  * the core projection (a @ omega, a.T @ y: rsvd.py:94-102, :140):
  *   trans = 0:  C (m x l) = A X,    X (n x l)
@@ -150,6 +163,17 @@ BRSVD_API int brsvd_rsvd_stream(brsvd_ctx* ctx, const void* A, int64_t m, int64_
                                 const void* omega, int omega_where, uint64_t seed, void* U,
                                 void* sigma, void* Vt, int out_where, int64_t panel, int nbuf,
                                 brsvd_stats* stats);
+
+/* brsvd_rsvd_stream with block_power = 1: the paper's two-pass BRSVD
+ * (brsvd_run with s > 1 and q >= 1, rsvd.py:150-215): each streamed column
+ * panel runs its whole power iteration while resident and the panel samples
+ * are summed, then one pass forms B; column-major A only. */
+BRSVD_API int brsvd_rsvd_stream_blocked(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n,
+                                        int64_t lda, int dtype, int layout, int k, int p,
+                                        int q, const void* omega, int omega_where,
+                                        uint64_t seed, void* U, void* sigma, void* Vt,
+                                        int out_where, int64_t panel, int nbuf,
+                                        int block_power, brsvd_stats* stats);
 
 /* Orthonormal basis of range(Y) (tsqr_factor, kernels.py:139-164).
  *   Y m x l column-major (ldy); Q m x l column-major; R (optional) l x l

@@ -161,6 +161,30 @@ def randomized_svd_blocked(a, k, p=10, q=0, seed=0, partitions=1):
     return dict(U=u, sigma=s, Vt=vt, rank_y=rank_y, rank_b=rank_b)
 
 
+def randomized_svd_paper(a, k, p, q, blocks, seed=0, omega=None):
+    """brsvd_run with s > 1 (rsvd.py:150-215): the per-block power iteration
+    of block_range_finder -- Y = sum_J (A_J A_J^T)^q A_J Omega_J with
+    Omega_J = gaussian_matrix(|J|, l, seed, 0, row_offset=j0) (rsvd.py:169-175),
+    no normalisation -- then Q = tsqr(Y), B[:, J] = Q^T A_J (rsvd.py:202-208)
+    and _finish (rsvd.py:117-123)."""
+    m, n = a.shape
+    l = k + p
+    y = None
+    blocks = [(int(j0), int(j1)) for j0, j1 in blocks]   # Python ints: row << 192
+    for j0, j1 in blocks:
+        om = (omega[j0:j1] if omega is not None
+              else normal_sketch(j1 - j0, l, seed, 0, j0, a.dtype))
+        contrib = power_sample(a[:, j0:j1], om, q)
+        y = contrib if y is None else y + contrib
+    qy, _, rank_y = orthonormal_range(y)
+    b = np.empty((l, n), dtype=a.dtype, order="F")
+    for j0, j1 in blocks:
+        b[:, j0:j1] = qy.T @ a[:, j0:j1]
+    w, s, vt, rank_b = core_svd(b)
+    u, vt = canonical_signs(qy @ w, vt)
+    return dict(U=u, sigma=s, Vt=vt, rank_y=rank_y, rank_b=rank_b)
+
+
 def frob_rel_error(a, u, sigma, vt):
     """||A - U diag(s) Vt||_F / ||A||_F (rsvd.py:396-432, in-memory branch)."""
     d = a - (u * sigma) @ vt

@@ -26,7 +26,8 @@ EXPORTED = (
     "brsvd_gaussian", "brsvd_profile_begin", "brsvd_profile_end",
     "brsvd_spectral_norm", "brsvd_ialm", "brsvd_sketch_product", "brsvd_gram",
     "brsvd_chol_basis", "brsvd_apply", "brsvd_normalize", "brsvd_colmax",
-    "brsvd_scale_cols", "brsvd_rsvd_stream", "brsvd_residual",
+    "brsvd_scale_cols", "brsvd_rsvd_stream", "brsvd_residual", "brsvd_rsvd_blocked",
+    "brsvd_rsvd_stream_blocked",
 )
 
 
@@ -80,6 +81,9 @@ def _declare(lib):
     lib.brsvd_rsvd.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, c_int, c_int,
                                c_int, vp, c_int, u64, vp, vp, vp, c_int,
                                ctypes.POINTER(BrsvdStats)]
+    lib.brsvd_rsvd_blocked.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, c_int,
+                                       c_int, c_int, vp, c_int, u64, vp, c_int, vp, vp, vp,
+                                       c_int, ctypes.POINTER(BrsvdStats)]
     lib.brsvd_tsqr.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, vp, vp,
                                ctypes.POINTER(i32)]
     lib.brsvd_small_svd.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, vp, vp, vp,
@@ -97,6 +101,9 @@ def _declare(lib):
     lib.brsvd_rsvd_stream.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, c_int, c_int,
                                       vp, c_int, u64, vp, vp, vp, c_int, i64, c_int,
                                       ctypes.POINTER(BrsvdStats)]
+    lib.brsvd_rsvd_stream_blocked.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int,
+                                              c_int, c_int, vp, c_int, u64, vp, vp, vp, c_int,
+                                              i64, c_int, c_int, ctypes.POINTER(BrsvdStats)]
     lib.brsvd_gram.argtypes = [vp, vp, i64, i64, i64, c_int, vp, i64, i64, vp]
     lib.brsvd_residual.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, vp, i64, vp, vp, i64,
                                    i64, ctypes.POINTER(dbl)]

@@ -225,7 +225,24 @@ int brsvd_rsvd(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda,
                int dtype, int layout, int a_where, int k, int p, int q,
                const void* omega, int omega_where, uint64_t seed, void* U,
                void* sigma, void* Vt, int out_where, brsvd_stats* stats) {
+  return brsvd_rsvd_blocked(ctx, A, m, n, lda, dtype, layout, a_where, k, p, q, omega,
+                            omega_where, seed, nullptr, 0, U, sigma, Vt, out_where, stats);
+}
+
+int brsvd_rsvd_blocked(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda,
+                       int dtype, int layout, int a_where, int k, int p, int q,
+                       const void* omega, int omega_where, uint64_t seed,
+                       const int64_t* col_bounds, int nblocks, void* U, void* sigma,
+                       void* Vt, int out_where, brsvd_stats* stats) {
   return guarded([&] {
+    if (nblocks > 0) {
+      BRSVD_REQUIRE(col_bounds != nullptr, kErrArg, "col_bounds is NULL");
+      BRSVD_REQUIRE(col_bounds[0] == 0 && col_bounds[nblocks] == n, kErrShape,
+                    "column blocks must tile [0, n)");
+      for (int b = 0; b < nblocks; ++b)
+        BRSVD_REQUIRE(col_bounds[b + 1] > col_bounds[b], kErrShape,
+                      "column blocks must be non-empty and increasing");
+    }
     BRSVD_REQUIRE(ctx != nullptr, kErrArg, "ctx is NULL");
     Ctx& c = ctx->c;
     BRSVD_CUDA(cudaSetDevice(c.device));
@@ -265,11 +282,12 @@ int brsvd_rsvd(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda,
       info = rsvd_device<double>(c, (const double*)aptr, m, n, ald, row_major, k, p, q,
                                  (const double*)ov.dptr, seed, (double*)uo.dptr,
                                  (double*)so.dptr, (double*)vo.dptr,
-                                 on_host ? &feed : nullptr);
+                                 on_host ? &feed : nullptr, col_bounds, nblocks);
     } else {
       info = rsvd_device<float>(c, (const float*)aptr, m, n, ald, row_major, k, p, q,
                                 (const float*)ov.dptr, seed, (float*)uo.dptr,
-                                (float*)so.dptr, (float*)vo.dptr, on_host ? &feed : nullptr);
+                                (float*)so.dptr, (float*)vo.dptr, on_host ? &feed : nullptr,
+                                col_bounds, nblocks);
     }
     uo.flush();
     so.flush();
@@ -284,7 +302,19 @@ int brsvd_rsvd_stream(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64
                       int dtype, int layout, int k, int p, int q, const void* omega,
                       int omega_where, uint64_t seed, void* U, void* sigma, void* Vt,
                       int out_where, int64_t panel, int nbuf, brsvd_stats* stats) {
+  return brsvd_rsvd_stream_blocked(ctx, A, m, n, lda, dtype, layout, k, p, q, omega,
+                                   omega_where, seed, U, sigma, Vt, out_where, panel, nbuf, 0,
+                                   stats);
+}
+
+int brsvd_rsvd_stream_blocked(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n,
+                              int64_t lda, int dtype, int layout, int k, int p, int q,
+                              const void* omega, int omega_where, uint64_t seed, void* U,
+                              void* sigma, void* Vt, int out_where, int64_t panel, int nbuf,
+                              int block_power, brsvd_stats* stats) {
   return guarded([&] {
+    BRSVD_REQUIRE(!block_power || layout == BRSVD_COL_MAJOR, kErrArg,
+                  "per-block power iteration streams column blocks (column-major A)");
     BRSVD_REQUIRE(ctx != nullptr && A != nullptr, kErrArg, "NULL argument");
     Ctx& c = ctx->c;
     BRSVD_CUDA(cudaSetDevice(c.device));
@@ -305,11 +335,13 @@ int brsvd_rsvd_stream(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64
     if (dtype == BRSVD_F64)
       info = rsvd_stream<double>(c, (const double*)A, m, n, lda, row_major, k, p, q,
                                  (const double*)ov.dptr, seed, (double*)uo.dptr,
-                                 (double*)so.dptr, (double*)vo.dptr, panel, nbuf);
+                                 (double*)so.dptr, (double*)vo.dptr, panel, nbuf,
+                                 block_power != 0);
     else
       info = rsvd_stream<float>(c, (const float*)A, m, n, lda, row_major, k, p, q,
                                 (const float*)ov.dptr, seed, (float*)uo.dptr,
-                                (float*)so.dptr, (float*)vo.dptr, panel, nbuf);
+                                (float*)so.dptr, (float*)vo.dptr, panel, nbuf,
+                                block_power != 0);
     uo.flush();
     so.flush();
     vo.flush();

@@ -134,9 +134,55 @@ bool feed_and_sample(Ctx& c, T* A, int64_t m, int64_t n, int64_t lda, bool row_m
 }
 
 template <typename T>
+__global__ void axpy_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx,
+                            T* __restrict__ y, int64_t ldy) {
+  const int64_t total = rows * cols;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = id % rows, j = id / rows;
+    y[i + j * ldy] += x[i + j * ldx];
+  }
+}
+
+template <typename T>
+void axpy(Ctx& c, const T* x, int64_t rows, int64_t cols, int64_t ldx, T* y, int64_t ldy) {
+  axpy_kernel<T><<<grid_for(rows * cols), 256, 0, c.stream>>>(x, rows, cols, ldx, y, ldy);
+  BRSVD_CHECK_LAUNCH();
+}
+
+// Paper-literal block sketch (block_range_finder, rsvd.py:150-185; PAPER.md
+// Alg. 2): Y = sum_J (A_J A_J^T)^q A_J Omega_J over the column blocks J of the
+// plan, each block's power iteration run to completion on the block (no
+// normalisation, like the reference), the block samples summed.  For q = 0
+// or one block this equals the global sample.
+template <typename T>
+void paper_sketch(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool row_major,
+                  const T* X, int l, int q, const int64_t* bounds, int nblk, T* Y,
+                  const float* arow, const float* acol) {
+  int64_t wmax = 0;
+  for (int b = 0; b < nblk; ++b) wmax = std::max(wmax, bounds[b + 1] - bounds[b]);
+  DBuf<T> YJ(c, (size_t)m * l), ZJ(c, (size_t)std::max<int64_t>(wmax, 1) * l);
+  BRSVD_CUDA(cudaMemsetAsync(Y, 0, sizeof(T) * m * l, c.stream));
+  for (int b = 0; b < nblk; ++b) {
+    const int64_t j0 = bounds[b], w = bounds[b + 1] - bounds[b];
+    if (w <= 0) continue;
+    const T* AJ = row_major ? A + j0 : A + j0 * lda;
+    big_nn<T>(c, AJ, m, w, lda, row_major, X + j0, n, l, YJ.p, m, arow);
+    for (int it = 0; it < q; ++it) {
+      big_tn<T>(c, AJ, m, w, lda, row_major, YJ.p, m, l, ZJ.p, w, acol ? acol + j0 : nullptr);
+      big_nn<T>(c, AJ, m, w, lda, row_major, ZJ.p, w, l, YJ.p, m, arow);
+    }
+    axpy_kernel<T><<<grid_for(m * l), 256, 0, c.stream>>>(YJ.p, m, l, m, Y, m);
+    BRSVD_CHECK_LAUNCH();
+  }
+}
+
+template <typename T>
 RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
                      bool row_major, int k, int p, int q, const T* omega,
-                     uint64_t seed, T* U, T* sigma, T* V, const HostFeed* feed = nullptr) {
+                     uint64_t seed, T* U, T* sigma, T* V, const HostFeed* feed = nullptr,
+                     const int64_t* blocks = nullptr, int nblk = 0) {
+  const bool paper = blocks != nullptr && nblk > 1 && q > 0;
   const int l = k + p;
   RsvdInfo info;
   StageEvents ev;
@@ -165,11 +211,23 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
     }
   }
   bool z_ready = false;
-  if (feed != nullptr)
+  if (paper) {
+    if (feed != nullptr) {  // land A first; the block sketch revisits every block q times
+      const int64_t a_rows = row_major ? n : m, a_cols = row_major ? m : n;
+      BRSVD_CUDA(cudaMemcpy2DAsync(const_cast<T*>(A), lda * sizeof(T), feed->host,
+                                   feed->ldh * sizeof(T), a_rows * sizeof(T), a_cols,
+                                   cudaMemcpyHostToDevice, c.stream));
+      if (arow.p)
+        absmax_rows_cols(c, reinterpret_cast<const float*>(A), m, n, lda, row_major, arow.p,
+                         acol.p, false);
+    }
+    paper_sketch<T>(c, A, m, n, lda, row_major, X, l, q, blocks, nblk, Y.p, arow.p, acol.p);
+  } else if (feed != nullptr) {
     z_ready = feed_and_sample<T>(c, const_cast<T*>(A), m, n, lda, row_major, *feed, X, l, Y.p,
                                  q > 0 ? Z.p : nullptr, arow.p, acol.p);
-  else
+  } else {
     big_nn<T>(c, A, m, n, lda, row_major, X, n, l, Y.p, m, arow.p);
+  }
   const MaxAbs p0 = maxabs<T>(c, Y.p, m, l, m);
   info.max_abs_y0 = p0.peak;
   bool nonfinite = p0.nonfinite;
@@ -178,7 +236,7 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
     info.log10_peak = INFINITY;
     return info;
   }
-  for (int it = 0; it < q; ++it) {
+  for (int it = 0; it < (paper ? 0 : q); ++it) {
     if (!(it == 0 && z_ready))
       big_tn<T>(c, A, m, n, lda, row_major, Y.p, m, l, Z.p, n, acol.p);
     normalize_sketch<T>(c, Z.p, n, l, n, Zn.p, n);
@@ -227,8 +285,10 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
   // Overflow guard of the unnormalised reference iteration: its sample is
   // (A A^T)^q A Omega, whose peak grows like max|A Omega| * sigma_1^(2q).
   const double lim = std::log10(0.01 * finfo_max<T>());
+  // (the paper-mode sample is already the powered, unnormalised one)
+  const int qg = paper ? 0 : q;
   if (info.max_abs_y0 > 0.0 && s0 > 0.0)
-    info.log10_peak = std::log10(info.max_abs_y0) + 2.0 * q * std::log10(s0);
+    info.log10_peak = std::log10(info.max_abs_y0) + 2.0 * qg * std::log10(s0);
   else
     info.log10_peak = info.max_abs_y0 > 0.0 ? std::log10(info.max_abs_y0) : -400.0;
   info.overflow = nonfinite || !std::isfinite(s0) || info.log10_peak > lim;

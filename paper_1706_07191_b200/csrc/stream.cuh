@@ -17,23 +17,6 @@
 
 namespace brsvd {
 
-template <typename T>
-__global__ void axpy_kernel(const T* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx,
-                            T* __restrict__ y, int64_t ldy) {
-  const int64_t total = rows * cols;
-  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
-       id += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = id % rows, j = id / rows;
-    y[i + j * ldy] += x[i + j * ldx];
-  }
-}
-
-template <typename T>
-void axpy(Ctx& c, const T* x, int64_t rows, int64_t cols, int64_t ldx, T* y, int64_t ldy) {
-  axpy_kernel<T><<<grid_for(rows * cols), 256, 0, c.stream>>>(x, rows, cols, ldx, y, ldy);
-  BRSVD_CHECK_LAUNCH();
-}
-
 // Ring of device panel buffers fed from host memory on a side stream.
 template <typename T>
 struct PanelStreamer {
@@ -96,10 +79,14 @@ struct PanelStreamer {
   }
 };
 
+// block_power (column panels only): the paper's two-pass scheme -- each panel
+// J runs its whole power iteration (A_J A_J^T)^q A_J Omega_J while resident,
+// the block samples are summed (block_range_finder, rsvd.py:150-185), then the
+// B pass: 2 passes for any q.
 template <typename T>
 RsvdInfo rsvd_stream(Ctx& c, const T* Ah, int64_t m, int64_t n, int64_t lda, bool row_major,
                      int k, int p, int q, const T* omega, uint64_t seed, T* U, T* sigma, T* V,
-                     int64_t panel, int nbuf) {
+                     int64_t panel, int nbuf, bool block_power = false) {
   const int l = k + p;
   RsvdInfo info;
   StageEvents ev;
@@ -148,7 +135,8 @@ RsvdInfo rsvd_stream(Ctx& c, const T* Ah, int64_t m, int64_t n, int64_t lda, boo
   } else {
     // column panels: Y = sum_J A_J Omega_J, then Y' = sum_J A_J (A_J^T Yn)
     DBuf<T> Yn(c, (size_t)m * l), Ynew(c, (size_t)m * l);
-    for (int it = 0; it <= q; ++it) {
+    const int iters = block_power ? 0 : q;
+    for (int it = 0; it <= iters; ++it) {
       T* acc = it == 0 ? Y.p : Ynew.p;
       BRSVD_CUDA(cudaMemsetAsync(acc, 0, sizeof(T) * m * l, c.stream));
       if (it > 0) normalize_sketch<T>(c, Y.p, m, l, m, Yn.p, m);
@@ -156,6 +144,10 @@ RsvdInfo rsvd_stream(Ctx& c, const T* Ah, int64_t m, int64_t n, int64_t lda, boo
         const int64_t w = j1 - j0;
         if (it == 0) {
           big_nn<T>(c, Ap, m, w, ld, false, X + j0, n, l, tmpY.p, m);
+          for (int pw = 0; block_power && pw < q; ++pw) {
+            big_tn<T>(c, Ap, m, w, ld, false, tmpY.p, m, l, tmpZ.p, pmax);
+            big_nn<T>(c, Ap, m, w, ld, false, tmpZ.p, pmax, l, tmpY.p, m);
+          }
         } else {
           big_tn<T>(c, Ap, m, w, ld, false, Yn.p, m, l, tmpZ.p, pmax);
           big_nn<T>(c, Ap, m, w, ld, false, tmpZ.p, pmax, l, tmpY.p, m);
@@ -213,8 +205,9 @@ RsvdInfo rsvd_stream(Ctx& c, const T* Ah, int64_t m, int64_t n, int64_t lda, boo
   info.ms_core = ev.ms(2, 3);
   info.ms_svd = ev.ms(3, 4);
   const double lim = std::log10(0.01 * finfo_max<T>());
+  const int qg = (block_power && !row_major) ? 0 : q;  // block sample is already powered
   info.log10_peak = (peak0 > 0.0 && s0 > 0.0)
-                        ? std::log10(peak0) + 2.0 * q * std::log10(s0)
+                        ? std::log10(peak0) + 2.0 * qg * std::log10(s0)
                         : (peak0 > 0.0 ? std::log10(peak0) : -400.0);
   info.overflow = !std::isfinite(s0) || info.log10_peak > lim;
   return info;

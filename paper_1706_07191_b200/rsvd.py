@@ -119,7 +119,7 @@ def host_outputs(m, n, l, npdt):
                 np.empty((l, n), dtype=npdt, order="C"))
 
 
-def run_rsvd(a, cfg, omega=None, warn=True):
+def run_rsvd(a, cfg, omega=None, warn=True, blocks=None):
     """One GPU decomposition; returns RsvdRun (factors + stats).
 
     ``a`` is a 2-D numpy array (host; results come back as numpy) or a torch
@@ -152,11 +152,17 @@ def run_rsvd(a, cfg, omega=None, warn=True):
         where = _lib.HOST
     keep, optr, owhere = _omega_arg(omega, n, l, npdt, device)
     stats = _lib.BrsvdStats()
+    bounds, nblk = None, 0
+    if blocks is not None and len(blocks) > 1:
+        edges = [int(blocks[0][0])] + [int(j1) for _, j1 in blocks]
+        bounds = (ctypes.c_int64 * len(edges))(*edges)
+        nblk = len(edges) - 1
     t0 = time.perf_counter()
-    rc = lib.brsvd_rsvd(ctx.handle, mat.ptr, m, n, mat.ld, mat.code, mat.layout, where,
-                        k, p, q, optr, owhere,
-                        ctypes.c_uint64(int(cfg.master_seed) & (2 ** 64 - 1)),
-                        ptrs[0], ptrs[1], ptrs[2], where, ctypes.byref(stats))
+    rc = lib.brsvd_rsvd_blocked(ctx.handle, mat.ptr, m, n, mat.ld, mat.code, mat.layout, where,
+                                k, p, q, optr, owhere,
+                                ctypes.c_uint64(int(cfg.master_seed) & (2 ** 64 - 1)),
+                                bounds, nblk, ptrs[0], ptrs[1], ptrs[2], where,
+                                ctypes.byref(stats))
     wall = time.perf_counter() - t0
     del keep
     _lib.check(rc)
@@ -195,7 +201,7 @@ def _load_store_to_device(store, plan):
     return dev.t()   # m x n column-major view
 
 
-def run_rsvd_stream(a, cfg, panel=None, nbuf=3, omega=None, warn=True):
+def run_rsvd_stream(a, cfg, panel=None, nbuf=3, omega=None, warn=True, block_power=False):
     """Out-of-core decomposition of a host-resident matrix (C ABI
     ``brsvd_rsvd_stream``): A is streamed over PCIe in panels of ``panel``
     rows (C-ordered ``a``) or columns (Fortran-ordered ``a``) through ``nbuf``
@@ -216,12 +222,12 @@ def run_rsvd_stream(a, cfg, panel=None, nbuf=3, omega=None, warn=True):
     keep, optr, owhere = _omega_arg(omega, n, l, mat.dtype, False)
     stats = _lib.BrsvdStats()
     t0 = time.perf_counter()
-    rc = _lib.load_library().brsvd_rsvd_stream(
+    rc = _lib.load_library().brsvd_rsvd_stream_blocked(
         ctx.handle, mat.ptr, m, n, mat.ld, mat.code, mat.layout, k, p, q, optr, owhere,
         ctypes.c_uint64(int(cfg.master_seed) & (2 ** 64 - 1)),
         ctypes.c_void_p(U.ctypes.data), ctypes.c_void_p(sigma.ctypes.data),
         ctypes.c_void_p(Vt.ctypes.data), _lib.HOST, int(panel), int(nbuf),
-        ctypes.byref(stats))
+        1 if block_power else 0, ctypes.byref(stats))
     wall = time.perf_counter() - t0
     del keep
     _lib.check(rc)
@@ -240,7 +246,12 @@ def _store_payload(store):
     return mm.T   # m x n, Fortran-ordered view
 
 
-def _run_store(store, cfg, memory_budget_bytes, stage_names):
+_MODES = ("global", "paper")
+
+
+def _run_store(store, cfg, memory_budget_bytes, stage_names, mode="global"):
+    if mode not in _MODES:
+        raise ValueError(f"mode must be one of {_MODES}, got {mode!r}")
     m, n = store.m, store.n
     cfg.validate(m, n)
     s = None if cfg.partitions == "auto" else int(cfg.partitions)
@@ -252,7 +263,8 @@ def _run_store(store, cfg, memory_budget_bytes, stage_names):
         # Out of core: the budget's column blocks are the streamed panels;
         # q + 2 passes over the store cross the boundary.
         t0 = time.perf_counter()
-        run = run_rsvd_stream(_store_payload(store), cfg, panel=plan.n_prime, nbuf=3)
+        run = run_rsvd_stream(_store_payload(store), cfg, panel=plan.n_prime, nbuf=3,
+                              block_power=(mode == "paper"))
         st = run.stats
         passes = st.words_read // (m * n)
         stats.words_read += int(st.words_read)
@@ -269,7 +281,7 @@ def _run_store(store, cfg, memory_budget_bytes, stage_names):
     t0 = time.perf_counter()
     a_dev = _load_store_to_device(store, plan)
     load_s = time.perf_counter() - t0
-    run = run_rsvd(a_dev, cfg)
+    run = run_rsvd(a_dev, cfg, blocks=list(plan) if mode == "paper" else None)
     f = run.factors
     factors = SvdFactors(U=f.U.cpu().numpy(), sigma=f.sigma.cpu().numpy(),
                          Vt=f.Vt.cpu().numpy(), target_rank=f.target_rank,
@@ -290,14 +302,21 @@ def _run_store(store, cfg, memory_budget_bytes, stage_names):
     return factors, stats, plan
 
 
-def brsvd_run(store, cfg, memory_budget_bytes=None):
+def brsvd_run(store, cfg, memory_budget_bytes=None, mode="global"):
     """Block randomized SVD of a stored matrix (rsvd.py:188-215) on the GPU.
 
-    Returns (factors, stats).  The store is streamed across the boundary once
-    into HBM; all power-iteration passes run from HBM.
+    Returns (factors, stats).  A store that fits the budget is streamed across
+    the boundary once into HBM and every pass runs from HBM; a larger one is
+    streamed in the budget's column blocks.
+
+    mode="global" (default): global power iteration, the semantics of
+    rsvd_incore / rsvd_naive_ooc (q + 2 passes when streamed).
+    mode="paper": the reference's per-block power iteration (Alg. 2,
+    rsvd.py:169-175) -- each column block's (A_J A_J^T)^q A_J Omega_J summed --
+    two passes for any q; identical to "global" when s = 1 or q = 0.
     """
     factors, stats, _ = _run_store(store, cfg, memory_budget_bytes,
-                                   ("sketch", "orthonormalize", "form_core", "svd"))
+                                   ("sketch", "orthonormalize", "form_core", "svd"), mode)
     return factors, stats
 
 
@@ -312,14 +331,14 @@ def rsvd_naive_ooc(store, cfg, memory_budget_bytes=None):
     return factors, stats
 
 
-def block_range_finder(store, cfg, memory_budget_bytes=None, plan=None):
+def block_range_finder(store, cfg, memory_budget_bytes=None, plan=None, mode="global"):
     """Orthonormal basis of the sample range (rsvd.py:150-185); returns (Q, plan).
 
     Q is the left factor U of the GPU decomposition: an orthonormal basis of
-    range(Y) (U = Q W with W orthogonal).
+    range(Y) (U = Q W with W orthogonal).  ``mode`` as in brsvd_run.
     """
     factors, stats, plan_used = _run_store(store, cfg, memory_budget_bytes,
-                                           ("sketch", "orthonormalize"))
+                                           ("sketch", "orthonormalize"), mode)
     return factors.U, (plan if plan is not None else plan_used)
 
 

@@ -93,3 +93,18 @@ def test_rpca_matches_reference():
 def test_shrink_piecewise():
     x = np.array([5.0, -5.0, 1.0, 0.0])
     np.testing.assert_array_equal(ref_cpu.soft_threshold(x, 2.0), [3.0, -3.0, 0.0, 0.0])
+
+
+@pytest.mark.parametrize("name", ["brsvd_paper_s4_q2.npz", "brsvd_paper_s3_q1.npz"])
+def test_paper_mode_matches_reference_brsvd_run(name):
+    """brsvd_run with s > 1, q >= 1: the per-block power iteration (two passes)."""
+    g = load(name)
+    k, p, q = int(g["k"]), int(g["p"]), int(g["q"])
+    blocks = [tuple(b) for b in g["blocks"]]
+    assert len(blocks) == int(g["s"])
+    out = ref_cpu.randomized_svd_paper(g["a"], k, p, q, blocks, seed=int(g["seed"]))
+    np.testing.assert_allclose(out["sigma"][:k], g["sigma"][:k], rtol=1e-10)
+    assert float(g["passes"]) == 2.0   # rsvd.py:188-193
+    # a different approximation from the global iteration (SURVEY §0.2)
+    glob = ref_cpu.randomized_svd(g["a"], k, p, q, seed=int(g["seed"]), omega=g["omega"])
+    assert np.max(np.abs(glob["sigma"][:k] - g["sigma"][:k]) / g["sigma"][:k]) > 1e-8
