@@ -222,6 +222,19 @@ BRSVD_API int brsvd_ialm(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n,
                          double* residuals, double* mus, double* svd_seconds,
                          double* iter_seconds);
 
+/* brsvd_ialm whose inner SVDs use the per-block power iteration over the
+ * column blocks [col_bounds[b], col_bounds[b+1]) -- the reference's
+ * out-of-core branch, which calls brsvd_run with the budget's plan
+ * (rpca.py:216-304, :274).  nblocks = 0: brsvd_ialm. */
+BRSVD_API int brsvd_ialm_blocked(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n,
+                                 int64_t ldm, int dtype, int layout, int where, int k, int p,
+                                 int q, uint64_t seed, const void* omega, double lam,
+                                 double mu0, double rho, double tol, int max_iterations,
+                                 const int64_t* col_bounds, int nblocks, void* L, void* S,
+                                 int out_where, int32_t* iterations, int32_t* converged,
+                                 double* residuals, double* mus, double* svd_seconds,
+                                 double* iter_seconds);
+
 /* ---- stage entry points for the row-sharded driver ---------------------
  * (paper_1706_07191_b200/distributed.py).  Device pointers only; the small
  * matrices are fp64 column-major.  Each replaces one step of the reference

@@ -150,6 +150,25 @@ def main():
                         converged=res.converged, norm2=n2)
     print("rpca iterations", res.iterations, "norm2", n2)
 
+    # RPCA out-of-core branch (rpca.py:216-304): store input, budget below the
+    # payload -> the inner SVD is brsvd_run over the budget's column blocks
+    budget = 192000
+    with tempfile.TemporaryDirectory() as d:
+        st = ref.MatrixStore.from_array(os.path.join(d, "m.oocm"), M)
+        cfgo = ref.RpcaConfig(target_rank=10, tol=1e-7, memory_budget_bytes=budget)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            reso = ref.ialm_rpca(st, cfgo)
+        Lo, So = reso.L.read_full(), reso.S.read_full()
+        plan = ref.plan_blocks(200, 200, 20, 8, memory_budget_bytes=budget)
+        st.close()
+    np.savez_compressed(os.path.join(OUT, "rpca_ooc.npz"), M=M, omega=omega, budget=budget,
+                        blocks=np.array(list(plan), dtype=np.int64), L=Lo, S=So,
+                        iterations=reso.iterations,
+                        residuals=np.array(reso.residual_history),
+                        converged=reso.converged)
+    print("rpca ooc iterations", reso.iterations, "blocks", len(list(plan)))
+
 
 if __name__ == "__main__":
     main()

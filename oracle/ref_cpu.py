@@ -223,8 +223,12 @@ def power_norm(mat, seed=0, tol=1e-10, max_iterations=100):
 
 
 def ialm(M, k, p=10, q=1, lam=None, mu0=None, rho=1.5, tol=1e-7,
-         max_iterations=100, seed=0):
-    """In-core inexact ALM robust PCA (rpca.py:168-213).
+         max_iterations=100, seed=0, blocks=None):
+    """Inexact ALM robust PCA: in-core (rpca.py:168-213) or, with ``blocks``
+    (the budget's column blocks), the out-of-core branch (rpca.py:216-304),
+    whose inner SVD is brsvd_run's per-block power iteration (rpca.py:274).
+    The out-of-core branch's block-wise W/L/S/Y updates are the same
+    elementwise arithmetic as the in-core ones.
 
     Returns dict(L, S, iterations, residuals, mus, converged).
     """
@@ -243,7 +247,8 @@ def ialm(M, k, p=10, q=1, lam=None, mu0=None, rho=1.5, tol=1e-7,
     it = 0
     for it in range(1, max_iterations + 1):
         W = M - S + Y / mu
-        f = randomized_svd(W, k, p, q, seed)
+        f = (randomized_svd(W, k, p, q, seed) if blocks is None
+             else randomized_svd_paper(W, k, p, q, blocks, seed=seed))
         L = (f["U"] * soft_threshold(f["sigma"], 1.0 / mu)) @ f["Vt"]
         S = soft_threshold(M - L + Y / mu, lam / mu)
         Z = M - L - S

@@ -27,7 +27,7 @@ EXPORTED = (
     "brsvd_spectral_norm", "brsvd_ialm", "brsvd_sketch_product", "brsvd_gram",
     "brsvd_chol_basis", "brsvd_apply", "brsvd_normalize", "brsvd_colmax",
     "brsvd_scale_cols", "brsvd_rsvd_stream", "brsvd_residual", "brsvd_rsvd_blocked",
-    "brsvd_rsvd_stream_blocked",
+    "brsvd_rsvd_stream_blocked", "brsvd_ialm_blocked",
 )
 
 
@@ -96,6 +96,10 @@ def _declare(lib):
     lib.brsvd_ialm.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, c_int, c_int,
                                c_int, u64, vp, dbl, dbl, dbl, dbl, c_int, vp, vp, c_int,
                                ctypes.POINTER(i32), ctypes.POINTER(i32), vp, vp, vp, vp]
+    lib.brsvd_ialm_blocked.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, c_int,
+                                       c_int, c_int, u64, vp, dbl, dbl, dbl, dbl, c_int, vp,
+                                       c_int, vp, vp, c_int, ctypes.POINTER(i32),
+                                       ctypes.POINTER(i32), vp, vp, vp, vp]
     lib.brsvd_sketch_product.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, vp,
                                          i64, i64, vp, i64]
     lib.brsvd_rsvd_stream.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, c_int, c_int,

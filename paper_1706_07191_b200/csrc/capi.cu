@@ -543,7 +543,22 @@ int brsvd_ialm(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n, int64_t ldm,
                void* L, void* S, int out_where, int32_t* iterations,
                int32_t* converged, double* residuals, double* mus, double* svd_seconds,
                double* iter_seconds) {
+  return brsvd_ialm_blocked(ctx, M, m, n, ldm, dtype, layout, where, k, p, q, seed, omega,
+                            lam, mu0, rho, tol, max_iterations, nullptr, 0, L, S, out_where,
+                            iterations, converged, residuals, mus, svd_seconds, iter_seconds);
+}
+
+int brsvd_ialm_blocked(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n, int64_t ldm,
+                       int dtype, int layout, int where, int k, int p, int q, uint64_t seed,
+                       const void* omega, double lam, double mu0, double rho, double tol,
+                       int max_iterations, const int64_t* col_bounds, int nblocks, void* L,
+                       void* S, int out_where, int32_t* iterations, int32_t* converged,
+                       double* residuals, double* mus, double* svd_seconds,
+                       double* iter_seconds) {
   return guarded([&] {
+    if (nblocks > 0)
+      BRSVD_REQUIRE(col_bounds != nullptr && col_bounds[0] == 0 && col_bounds[nblocks] == n,
+                    kErrShape, "column blocks must tile [0, n)");
     BRSVD_REQUIRE(ctx != nullptr, kErrArg, "ctx is NULL");
     BRSVD_REQUIRE(residuals && mus && svd_seconds && iter_seconds, kErrArg,
                   "history arrays are required");
@@ -568,11 +583,12 @@ int brsvd_ialm(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n, int64_t ldm,
       r = ialm_device<double>(c, (const double*)mv.dptr, m, n, row_major, k, p, q, seed,
                               (const double*)ov.dptr, lam, mu0, rho, tol, max_iterations, (double*)lo.dptr,
                               (double*)so.dptr, residuals, mus, svd_seconds,
-                              iter_seconds);
+                              iter_seconds, col_bounds, nblocks);
     else
       r = ialm_device<float>(c, (const float*)mv.dptr, m, n, row_major, k, p, q, seed,
                              (const float*)ov.dptr, lam, mu0, rho, tol, max_iterations, (float*)lo.dptr,
-                             (float*)so.dptr, residuals, mus, svd_seconds, iter_seconds);
+                             (float*)so.dptr, residuals, mus, svd_seconds, iter_seconds,
+                             col_bounds, nblocks);
     lo.flush();
     so.flush();
     BRSVD_CUDA(cudaStreamSynchronize(c.stream));

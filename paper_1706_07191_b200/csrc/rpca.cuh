@@ -320,7 +320,8 @@ IalmOut ialm_device(Ctx& c, const T* Mx, int64_t m, int64_t n, bool row_major, i
                     int p, int q, uint64_t seed, const T* omega, double lam, double mu0,
                     double rho,
                     double tol, int max_it, T* Lout, T* Sout, double* residuals,
-                    double* mus, double* svd_s, double* iter_s) {
+                    double* mus, double* svd_s, double* iter_s,
+                    const int64_t* blocks = nullptr, int nblk = 0) {
   const int l = k + p;
   const int64_t total = m * n;
   const int64_t ld = row_major ? n : m;
@@ -365,7 +366,10 @@ IalmOut ialm_device(Ctx& c, const T* Mx, int64_t m, int64_t n, bool row_major, i
   for (int it = 1; it <= max_it; ++it) {
     const auto t0 = std::chrono::steady_clock::now();
     ev.rec(0, c.stream);
-    rsvd_device<T>(c, W.p, m, n, ld, row_major, k, p, q, Om.p, seed, U.p, sig.p, V.p);
+    // blocks: the reference's out-of-core branch runs brsvd_run with the
+    // budget's column blocks (per-block power iteration, rpca.py:274)
+    rsvd_device<T>(c, W.p, m, n, ld, row_major, k, p, q, Om.p, seed, U.p, sig.p, V.p,
+                   nullptr, blocks, nblk);
     ev.rec(1, c.stream);
     int64_t np = 0;
     rpca_step<T>(c, 0, nf, ns, ld, l, F, ldf, G, ldg, sig.p, mu, lam, rho, Mx, Y.p, S,

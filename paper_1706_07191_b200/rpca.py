@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _lib
 from ._arrays import DeviceMatrix, HostMatrix, is_torch, torch_stream_ptr
-from .store import MatrixStore
+from .store import MatrixStore, plan_blocks
 
 __all__ = ["RpcaConfig", "RpcaResult", "shrink", "spectral_norm_estimate",
            "ialm_rpca"]
@@ -128,14 +128,23 @@ def ialm_rpca(m_input, cfg, omega=None):
     """
     cfg.validate()
     as_stores = False
+    blocks = None
     if isinstance(m_input, MatrixStore):
         budget = cfg.memory_budget_bytes
         as_stores = budget is not None and m_input.payload_bytes > budget
+        if as_stores:
+            # the reference's out-of-core branch calls brsvd_run(W, sketch,
+            # memory_budget_bytes=budget) (rpca.py:274): the inner SVDs use the
+            # per-block power iteration over that plan's column blocks
+            l_ = int(cfg.target_rank) + int(cfg.oversampling)
+            plan = plan_blocks(m_input.n, m_input.m, l_, m_input.element_size,
+                               memory_budget_bytes=budget)
+            blocks = list(plan)
         m_input = m_input.read_full()
     device = is_torch(m_input)
     mat = DeviceMatrix(m_input) if device else HostMatrix(m_input, "M")
     m, n = mat.shape
-    fn = _require("brsvd_ialm")
+    fn = _require("brsvd_ialm_blocked")
     ctx = _lib.context(getattr(mat, "device", None))
     maxit = int(cfg.max_iterations)
     if device:
@@ -178,6 +187,11 @@ def ialm_rpca(m_input, cfg, omega=None):
     else:
         om, optr = None, None
     dptr = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    bounds, nblk = None, 0
+    if blocks is not None and len(blocks) > 1:
+        edges = [int(blocks[0][0])] + [int(j1) for _, j1 in blocks]
+        bounds = (ctypes.c_int64 * len(edges))(*edges)
+        nblk = len(edges) - 1
     _lib.check(fn(
         ctx.handle, mat.ptr, m, n, mat.ld, mat.code, mat.layout, where,
         int(cfg.target_rank), int(cfg.oversampling), int(cfg.power_exponent),
@@ -185,7 +199,7 @@ def ialm_rpca(m_input, cfg, omega=None):
         ctypes.c_double(nan if cfg.lam is None else float(cfg.lam)),
         ctypes.c_double(nan if cfg.mu0 is None else float(cfg.mu0)),
         ctypes.c_double(float(cfg.rho)), ctypes.c_double(float(cfg.tol)), maxit,
-        lp, sp, where, ctypes.byref(iters), ctypes.byref(conv),
+        bounds, nblk, lp, sp, where, ctypes.byref(iters), ctypes.byref(conv),
         dptr(res), dptr(mus), dptr(svd_s), dptr(it_s)))
     k = iters.value
     residuals = [float(r) for r in res[:k]]

@@ -108,3 +108,14 @@ def test_paper_mode_matches_reference_brsvd_run(name):
     # a different approximation from the global iteration
     glob = ref_cpu.randomized_svd(g["a"], k, p, q, seed=int(g["seed"]), omega=g["omega"])
     assert np.max(np.abs(glob["sigma"][:k] - g["sigma"][:k]) / g["sigma"][:k]) > 1e-8
+
+
+def test_rpca_out_of_core_branch_matches_reference():
+    """rpca.py:216-304: store input above the budget; the inner SVD is the
+    per-block brsvd_run over the budget's column blocks."""
+    g = load("rpca_ooc.npz")
+    blocks = [(int(a), int(b)) for a, b in g["blocks"]]
+    out = ref_cpu.ialm(g["M"], 10, 10, 1, blocks=blocks)
+    assert out["iterations"] == int(g["iterations"])
+    np.testing.assert_allclose(out["residuals"], g["residuals"], rtol=1e-6)
+    np.testing.assert_allclose(out["L"], g["L"], atol=1e-8)
