@@ -140,6 +140,20 @@ BRSVD_API int brsvd_sketch_product(brsvd_ctx* ctx, const void* A, int64_t m, int
                                    const void* X, int64_t ldx, int64_t l, void* C,
                                    int64_t ldc);
 
+/* brsvd_sketch_product with the per-row (trans = 0) or per-column (trans = 1)
+ * maxima |A| of brsvd_absmax (float, device; NULL: computed per call), which
+ * set the power-of-two scales of the fp16-split tensor-core product.  A caller
+ * issuing several products on the same A computes them once. */
+BRSVD_API int brsvd_sketch_product_scaled(brsvd_ctx* ctx, const void* A, int64_t m,
+                                          int64_t n, int64_t lda, int dtype, int layout,
+                                          int trans, const void* X, int64_t ldx, int64_t l,
+                                          void* C, int64_t ldc, const float* amax);
+
+/* Row maxima (m) and column maxima (n) of |A| (fp32 A, device outputs; either
+ * may be NULL). */
+BRSVD_API int brsvd_absmax(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda,
+                           int dtype, int layout, float* row_max, float* col_max);
+
 /* Fused residual of a rank-l factorisation, one pass over A
  * (relative_frobenius_error, rsvd.py:396-432):
  *   out[0] = ||A - U diag(sigma) Vt||_F^2,   out[1] = ||A||_F^2   (fp64, host)

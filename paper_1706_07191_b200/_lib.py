@@ -27,7 +27,8 @@ EXPORTED = (
     "brsvd_spectral_norm", "brsvd_ialm", "brsvd_sketch_product", "brsvd_gram",
     "brsvd_chol_basis", "brsvd_apply", "brsvd_normalize", "brsvd_colmax",
     "brsvd_scale_cols", "brsvd_rsvd_stream", "brsvd_residual", "brsvd_rsvd_blocked",
-    "brsvd_rsvd_stream_blocked", "brsvd_ialm_blocked",
+    "brsvd_rsvd_stream_blocked", "brsvd_ialm_blocked", "brsvd_sketch_product_scaled",
+    "brsvd_absmax",
 )
 
 
@@ -102,6 +103,9 @@ def _declare(lib):
                                        ctypes.POINTER(i32), vp, vp, vp, vp]
     lib.brsvd_sketch_product.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, vp,
                                          i64, i64, vp, i64]
+    lib.brsvd_sketch_product_scaled.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int,
+                                                vp, i64, i64, vp, i64, vp]
+    lib.brsvd_absmax.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, vp, vp]
     lib.brsvd_rsvd_stream.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, c_int, c_int,
                                       vp, c_int, u64, vp, vp, vp, c_int, i64, c_int,
                                       ctypes.POINTER(BrsvdStats)]

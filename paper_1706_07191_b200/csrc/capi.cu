@@ -374,6 +374,14 @@ int brsvd_residual(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t 
 int brsvd_sketch_product(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda,
                          int dtype, int layout, int trans, const void* X, int64_t ldx,
                          int64_t l, void* C, int64_t ldc) {
+  return brsvd_sketch_product_scaled(ctx, A, m, n, lda, dtype, layout, trans, X, ldx, l, C,
+                                     ldc, nullptr);
+}
+
+int brsvd_sketch_product_scaled(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n,
+                                int64_t lda, int dtype, int layout, int trans, const void* X,
+                                int64_t ldx, int64_t l, void* C, int64_t ldc,
+                                const float* amax) {
   return guarded([&] {
     BRSVD_REQUIRE(ctx != nullptr, kErrArg, "ctx is NULL");
     Ctx& c = ctx->c;
@@ -390,13 +398,25 @@ int brsvd_sketch_product(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, in
                        (int)l, (double*)C, ldc);
     } else {
       if (trans)
-        big_tn<float>(c, (const float*)A, m, n, lda, row_major, (const float*)X, ldx,
-                      (int)l, (float*)C, ldc);
+        big_tn<float>(c, (const float*)A, m, n, lda, row_major, (const float*)X, ldx, (int)l,
+                      (float*)C, ldc, amax);
       else
-        big_nn<float>(c, (const float*)A, m, n, lda, row_major, (const float*)X, ldx,
-                      (int)l, (float*)C, ldc);
+        big_nn<float>(c, (const float*)A, m, n, lda, row_major, (const float*)X, ldx, (int)l,
+                      (float*)C, ldc, amax);
     }
-    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+    return (int)kOk;
+  });
+}
+
+int brsvd_absmax(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda, int dtype,
+                 int layout, float* row_max, float* col_max) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && A != nullptr, kErrArg, "NULL argument");
+    BRSVD_REQUIRE(dtype == BRSVD_F32, kErrArg, "absmax scales serve the fp32 products");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    absmax_rows_cols(c, (const float*)A, m, n, lda, layout == BRSVD_ROW_MAJOR, row_max,
+                     col_max);
     return (int)kOk;
   });
 }
@@ -616,7 +636,6 @@ int brsvd_gram(brsvd_ctx* ctx, const void* X, int64_t r, int64_t k1, int64_t ldx
     else
       gemm_tn_cm<float, float, double>(c, k1, k2, r, (const float*)X, ldx, (const float*)W,
                                        ldw, G, k1);
-    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
     return (int)kOk;
   });
 }
@@ -661,12 +680,13 @@ int brsvd_apply(brsvd_ctx* ctx, const void* X, int64_t r, int64_t k, int64_t ldx
 #define BRSVD_APPLY(TX, TO)                                                                \
   gemm_nn_cm<TX, double, TO>(c, r, kt, k, (const TX*)X, ldx, T, k, (TO*)out, ldo, alpha, \
                              beta, beta != 0.0 ? (const TO*)out : nullptr, ldo)
-    if (dtype == BRSVD_F64 && out_dtype == BRSVD_F64) BRSVD_APPLY(double, double);
+    if (dtype == BRSVD_F32 && out_dtype == BRSVD_F32 && alpha == 1.0 && beta == 0.0)
+      apply_basis<float>(c, (const float*)X, r, (int)k, ldx, T, k, (int)kt, (float*)out, ldo);
+    else if (dtype == BRSVD_F64 && out_dtype == BRSVD_F64) BRSVD_APPLY(double, double);
     else if (dtype == BRSVD_F64) BRSVD_APPLY(double, float);
     else if (out_dtype == BRSVD_F64) BRSVD_APPLY(float, double);
     else BRSVD_APPLY(float, float);
 #undef BRSVD_APPLY
-    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
     return (int)kOk;
   });
 }
@@ -682,7 +702,6 @@ int brsvd_normalize(brsvd_ctx* ctx, const void* Z, int64_t n, int64_t l, int64_t
       normalize_sketch<double>(c, (const double*)Z, n, (int)l, ldz, (double*)Zout, ldo);
     else
       normalize_sketch<float>(c, (const float*)Z, n, (int)l, ldz, (float*)Zout, ldo);
-    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
     return (int)kOk;
   });
 }
@@ -727,7 +746,6 @@ int brsvd_scale_cols(brsvd_ctx* ctx, void* X, int64_t r, int64_t l, int64_t ldx,
       scale_cols_by_kernel<float, double><<<grid_for(r * l), 256, 0, c.stream>>>(
           (float*)X, r, l, ldx, ds.p);
     BRSVD_CHECK_LAUNCH();
-    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
     return (int)kOk;
   });
 }

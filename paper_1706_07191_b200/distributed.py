@@ -131,7 +131,22 @@ class GpuOps:
     def dtype_of(self, A):
         return A.dtype
 
-    def product(self, A, X, trans):
+    def absmax(self, A):
+        """(row maxima, column maxima) of |A| for the fp16-split products
+        (brsvd_absmax), once per decomposition; None for fp64 data."""
+        from ._arrays import DeviceMatrix
+        if A.dtype != self.torch.float32:
+            return None
+        self._sync_stream()
+        mat = DeviceMatrix(A)
+        m, n = mat.shape
+        rmax = self.torch.empty(m, dtype=self.torch.float32, device=self.device)
+        cmax = self.torch.empty(n, dtype=self.torch.float32, device=self.device)
+        _lib.check(self.lib.brsvd_absmax(self.ctx.handle, mat.ptr, m, n, mat.ld, mat.code,
+                                         mat.layout, _vp(rmax), _vp(cmax)))
+        return rmax, cmax
+
+    def product(self, A, X, trans, amax=None):
         from ._arrays import DeviceMatrix
         self._sync_stream()
         mat = DeviceMatrix(A)
@@ -139,9 +154,10 @@ class GpuOps:
         rows = n if trans else m
         l = X.shape[1]
         C = _cm_empty(rows, l, A.dtype, self.device)
-        _lib.check(self.lib.brsvd_sketch_product(
+        scale = None if amax is None else _vp(amax[1] if trans else amax[0])
+        _lib.check(self.lib.brsvd_sketch_product_scaled(
             self.ctx.handle, mat.ptr, m, n, mat.ld, mat.code, mat.layout, int(trans),
-            _vp(X), _ld(X), l, _vp(C), rows))
+            _vp(X), _ld(X), l, _vp(C), rows, scale))
         return C
 
     def gram(self, X, W=None):
@@ -245,11 +261,22 @@ class GpuOps:
 
 # ---------------------------------------------------------------------------
 def _orth_sharded(Y, ops, comm, eps_data, row_offset, m_total, seed):
-    """Rank-revealing CholQR2 of the row-sharded Y (runtime.cuh orth_full,
+    """Rank-revealing CholQR2 of the row-sharded Y (orth.cuh orth_full,
     level 1 + completion) with all-reduced Grams."""
     l = Y.shape[1]
     G = comm.allreduce_sum(ops.gram(Y))
     T, kept, rank_ref = ops.chol_basis(G, 0.0, 4.0 * l * eps_data, l * eps_data, 1e-12)
+    if eps_data > 1e-10:
+        # fp32 data (orth_full_f32): fp32 basis, the dropped directions
+        # completed by Gaussian columns inside the second CholQR pass
+        dt = ops.dtype_of(Y)
+        Q1 = ops.apply(Y, ops.cols(T, kept), dt) if kept > 0 else None
+        if kept < l:
+            W = ops.gaussian(Y.shape[0], l - kept, seed, 0x636f6d706c657465, row_offset, dt)
+            Q1 = W if Q1 is None else ops.hstack(Q1, W)
+        G2 = comm.allreduce_sum(ops.gram(Q1))
+        T2, _, _ = ops.chol_basis(G2)
+        return ops.apply(Q1, T2, dt), min(rank_ref, kept)
     f64 = ops.torch.float64 if hasattr(ops, "torch") else np.float64
     Q = None
     if kept > 0:
@@ -292,7 +319,8 @@ def rsvd_sharded(A_local, cfg, row_offset, m_total, comm=None, ops=None, omega=N
     eps_data = _EPS[npdt]
     seed = int(cfg.master_seed)
     X = ops.asarray(omega, dtype) if omega is not None else ops.gaussian(n, l, seed, 0, 0, dtype)
-    Y = ops.product(A_local, X, False)
+    amax = ops.absmax(A_local) if hasattr(ops, "absmax") else None
+    Y = ops.product(A_local, X, False, amax)
     vals, _ = ops.colmax(Y, row_offset)
     bad = not np.all(np.isfinite(vals)) or np.any(vals < 0)
     peak0 = comm.allreduce_max(float(np.max(vals)) if vals.size else 0.0)
@@ -300,11 +328,11 @@ def rsvd_sharded(A_local, cfg, row_offset, m_total, comm=None, ops=None, omega=N
     if bad:
         raise FloatingPointError("sample matrix is not finite; the overflow guard fires")
     for _ in range(q):
-        Z = comm.allreduce_sum(ops.product(A_local, Y, True))
-        Y = ops.product(A_local, ops.normalize(Z), False)
+        Z = comm.allreduce_sum(ops.product(A_local, Y, True, amax))
+        Y = ops.product(A_local, ops.normalize(Z), False, amax)
     Q, rank_y = _orth_sharded(Y, ops, comm, eps_data, row_offset, m_total, seed ^ 0x7153)
     Qd = ops.cast(Q, dtype)
-    Bt = comm.allreduce_sum(ops.product(A_local, Qd, True))
+    Bt = comm.allreduce_sum(ops.product(A_local, Qd, True, amax))
     W, sigma, Vt, rank_b = ops.small_svd(Bt)
     U = ops.apply(Q, W, dtype)
     # _fix_signs (rsvd.py:105-115) over the global rows

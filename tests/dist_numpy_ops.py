@@ -19,7 +19,10 @@ class NumpyOps:
     def asarray(self, x, dtype):
         return np.asfortranarray(np.asarray(x), dtype=dtype)
 
-    def product(self, A, X, trans):
+    def absmax(self, A):
+        return None   # scales of the fp16-split tensor-core products: GPU only
+
+    def product(self, A, X, trans, amax=None):
         return np.asfortranarray((A.T if trans else A) @ X)
 
     def gram(self, X, W=None):
