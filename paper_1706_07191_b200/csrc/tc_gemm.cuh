@@ -34,12 +34,17 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 16;              // fp32 K elements per stage (64-byte rows)
-constexpr int STAGES = 6;
+constexpr int STAGES_TF32 = 6;   // smem ring depth (TMEM A slots: 6 x 32 columns)
+constexpr int STAGES_H16 = 6;    // fp16 split: 6 x 32 TMEM columns (32 k per stage)
 constexpr int NPAD_MAX = 320;   // l <= 320: two CTAs of <= 160 columns
 constexpr int kThreads = 640;   // 4 role warps + 16 converter warps
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kASlot = 320;    // TMEM columns [320, 512): six A staging slots
 constexpr uint32_t A_STAGE_BYTES = BM * BK * 4;
+// fp16 split: 32 k values per stage (128-byte fp32 A rows, 64-byte fp16 B
+// rows) -- half the stages, barrier round trips and TMA issues per byte of A
+constexpr int BK_H16 = 32;
+constexpr uint32_t A_STAGE_BYTES_H16 = BM * BK_H16 * 4;
 
 struct Params {
   int64_t M, K;
@@ -238,11 +243,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const __grid_constant__ CUtensorMap mapBhi,
                     const __grid_constant__ CUtensorMap mapBlo, const Params p) {
   constexpr int NH = NCMAX / 4;                          // running sums per thread
+  // deeper ring for the fp16 split: the stage round trip (TMA -> convert ->
+  // MMA -> commit) is latency-bound, so throughput scales with stages in flight
+  constexpr int STAGES = H16 ? STAGES_H16 : STAGES_TF32;
+  constexpr int BKK = H16 ? BK_H16 : BK;                  // k values per stage
+  constexpr uint32_t ASB = H16 ? A_STAGE_BYTES_H16 : A_STAGE_BYTES;
+  constexpr int CHUNK = 128 / BKK;                        // stages per accumulator chunk
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_dyn + 1023) & ~(uintptr_t)1023);
   const int nc = p.rows_c;                               // columns of this CTA
-  const uint32_t b_bytes = (uint32_t)nc * BK * (H16 ? 2 : 4);  // one of hi / lo
-  const uint32_t stage_bytes = A_STAGE_BYTES + 2 * b_bytes;
+  const uint32_t b_bytes = (uint32_t)nc * BKK * (H16 ? 2 : 4);  // one of hi / lo
+  const uint32_t stage_bytes = ASB + 2 * b_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * stage_bytes);
   uint64_t* freeb = full + STAGES;
   uint64_t* tfull = freeb + STAGES;
@@ -256,11 +267,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tile = blockIdx.x / p.ksplit;
   const int64_t m0 = (int64_t)(tile / tiles_n) * BM;
   const int n0 = (tile % tiles_n) * nc;
-  const int nk_all = (int)((p.K + BK - 1) / BK);
+  const int nk_all = (int)((p.K + BKK - 1) / BKK);
   const int per = (nk_all + p.ksplit - 1) / p.ksplit;
   const int kb_begin = ks * per;
   const int nk = max(0, min(nk_all, kb_begin + per) - kb_begin);
-  const int nchunk = (nk + kChunkKB - 1) / kChunkKB;
+  const int nchunk = (nk + CHUNK - 1) / CHUNK;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -296,17 +307,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ph = (kb / STAGES) & 1;
         mbar_wait(&freeb[s], ph ^ 1);
         uint8_t* st = smem + (size_t)s * stage_bytes;
+        const int k0 = (kb_begin + kb) * BKK;
         mbar_expect_tx(&full[s], stage_bytes);
-        const int k0 = (kb_begin + kb) * BK;
         if (A_KMAJOR) {
           tma_load_2d(st, &mapA, &full[s], k0, (int)m0);
         } else {
 #pragma unroll
           for (int b = 0; b < 4; ++b)
-            tma_load_2d(st + b * (32 * BK * 4), &mapA, &full[s], (int)m0 + 32 * b, k0);
+            tma_load_2d(st + b * (32 * BKK * 4), &mapA, &full[s], (int)m0 + 32 * b, k0);
         }
-        tma_load_2d(st + A_STAGE_BYTES, &mapBhi, &full[s], k0, n0);
-        tma_load_2d(st + A_STAGE_BYTES + b_bytes, &mapBlo, &full[s], k0, n0);
+        tma_load_2d(st + ASB, &mapBhi, &full[s], k0, n0);
+        tma_load_2d(st + ASB + b_bytes, &mapBlo, &full[s], k0, n0);
       }
     }
   } else if (warp == 1) {
@@ -318,24 +329,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % STAGES;
         const uint32_t ph = (kb / STAGES) & 1;
-        const int chunk = kb / kChunkKB;
+        const int chunk = kb / CHUNK;
         const int buf = chunk & 1;
-        const bool chunk_start = (kb % kChunkKB) == 0;
+        const bool chunk_start = (kb % CHUNK) == 0;
         if (chunk_start && chunk >= 2) mbar_wait(&accfree[buf], ((chunk >> 1) - 1) & 1);
         mbar_wait(&tfull[s], ph);
         mbar_wait(&full[s], ph);
         tc_after_sync();
-        const uint32_t bh = smem_u32(smem + (size_t)s * stage_bytes + A_STAGE_BYTES);
+        const uint32_t bh = smem_u32(smem + (size_t)s * stage_bytes + ASB);
         const uint32_t bl = bh + b_bytes;
         const uint32_t d = tmem + (uint32_t)(buf * nc);
         if constexpr (H16) {
-          // one K=16 step: A hi/lo in 8 TMEM columns each (fp16 pairs)
-          const uint32_t a_hi = tmem + kASlot + s * 16, a_lo = a_hi + 8;
-          const uint64_t dh = desc_kmajor_sw32(bh), dl = desc_kmajor_sw32(bl);
-          const uint32_t acc = chunk_start ? 0u : 1u;
-          mma_f16_ts(d, a_lo, dh, idesc, acc);
-          mma_f16_ts(d, a_hi, dl, idesc, 1u);
-          mma_f16_ts(d, a_hi, dh, idesc, 1u);
+          // two K=16 steps; A hi / lo in 16 TMEM columns each (fp16 pairs),
+          // B rows of 64 bytes (32 fp16), 64-byte swizzle
+          const uint32_t a_hi = tmem + kASlot + s * 32, a_lo = a_hi + 16;
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            const uint64_t dh = desc_kmajor_sw64(bh + kk * 32);
+            const uint64_t dl = desc_kmajor_sw64(bl + kk * 32);
+            const uint32_t acc = (chunk_start && kk == 0) ? 0u : 1u;
+            mma_f16_ts(d, a_lo + kk * 8, dh, idesc, acc);
+            mma_f16_ts(d, a_hi + kk * 8, dl, idesc, 1u);
+            mma_f16_ts(d, a_hi + kk * 8, dh, idesc, 1u);
+          }
         } else {
           const uint32_t a_hi = tmem + kASlot + s * 32, a_lo = a_hi + 16;
 #pragma unroll
@@ -349,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         mma_commit(&freeb[s]);
-        if ((kb % kChunkKB) == kChunkKB - 1 || kb == nk - 1) mma_commit(&accready[buf]);
+        if ((kb % CHUNK) == CHUNK - 1 || kb == nk - 1) mma_commit(&accready[buf]);
       }
     }
   } else if (warp >= 4) {  // ---------------- converters + accumulator flushes
@@ -398,37 +414,57 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t ph = (kb / STAGES) & 1;
       mbar_wait(&full[s], ph);
       const uint32_t sa = smem_base + (uint32_t)s * stage_bytes;
-      float v[8];
-      if (A_KMAJOR) {
-        // 64-byte rows; TMA 64B swizzle puts 16B chunk j of row r at j^((r>>1)&3)
-        const uint32_t row = sa + r * 64;
-#pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          const int j = 2 * half + jj;
-          const float4 x = lds128(row + ((j ^ ((r >> 1) & 3)) << 4));
-          v[4 * jj + 0] = x.x;
-          v[4 * jj + 1] = x.y;
-          v[4 * jj + 2] = x.z;
-          v[4 * jj + 3] = x.w;
-        }
-      } else {
-        // four (32 rows x 16 k) boxes, 32 consecutive rows per k
-        const uint32_t box = sa + wq * (32 * BK * 4) + lane * 4;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = lds32(box + (8 * half + k) * 128);
-      }
       if constexpr (H16) {
-        uint32_t hi[4], lo[4];
+        // 16 k values of row r: k = 16 half .. + 15
+        float v[16];
+        if (A_KMAJOR) {
+          // 128-byte rows; TMA 128B swizzle puts 16B chunk j of row r at j^(r&7)
+          const uint32_t row = sa + r * 128;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+          for (int jj = 0; jj < 4; ++jj) {
+            const int j = 4 * half + jj;
+            const float4 x = lds128(row + ((j ^ (r & 7)) << 4));
+            v[4 * jj + 0] = x.x;
+            v[4 * jj + 1] = x.y;
+            v[4 * jj + 2] = x.z;
+            v[4 * jj + 3] = x.w;
+          }
+        } else {
+          // four (32 rows x 32 k) boxes, 32 consecutive rows per k
+          const uint32_t box = sa + wq * (32 * BKK * 4) + lane * 4;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) v[k] = lds32(box + (16 * half + k) * 128);
+        }
+        uint32_t hi[8], lo[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
           const float x0 = v[2 * i] * rscale, x1 = v[2 * i + 1] * rscale;
           hi[i] = pack_h2(x0, x1);
           const float2 hf = unpack_h2(hi[i]);
           lo[i] = pack_h2(x0 - hf.x, x1 - hf.y);
         }
-        tmem_st4(tmem + lane_base + kASlot + s * 16 + 4 * half, hi);
-        tmem_st4(tmem + lane_base + kASlot + s * 16 + 8 + 4 * half, lo);
+        tmem_st8(tmem + lane_base + kASlot + s * 32 + 8 * half, hi);
+        tmem_st8(tmem + lane_base + kASlot + s * 32 + 16 + 8 * half, lo);
       } else {
+        float v[8];
+        if (A_KMAJOR) {
+          // 64-byte rows; TMA 64B swizzle puts 16B chunk j of row r at j^((r>>1)&3)
+          const uint32_t row = sa + r * 64;
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) {
+            const int j = 2 * half + jj;
+            const float4 x = lds128(row + ((j ^ ((r >> 1) & 3)) << 4));
+            v[4 * jj + 0] = x.x;
+            v[4 * jj + 1] = x.y;
+            v[4 * jj + 2] = x.z;
+            v[4 * jj + 3] = x.w;
+          }
+        } else {
+          // four (32 rows x 16 k) boxes, 32 consecutive rows per k
+          const uint32_t box = sa + wq * (32 * BK * 4) + lane * 4;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] = lds32(box + (8 * half + k) * 128);
+        }
         uint32_t hi[8], lo[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -444,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tfull[s]);
       // earlier chunks' accumulators are complete once this chunk started
-      while (flushed < kb / kChunkKB) flush(flushed++);
+      while (flushed < kb / CHUNK) flush(flushed++);
     }
     while (flushed < nchunk) flush(flushed++);
     const int64_t row = m0 + r;
@@ -615,8 +651,10 @@ inline Geometry geometry(int l) {
 }
 
 inline size_t smem_bytes(int rows_c, bool h16 = false) {
-  return (size_t)STAGES * (A_STAGE_BYTES + 2u * (uint32_t)rows_c * BK * (h16 ? 2 : 4)) + 128 +
-         1024;
+  return h16 ? (size_t)STAGES_H16 * (A_STAGE_BYTES_H16 + 2u * (uint32_t)rows_c * BK_H16 * 2) +
+                   512 + 1024
+             : (size_t)STAGES_TF32 * (A_STAGE_BYTES + 2u * (uint32_t)rows_c * BK * 4) + 512 +
+                   1024;
 }
 
 inline bool env_enabled() {
@@ -692,9 +730,12 @@ inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, 
   // A as stored: row-major (m x n) has n contiguous; column-major has m contiguous.
   const uint64_t inner = row_major ? (uint64_t)n : (uint64_t)m;
   const uint64_t outer = row_major ? (uint64_t)m : (uint64_t)n;
+  const bool h16m = h16_enabled();
+  const uint32_t bka = h16m ? BK_H16 : BK;
   const CUtensorMap mapA =
-      kmajor ? make_map(A, inner, outer, (uint64_t)lda * 4, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B)
-             : make_map(A, inner, outer, (uint64_t)lda * 4, 32, BK, CU_TENSOR_MAP_SWIZZLE_NONE);
+      kmajor ? make_map(A, inner, outer, (uint64_t)lda * 4, bka, BM,
+                        h16m ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)
+             : make_map(A, inner, outer, (uint64_t)lda * 4, 32, bka, CU_TENSOR_MAP_SWIZZLE_NONE);
   Params p;
   p.M = M;
   p.K = K;
@@ -732,11 +773,11 @@ inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, 
         X, K, l, ldx, g.npad, kld, bmax.p, reinterpret_cast<uint16_t*>(hi.p),
         reinterpret_cast<uint16_t*>(lo.p), cinv.p);
     BRSVD_CHECK_LAUNCH();
-    mapBhi = make_map(hi.p, (uint64_t)kld, (uint64_t)g.npad, (uint64_t)kld * 2, BK,
-                      (uint32_t)g.rows_c, CU_TENSOR_MAP_SWIZZLE_32B,
+    mapBhi = make_map(hi.p, (uint64_t)kld, (uint64_t)g.npad, (uint64_t)kld * 2, BK_H16,
+                      (uint32_t)g.rows_c, CU_TENSOR_MAP_SWIZZLE_64B,
                       CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
-    mapBlo = make_map(lo.p, (uint64_t)kld, (uint64_t)g.npad, (uint64_t)kld * 2, BK,
-                      (uint32_t)g.rows_c, CU_TENSOR_MAP_SWIZZLE_32B,
+    mapBlo = make_map(lo.p, (uint64_t)kld, (uint64_t)g.npad, (uint64_t)kld * 2, BK_H16,
+                      (uint32_t)g.rows_c, CU_TENSOR_MAP_SWIZZLE_64B,
                       CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
     p.row_max = opa_max;
     p.col_inv = cinv.p;
