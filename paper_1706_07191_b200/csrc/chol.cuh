@@ -254,7 +254,8 @@ __device__ long long g_ci_t[64];
 __host__ __device__ inline int cholinv_ldp(int n) { return (n + 3) & ~3; }
 __host__ __device__ inline size_t cholinv_big(int n) {
   const size_t p1 = (size_t)n * kCiLd + (size_t)kCiNB * cholinv_ldp(n);  // phase 1 panels
-  const size_t p2 = (size_t)2 * kCiNB * n;                              // phase 2
+  const size_t nblk = (size_t)(n + kCiNB - 1) / kCiNB;
+  const size_t p2 = (2 * nblk + 2) * kCiNB * kCiLd;                     // phase 2
   return p1 > p2 ? p1 : p2;
 }
 inline size_t cholinv_smem(int n) {
@@ -388,57 +389,33 @@ __global__ void __launch_bounds__(kCiThreads, 1)
       // zero the strict upper triangle of the block
       for (int j = r + 1; j < nb; ++j) Lrow[j] = 0.0;
       __syncwarp();
-      if (pi == 0) CI_T(9);
-      // Di = L11^-1 (lower); lane c computes column c from its own earlier
-      // entries, two partial sums per row
-      const int c = lane;
-      double rinv[1];
-      for (int rr = 0; rr < nb; ++rr) {
-        rinv[0] = Di[kCiNB * kCiLd - kCiNB + rr];
-        double v0 = (rr == c) ? 1.0 : 0.0, v1 = 0.0;
-        if (rr > c) {
-          const double* lr = Lp + rr * kCiLd;
-          int k = c;
-#pragma unroll 4
-          for (; k + 1 < rr; k += 2) {
-            v0 = fma(-lr[k], Di[k * kCiLd + c], v0);
-            v1 = fma(-lr[k + 1], Di[(k + 1) * kCiLd + c], v1);
-          }
-          if (k < rr) v0 = fma(-lr[k], Di[k * kCiLd + c], v0);
-        }
-        const double x = (rr >= c && c < nb) ? (v0 + v1) * rinv[0] : 0.0;
-        __syncwarp();
-        Di[rr * kCiLd + c] = x;
-        __syncwarp();
-      }
     }
     __syncthreads();
     if (pi == 0) CI_T(3);
-    // TRSM: L21 = A21 L11^-T (rows nb..rows-1) into the k-major copy PT
-    // (zero-padded to a multiple of 4 rows); dropped columns are zero.
+    // TRSM: L21 = A21 L11^-T (rows nb..rows-1) by forward substitution, one
+    // thread per row with the row in registers (L11 rows broadcast from
+    // shared memory), into the k-major copy PT (zero-padded to a multiple of 4
+    // rows).  Dropped columns are zero (their L11 column is e_c).
     const int rpad = (rows + 3) & ~3;
     {
-      // thread = (row i, group of 4 columns); one load of L[i][k] feeds four
-      // independent accumulator chains
-      const int nr = rpad - nb;
-      const int ng = (nb + 3) / 4;
-      for (int e = tid; e < nr * ng; e += nt) {
-        const int i = nb + e % nr, c0 = 4 * (e / nr);
-        double v[4] = {0.0, 0.0, 0.0, 0.0};
-        if (i < rows) {
-          const double* li = Lp + i * kCiLd;
-          const int kend = min(c0 + 3, nb - 1);
-#pragma unroll 4
-          for (int k = 0; k <= kend; ++k) {
-            const double lv = li[k];
+      const double* rinv = Di + kCiNB * kCiLd - kCiNB;   // 1 / L11[c][c] (factor scratch)
+      for (int i = nb + tid; i < rpad; i += nt) {
+        double x[kCiNB];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (k <= c0 + q && c0 + q < nb) v[q] = fma(lv, Di[(c0 + q) * kCiLd + k], v[q]);
+        for (int c = 0; c < kCiNB; ++c) x[c] = (i < rows && c < nb) ? Lp[i * kCiLd + c] : 0.0;
+#pragma unroll
+        for (int c = 0; c < kCiNB; ++c) {
+          if (c < nb) {
+            const double* lc = Lp + c * kCiLd;
+            double v = x[c];
+#pragma unroll
+            for (int k = 0; k < c; ++k) v = fma(-x[k], lc[k], v);
+            x[c] = dropped[p0 + c] ? 0.0 : v * rinv[c];
           }
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (c0 + q < nb) PT[(c0 + q) * ldp + i] = dropped[p0 + c0 + q] ? 0.0 : v[q];
+        for (int c = 0; c < kCiNB; ++c)
+          if (c < nb) PT[c * ldp + i] = i < rows ? x[c] : 0.0;
       }
     }
     __syncthreads();
@@ -448,10 +425,6 @@ __global__ void __launch_bounds__(kCiThreads, 1)
         const int i = e % rows, c = e / rows;
         if (i >= c)
           A[(int64_t)(p0 + c) * ld + (p0 + i)] = i < nb ? Lp[i * kCiLd + c] : PT[c * ldp + i];
-      }
-      for (int e = tid; e < nb * nb; e += nt) {
-        const int r = e % nb, c = e / nb;
-        X[(int64_t)(p0 + c) * n + (p0 + r)] = Di[r * kCiLd + c];
       }
     }
     if (pi == 0) CI_T(4);
@@ -512,79 +485,194 @@ __global__ void __launch_bounds__(kCiThreads, 1)
   }
 
   CI_T(6);
-  // ---- phase 2: X = L^-1 by block rows ----------------------------------
-  double* Lr = cism;                      // Lr[k * 32 + r]: block row of L, k < i0
-  double* Rr = cism + (size_t)kCiNB * n;  // Rr[col * 32 + r]: rhs
-  for (int i0 = kCiNB; i0 < n; i0 += kCiNB) {
-    const int nbI = min(kCiNB, n - i0);
-    for (int e = tid; e < i0 * nbI; e += nt) {
-      const int r = e % nbI, k = e / nbI;
-      Lr[k * kCiNB + r] = A[(int64_t)k * ld + (i0 + r)];
+  // ---- phase 2: T = S L^-T by block columns of X = L^-1 -----------------
+  // Block column J of X depends only on L: X_JJ = L_JJ^-1 and, for I > J,
+  // X_IJ = -L_II^-1 sum_{K=J..I-1} L_IK X_KJ.  Every CTA inverts the diagonal
+  // blocks (one warp each), then builds its own block columns J = me, me+C, ..
+  // in shared memory and writes rows J of T (T[k][j] = s_k X[j][k]) directly;
+  // no cluster barrier.
+  const int nblk = (n + kCiNB - 1) / kCiNB;
+  constexpr int BB = kCiNB * kCiLd;                      // one 32 x 33 block
+  double* Dinv = cism;                                   // nblk blocks: L_II^-1
+  double* Xc = cism + (size_t)nblk * BB;                 // nblk blocks: column J of X
+  double* Rb = Xc + (size_t)nblk * BB;                   // scratch block
+  double* Lt = Rb + BB;                                  // staged L_IK block
+  // diagonal blocks of L -> Xc (scratch), inverted by one warp each into Dinv
+  for (int e = tid; e < nblk * kCiNB * kCiNB; e += nt) {
+    const int bI = e / (kCiNB * kCiNB), rc = e % (kCiNB * kCiNB);
+    const int r = rc % kCiNB, cc = rc / kCiNB, i0 = bI * kCiNB;
+    const bool ok = i0 + r < n && i0 + cc < n && r >= cc;
+    Xc[(size_t)bI * BB + r * kCiLd + cc] = ok ? A[(int64_t)(i0 + cc) * ld + (i0 + r)] : 0.0;
+  }
+  __syncthreads();
+  for (int bI = warp; bI < nblk; bI += nw) {
+    const int nbI = min(kCiNB, n - bI * kCiNB);
+    const double* Lb = Xc + (size_t)bI * BB;
+    double* Dv = Dinv + (size_t)bI * BB;
+    const int c = lane;   // column c of the inverse, rows r >= c
+    for (int r = 0; r < kCiNB; ++r) {
+      double v0 = (r == c) ? 1.0 : 0.0, v1 = 0.0;
+      if (c < r && r < nbI) {
+        int k = c;
+        for (; k + 1 < r; k += 2) {
+          v0 = fma(-Lb[r * kCiLd + k], Dv[k * kCiLd + c], v0);
+          v1 = fma(-Lb[r * kCiLd + k + 1], Dv[(k + 1) * kCiLd + c], v1);
+        }
+        if (k < r) v0 = fma(-Lb[r * kCiLd + k], Dv[k * kCiLd + c], v0);
+      }
+      const double x = (r >= c && r < nbI && c < nbI) ? (v0 + v1) / Lb[r * kCiLd + r] : 0.0;
+      __syncwarp();
+      Dv[r * kCiLd + c] = x;
+      __syncwarp();
     }
-    for (int e = tid; e < nbI * nbI; e += nt) {
-      const int r = e % nbI, c = e / nbI;
-      Di[r * kCiLd + c] = X[(int64_t)(i0 + c) * n + (i0 + r)];
+  }
+  __syncthreads();
+  for (int bJ = me; bJ < nblk; bJ += C) {
+    const int j0 = bJ * kCiNB, nbJ = min(kCiNB, n - j0);
+    for (int e = tid; e < BB; e += nt) Xc[(size_t)bJ * BB + e] = Dinv[(size_t)bJ * BB + e];
+    __syncthreads();
+    for (int bI = bJ + 1; bI < nblk; ++bI) {
+      const int i0 = bI * kCiNB, nbI = min(kCiNB, n - i0);
+      // Rb = sum_{K=J..I-1} L_IK X_KJ, L_IK staged block by block
+      double acc4[4] = {0.0, 0.0, 0.0, 0.0};
+      // the next L_IK block is loaded into registers while the current one
+      // is consumed (global latency off the critical path)
+      double nxt[2];
+      auto fetch = [&](int bK) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int e = tid + q * nt;
+          const int r = e % kCiNB, kk = e / kCiNB;
+          nxt[q] = (r < nbI) ? A[(int64_t)(bK * kCiNB + kk) * ld + (i0 + r)] : 0.0;
+        }
+      };
+      fetch(bJ);
+      for (int bK = bJ; bK < bI; ++bK) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int e = tid + q * nt;
+          Lt[(e % kCiNB) * kCiLd + e / kCiNB] = nxt[q];
+        }
+        __syncthreads();
+        if (bK + 1 < bI) fetch(bK + 1);
+        const double* xk = Xc + (size_t)bK * BB;
+        // 256 threads: row r, columns 4 cg .. 4 cg + 3 (the L_IK value is
+        // reused from a register, the X_KJ values are warp broadcasts)
+        if (tid < 256) {
+          const int r = tid % kCiNB, c0 = 4 * (tid / kCiNB);
+#pragma unroll 8
+          for (int kk = 0; kk < kCiNB; ++kk) {
+            const double lv = Lt[r * kCiLd + kk];
+            acc4[0] = fma(lv, xk[kk * kCiLd + c0], acc4[0]);
+            acc4[1] = fma(lv, xk[kk * kCiLd + c0 + 1], acc4[1]);
+            acc4[2] = fma(lv, xk[kk * kCiLd + c0 + 2], acc4[2]);
+            acc4[3] = fma(lv, xk[kk * kCiLd + c0 + 3], acc4[3]);
+          }
+        }
+        __syncthreads();
+      }
+      if (tid < 256) {
+        const int r = tid % kCiNB, c0 = 4 * (tid / kCiNB);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Rb[r * kCiLd + c0 + q] = acc4[q];
+      }
+      __syncthreads();
+      // X_IJ = -L_II^-1 Rb
+      const double* Dv = Dinv + (size_t)bI * BB;
+      double* xo = Xc + (size_t)bI * BB;
+      for (int e = tid; e < kCiNB * kCiNB; e += nt) {
+        const int r = e % kCiNB, cc = e / kCiNB;
+        double v = 0.0;
+        for (int j = 0; j <= r; ++j) v = fma(Dv[r * kCiLd + j], Rb[j * kCiLd + cc], v);
+        xo[r * kCiLd + cc] = -v;
+      }
+      __syncthreads();
+    }
+    // rows k in block J of T: T[k][j] = s_k X[j][k] for j >= k (X row j lives
+    // in block I(j) >= J of this column), 0 below the diagonal; zero the
+    // strict upper triangle of A (L) in these columns
+    for (int e = tid; e < kCiNB * n; e += nt) {
+      const int kk = e % kCiNB, j = e / kCiNB;
+      const int k = j0 + kk;
+      if (kk >= nbJ) continue;
+      double v = 0.0;
+      if (j >= k) {
+        const int bI = j / kCiNB;
+        v = sc[k] * Xc[(size_t)bI * BB + (j - bI * kCiNB) * kCiLd + kk];
+      }
+      T[(int64_t)j * n + k] = v;
+    }
+    for (int e = tid; e < nbJ * j0; e += nt) {
+      const int i = e % j0, cc = e / j0;
+      A[(int64_t)(j0 + cc) * ld + i] = 0.0;
+    }
+    for (int e = tid; e < nbJ * nbJ; e += nt) {
+      const int i = e % nbJ, cc = e / nbJ;
+      if (i < cc) A[(int64_t)(j0 + cc) * ld + (j0 + i)] = 0.0;
     }
     __syncthreads();
-    // a warp per column (lanes = rows r), columns split over the cluster:
-    // Rr[:, col] = sum_{k = col .. i0-1} L[i0 + r, k] X[k, col], then
-    // X[i0 + r, col] = -sum_j Di[r, j] Rr[j, col]
-    for (int col = gw; col < i0; col += gnw) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      const double* xc = X + (int64_t)col * n;
-      if (lane < nbI) {
-        int k = col;
-        for (; k + 3 < i0; k += 4) {
-          a0 = fma(Lr[k * kCiNB + lane], xc[k], a0);
-          a1 = fma(Lr[(k + 1) * kCiNB + lane], xc[k + 1], a1);
-          a2 = fma(Lr[(k + 2) * kCiNB + lane], xc[k + 2], a2);
-          a3 = fma(Lr[(k + 3) * kCiNB + lane], xc[k + 3], a3);
-        }
-        for (; k < i0; ++k) a0 = fma(Lr[k * kCiNB + lane], xc[k], a0);
-      }
-      const double rr = (a0 + a1) + (a2 + a3);
-      double v = 0.0;
-#pragma unroll
-      for (int j = 0; j < kCiNB; ++j) {
-        const double rj = __shfl_sync(0xffffffffu, rr, j);
-        if (j <= lane && j < nbI) v = fma(Di[lane * kCiLd + j], rj, v);
-      }
-      if (lane < nbI) X[(int64_t)col * n + (i0 + lane)] = -v;
-    }
-    cluster.sync();
   }
-
   CI_T(7);
-  // ---- phase 3: T = S X^T (upper triangular), info ------------------------
-  for (int e = gt; e < n * n; e += gnt) {
-    const int k = e % n, j = e / n;  // T[k, j]
-    T[(int64_t)j * n + k] = (k <= j) ? sc[k] * X[(int64_t)k * n + j] : 0.0;
-    if (k < j) A[(int64_t)j * ld + k] = 0.0;
-  }
-  if (leader && tid == 0 && info) {
-    double minr = 1.0;
-    for (int j = 0; j < n; ++j) {
+  if (leader && info) {
+    // info[0] = min pivot / diagonal, info[1] = reference rank, info[2] =
+    // kept count (block reductions); keep[] in column order (thread 0)
+    __shared__ double r_min[32], r_fro[32];
+    __shared__ int r_kept[32];
+    double mn = 1.0, fro2 = 0.0;
+    int kc = 0;
+    for (int j = tid; j < n; j += nt) {
       const double rt = (d0[j] > 0.0 && Rat[j] == Rat[j]) ? Rat[j] / d0[j] : -1.0;
-      minr = fmin(minr, rt);
+      mn = fmin(mn, rt);
+      if (sc[j] > 0.0) fro2 += 1.0 / (sc[j] * sc[j]);
+      kc += dropped[j] ? 0 : 1;
     }
-    info[0] = minr;
-    int kept = 0;
-    for (int j = 0; j < n; ++j)
-      if (!dropped[j]) {
-        if (keep) keep[kept] = j;
-        ++kept;
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      fro2 += __shfl_xor_sync(0xffffffffu, fro2, o);
+      kc += __shfl_xor_sync(0xffffffffu, kc, o);
+    }
+    if (lane == 0) {
+      r_min[warp] = mn;
+      r_fro[warp] = fro2;
+      r_kept[warp] = kc;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      mn = lane < nw ? r_min[lane] : 1.0;
+      fro2 = lane < nw ? r_fro[lane] : 0.0;
+      kc = lane < nw ? r_kept[lane] : 0;
+      for (int o = 16; o > 0; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        fro2 += __shfl_xor_sync(0xffffffffu, fro2, o);
+        kc += __shfl_xor_sync(0xffffffffu, kc, o);
       }
-    info[2] = (double)kept;
-    CI_T(8);
-    if (rank_tol > 0.0) {
-      double fro2 = 0.0;
-      for (int j = 0; j < n; ++j)
-        if (sc[j] > 0.0) fro2 += 1.0 / (sc[j] * sc[j]);
-      const double cut = rank_tol * sqrt(fro2);
-      int rk = 0;
-      for (int j = 0; j < n; ++j)
-        if (!dropped[j] && sc[j] > 0.0 && dL[j] / sc[j] > cut) ++rk;
-      info[1] = (double)rk;
+      if (lane == 0) {
+        r_min[0] = mn;
+        r_fro[0] = fro2;
+        r_kept[0] = kc;
+      }
+    }
+    __syncthreads();
+    const double cut = rank_tol * sqrt(r_fro[0]);
+    int rk = 0;
+    for (int j = tid; j < n; j += nt)
+      rk += (!dropped[j] && sc[j] > 0.0 && dL[j] / sc[j] > cut) ? 1 : 0;
+    rk = __reduce_add_sync(0xffffffffu, rk);
+    __syncthreads();
+    if (lane == 0) r_kept[warp] = rk;
+    __syncthreads();
+    if (tid == 0) {
+      int tot = 0;
+      for (int w = 0; w < nw; ++w) tot += r_kept[w];
+      info[0] = r_min[0];
+      info[2] = (double)kc;
+      info[1] = rank_tol > 0.0 ? (double)tot : 0.0;
+      if (keep) {
+        int kept = 0;
+        for (int j = 0; j < n; ++j)
+          if (!dropped[j]) keep[kept++] = j;
+      }
+      CI_T(8);
     }
   }
 }

@@ -29,7 +29,7 @@ void apply_basis(Ctx& c, const T* X, int64_t r, int li, int64_t ldx, const doubl
   gemm_nn_cm<T, double, T>(c, r, lo, li, X, ldx, Tm, ldt, Out, ldo);
 }
 
-constexpr int kCholMaxL = 384;  // chol_kernel shared-memory limit (~197 KB)
+constexpr int kCholMaxL = 320;  // cholinv_kernel shared-memory limit (~196 KB at 320)
 
 // Cholesky basis change of X (r x l): with s_j = 1/||x_j|| and the scaled Gram
 // G~ = S X^T X S, factor G~ + shift I = L L^T and return T = S L^-T in Tm
