@@ -345,50 +345,38 @@ __global__ void __launch_bounds__(kCiThreads, 1)
     }
     __syncthreads();
     if (pi == 0) CI_T(2);
-    if (warp == 0) {
-      // factor the diagonal block in shared memory, lane r owning row r; the
-      // pivot test avoids divisions (piv/dg is only recorded for info[0]) and
-      // the factor uses rsqrt.  Loops stay rolled (instruction cache).
-      // Left-looking (Crout) column by column: lane r forms
-      // d_r = A[r][c] - L[r][:c] . L[c][:c] with independent loads (no
-      // stores in the dot), lane c's value is the pivot.
-      const int r = lane;
-      double* Lrow = Lp + r * kCiLd;
-      for (int c = 0; c < nb; ++c) {
-        const double* Lc = Lp + c * kCiLd;
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        if (r >= c && r < nb) {
-          int k = 0;
-#pragma unroll 2
-          for (; k + 3 < c; k += 4) {
-            s0 = fma(Lrow[k], Lc[k], s0);
-            s1 = fma(Lrow[k + 1], Lc[k + 1], s1);
-            s2 = fma(Lrow[k + 2], Lc[k + 2], s2);
-            s3 = fma(Lrow[k + 3], Lc[k + 3], s3);
-          }
-          for (; k < c; ++k) s0 = fma(Lrow[k], Lc[k], s0);
-        }
-        const double dr = (r >= c && r < nb) ? Lrow[c] - ((s0 + s1) + (s2 + s3)) : 0.0;
-        const double piv = __shfl_sync(0xffffffffu, dr, c);
-        const double dg = d0[p0 + c];
-        const bool drop = !(piv > 0.0) ||
-                          (drop_ratio > 0.0 && (!(dg > 0.0) || !(piv > drop_ratio * dg)));
-        const double inv = drop ? 0.0 : rsqrt(piv);
-        if (r == c) {
-          const double dsq = piv * inv;
-          Lrow[c] = drop ? 1.0 : dsq;
-          Di[kCiNB * kCiLd - kCiNB + c] = drop ? 1.0 : inv;  // scratch: 1 / L[c][c]
-          dropped[p0 + c] = drop ? 1 : 0;
-          dL[p0 + c] = drop ? 0.0 : dsq;
-          Rat[p0 + c] = piv;
-        } else if (r > c && r < nb) {
-          Lrow[c] = dr * inv;
-        }
-        __syncwarp();
+    // factor the diagonal block right-looking with all threads: per column a
+    // pivot (rsqrt, no divisions -- piv/dg is only recorded for info[0]), a
+    // column scale and a rank-1 update of the trailing block, three barriers
+    double* rinv = Di + kCiNB * kCiLd - kCiNB;   // 1 / L11[c][c] for the TRSM
+    for (int c = 0; c < nb; ++c) {
+      const double piv = Lp[c * kCiLd + c];
+      const double dg = d0[p0 + c];
+      const bool drop = !(piv > 0.0) ||
+                        (drop_ratio > 0.0 && (!(dg > 0.0) || !(piv > drop_ratio * dg)));
+      const double inv = drop ? 0.0 : rsqrt(piv);
+      __syncthreads();
+      if (tid == 0) {
+        const double dsq = piv * inv;
+        Lp[c * kCiLd + c] = drop ? 1.0 : dsq;
+        rinv[c] = drop ? 1.0 : inv;
+        dropped[p0 + c] = drop ? 1 : 0;
+        dL[p0 + c] = drop ? 0.0 : dsq;
+        Rat[p0 + c] = piv;
       }
-      // zero the strict upper triangle of the block
-      for (int j = r + 1; j < nb; ++j) Lrow[j] = 0.0;
-      __syncwarp();
+      const int rest = nb - c - 1;
+      if (tid < rest) Lp[(c + 1 + tid) * kCiLd + c] *= inv;
+      __syncthreads();
+      for (int e = tid; e < rest * rest; e += nt) {
+        const int i = c + 1 + e % rest, j = c + 1 + e / rest;
+        if (i >= j) Lp[i * kCiLd + j] = fma(-Lp[i * kCiLd + c], Lp[j * kCiLd + c], Lp[i * kCiLd + j]);
+      }
+    }
+    __syncthreads();
+    // zero the strict upper triangle of the block
+    for (int e = tid; e < nb * nb; e += nt) {
+      const int i = e % nb, j = e / nb;
+      if (i < j) Lp[i * kCiLd + j] = 0.0;
     }
     __syncthreads();
     if (pi == 0) CI_T(3);
@@ -398,7 +386,6 @@ __global__ void __launch_bounds__(kCiThreads, 1)
     // rows).  Dropped columns are zero (their L11 column is e_c).
     const int rpad = (rows + 3) & ~3;
     {
-      const double* rinv = Di + kCiNB * kCiLd - kCiNB;   // 1 / L11[c][c] (factor scratch)
       for (int i = nb + tid; i < rpad; i += nt) {
         double x[kCiNB];
 #pragma unroll
