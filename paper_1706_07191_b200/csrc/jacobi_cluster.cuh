@@ -144,6 +144,94 @@ __device__ __forceinline__ bool jc_rotate(R* __restrict__ x, R* __restrict__ y,
   return true;
 }
 
+// Cross-round rotation with the block-a column x held in registers for the
+// whole round (xr: G part, xv: V part) and the partner y in shared memory:
+// the x loads and stores of jc_rotate disappear from every step.  Returns
+// true if rotated.
+template <typename R, int NP2>
+__device__ __forceinline__ bool jc_rotate_x(typename Vec2<R>::type (&xr)[NP2],
+                                            typename Vec2<R>::type (&xv)[NP2],
+                                            R* __restrict__ y, R* __restrict__ vy, int lp,
+                                            R tol2, R floor2, int lane) {
+  using V2 = typename Vec2<R>::type;
+  V2 yr[NP2];
+  R g = 0, aa = 0, b = 0;
+#pragma unroll
+  for (int k = 0; k < NP2; ++k) {
+    const int i = 2 * lane + 64 * k;
+    if (i < lp) {
+      yr[k] = *reinterpret_cast<const V2*>(y + i);
+    } else {
+      yr[k].x = yr[k].y = R(0);
+    }
+    g = fma(xr[k].x, yr[k].x, g);
+    aa = fma(xr[k].x, xr[k].x, aa);
+    b = fma(yr[k].x, yr[k].x, b);
+    g = fma(xr[k].y, yr[k].y, g);
+    aa = fma(xr[k].y, xr[k].y, aa);
+    b = fma(yr[k].y, yr[k].y, b);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    g += __shfl_xor_sync(0xffffffffu, g, o);
+    aa += __shfl_xor_sync(0xffffffffu, aa, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  const R a = aa;   // exact norms: cached ones drift and cost a sweep
+  if (!(a > floor2 && b > floor2)) return false;
+  if (!(g * g > tol2 * a * b)) return false;
+  R t;
+  if (sizeof(R) == 4) {
+    const float zeta = __fdividef((float)(b - a), 2.0f * (float)g);
+    const float az = fabsf(zeta);
+    if (az > 1e18f) {
+      t = (R)__fdividef(0.5f, zeta);
+    } else {
+      const float w = fmaf(zeta, zeta, 1.0f);
+      t = (R)copysignf(__fdividef(1.0f, az + w * rsqrtf(w)), zeta);
+    }
+  } else {
+    const R zeta = (b - a) / (R(2) * g);
+    if (fabs(zeta) > R(1e150)) {
+      t = R(0.5) / zeta;
+    } else {
+      t = copysign(R(1), zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, R(1))));
+    }
+  }
+  if (t == R(0)) return false;
+  const R c = jc_rsqrt<R>(fma(t, t, R(1)));
+  const R s = c * t;
+#pragma unroll
+  for (int k = 0; k < NP2; ++k) {
+    const int i = 2 * lane + 64 * k;
+    const V2 x0 = xr[k];
+    xr[k].x = c * x0.x - s * yr[k].x;
+    xr[k].y = c * x0.y - s * yr[k].y;
+    V2 ny;
+    ny.x = s * x0.x + c * yr[k].x;
+    ny.y = s * x0.y + c * yr[k].y;
+    if (i < lp) *reinterpret_cast<V2*>(y + i) = ny;
+  }
+#pragma unroll
+  for (int k = 0; k < NP2; ++k) {
+    const int i = 2 * lane + 64 * k;
+    V2 yv;
+    if (i < lp) {
+      yv = *reinterpret_cast<const V2*>(vy + i);
+    } else {
+      yv.x = yv.y = R(0);
+    }
+    const V2 x0 = xv[k];
+    xv[k].x = c * x0.x - s * yv.x;
+    xv[k].y = c * x0.y - s * yv.y;
+    V2 ny;
+    ny.x = s * x0.x + c * yv.x;
+    ny.y = s * x0.y + c * yv.y;
+    if (i < lp) *reinterpret_cast<V2*>(vy + i) = ny;
+  }
+  return true;
+}
+
 // Shared memory: buf[2][2 slots][bw columns][2 * lp] of R, where a column is
 // its G part (lp entries, lp = l rounded up to 4) followed by its V part.
 template <typename R>
@@ -239,15 +327,45 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
         __syncthreads();
       }
     } else {
+      // cross pairs: warp p keeps column p of block a in registers for the
+      // whole round; the block-b columns pass from warp to warp through shared
+      // memory (nwarps >= bw)
+      using V2 = typename Vec2<R>::type;
+      const int p = warp;
+      const bool own = p < bw && p < va;
+      V2 xr[NP2], xv[NP2];
+      R* xcol = cur + (size_t)p * colsz;
+      if (own) {
+#pragma unroll
+        for (int k = 0; k < NP2; ++k) {
+          const int i = 2 * lane + 64 * k;
+          if (i < lp) {
+            xr[k] = *reinterpret_cast<const V2*>(xcol + i);
+            xv[k] = *reinterpret_cast<const V2*>(xcol + lp + i);
+          } else {
+            xr[k].x = xr[k].y = xv[k].x = xv[k].y = R(0);
+          }
+        }
+      }
       for (int st = 0; st < bw; ++st) {
-        for (int p = warp; p < bw; p += nwarps) {
+        if (own) {
           const int jb = p + st < bw ? p + st : p + st - bw;
-          if (p >= va || jb >= vb) continue;
-          R* x = cur + (size_t)p * colsz;
-          R* y = cur + slotsz + (size_t)jb * colsz;
-          if (jc_rotate<R, NP2>(x, y, x + lp, y + lp, lp, tol2, floor2, lane)) ++my_rot;
+          if (jb < vb) {
+            R* y = cur + slotsz + (size_t)jb * colsz;
+            if (jc_rotate_x<R, NP2>(xr, xv, y, y + lp, lp, tol2, floor2, lane)) ++my_rot;
+          }
         }
         __syncthreads();
+      }
+      if (own) {
+#pragma unroll
+        for (int k = 0; k < NP2; ++k) {
+          const int i = 2 * lane + 64 * k;
+          if (i < lp) {
+            *reinterpret_cast<V2*>(xcol + i) = xr[k];
+            *reinterpret_cast<V2*>(xcol + lp + i) = xv[k];
+          }
+        }
       }
     }
     const bool sweep_end = (tr == nb - 2);
