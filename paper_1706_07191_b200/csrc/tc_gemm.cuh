@@ -548,6 +548,41 @@ __global__ void tc_colmax_kernel(const float* __restrict__ X, int64_t K, int n_s
   if ((threadIdx.x & 31) == 0) atomicMax(&cmax[j], m);
 }
 
+// One CTA per (padded) column: max |X[:, j]| by a block reduction, then the
+// scaled fp16 (hi, lo) split of that column -- one pass, no atomics.
+__global__ void __launch_bounds__(256)
+    tc_split16_col_kernel(const float* __restrict__ X, int64_t K, int n_src, int64_t ldx,
+                          int64_t kld, uint16_t* __restrict__ hi, uint16_t* __restrict__ lo,
+                          float* __restrict__ col_inv) {
+  __shared__ unsigned red[8];
+  const int j = blockIdx.x;
+  const float* col = X + (int64_t)j * ldx;
+  const bool real = j < n_src;
+  unsigned m = 0;
+  if (real)
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x)
+      m = max(m, __float_as_uint(fabsf(col[k])));
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int w = 0; w < 8; ++w) t = max(t, red[w]);
+    red[0] = t;
+  }
+  __syncthreads();
+  const float sc = real ? h16_scale(__uint_as_float(red[0])) : 1.f;
+  if (threadIdx.x == 0) col_inv[j] = 1.f / sc;
+  uint16_t* h = hi + (int64_t)j * kld;
+  uint16_t* l = lo + (int64_t)j * kld;
+  for (int64_t k = threadIdx.x; k < kld; k += blockDim.x) {
+    const float x = (real && k < K) ? col[k] * sc : 0.f;
+    const __half hh = __float2half_rn(x);
+    h[k] = __half_as_ushort(hh);
+    l[k] = __half_as_ushort(__float2half_rn(x - __half2float(hh)));
+  }
+}
+
 __global__ void tc_split16_kernel(const float* __restrict__ X, int64_t K, int n_src,
                                   int64_t ldx, int npad, int64_t kld,
                                   const unsigned* __restrict__ cmax,
@@ -749,7 +784,6 @@ inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, 
   p.row_max = nullptr;
   p.col_inv = nullptr;
   DBuf<float> hi, lo, opmax, cinv;
-  DBuf<unsigned> bmax;
   CUtensorMap mapBhi, mapBlo;
   if (h16) {
     const int64_t kld = ceil_div(K, 8) * 8;
@@ -761,16 +795,11 @@ inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, 
         absmax_rows_cols(c, A, m, n, lda, row_major, opmax.p, nullptr);
       opa_max = opmax.p;
     }
-    bmax.alloc(c, (size_t)g.npad);
     cinv.alloc(c, (size_t)g.npad);
     hi.alloc(c, (size_t)g.npad * kld / 2 + 8);
     lo.alloc(c, (size_t)g.npad * kld / 2 + 8);
-    BRSVD_CUDA(cudaMemsetAsync(bmax.p, 0, sizeof(unsigned) * g.npad, c.stream));
-    tc_colmax_kernel<<<dim3((unsigned)std::min<int64_t>(ceil_div(K, 256), 64), (unsigned)l), 256,
-                       0, c.stream>>>(X, K, l, ldx, bmax.p);
-    BRSVD_CHECK_LAUNCH();
-    tc_split16_kernel<<<grid_for((int64_t)g.npad * kld), 256, 0, c.stream>>>(
-        X, K, l, ldx, g.npad, kld, bmax.p, reinterpret_cast<uint16_t*>(hi.p),
+    tc_split16_col_kernel<<<(unsigned)g.npad, 256, 0, c.stream>>>(
+        X, K, l, ldx, kld, reinterpret_cast<uint16_t*>(hi.p),
         reinterpret_cast<uint16_t*>(lo.p), cinv.p);
     BRSVD_CHECK_LAUNCH();
     mapBhi = make_map(hi.p, (uint64_t)kld, (uint64_t)g.npad, (uint64_t)kld * 2, BK_H16,
