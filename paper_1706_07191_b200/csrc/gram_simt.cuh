@@ -17,7 +17,7 @@
 namespace brsvd {
 namespace gram {
 
-constexpr int BK = 16;  // k slab
+constexpr int BK = 32;  // k slab
 template <int BT> struct Cfg {
   static constexpr int LDS = BT + 4;                       // padded k-major row (doubles)
   static constexpr int TY = BT / 8, TX = BT / 4;           // 8 x 4 outputs per thread
