@@ -35,15 +35,16 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int BK = 16;              // fp32 K elements per stage (64-byte rows)
 constexpr int STAGES_TF32 = 6;   // smem ring depth (TMEM A slots: 6 x 32 columns)
-constexpr int STAGES_H16 = 6;    // fp16 split: 6 x 32 TMEM columns (32 k per stage)
+constexpr int STAGES_H16 = 3;    // fp16 split: 3 x 64 TMEM columns (64 k per stage)
 constexpr int NPAD_MAX = 320;   // l <= 320: two CTAs of <= 160 columns
 constexpr int kThreads = 640;   // 4 role warps + 16 converter warps
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kASlot = 320;    // TMEM columns [320, 512): six A staging slots
 constexpr uint32_t A_STAGE_BYTES = BM * BK * 4;
-// fp16 split: 32 k values per stage (128-byte fp32 A rows, 64-byte fp16 B
-// rows) -- half the stages, barrier round trips and TMA issues per byte of A
-constexpr int BK_H16 = 32;
+// fp16 split: 64 k values per stage (two 128-byte-swizzled fp32 A boxes,
+// 128-byte fp16 B rows) -- a quarter of the stages, barrier round trips and
+// TMA issues per byte of A of the 16-k tf32 ring
+constexpr int BK_H16 = 64;
 constexpr uint32_t A_STAGE_BYTES_H16 = BM * BK_H16 * 4;
 
 struct Params {
@@ -119,6 +120,16 @@ __device__ __forceinline__ uint64_t desc_kmajor_sw32(uint32_t saddr) {
   d |= (uint64_t)(256 >> 4) << 32;   // SBO
   d |= (uint64_t)1 << 46;            // descriptor version (sm100)
   d |= (uint64_t)6 << 61;            // SWIZZLE_32B
+  return d;
+}
+// K-major operand, 128-byte swizzle (64 fp16 per row): 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t desc_kmajor_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;            // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO
+  d |= (uint64_t)1 << 46;            // descriptor version (sm100)
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
   return d;
 }
 __device__ __forceinline__ void mma_f16_ts(uint32_t d, uint32_t a, uint64_t bdesc,
@@ -277,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&freeb[s], 1);
-      mbar_init(&tfull[s], 8);
+      mbar_init(&tfull[s], H16 ? 16 : 8);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accready[b], 1);
@@ -310,7 +321,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int k0 = (kb_begin + kb) * BKK;
         mbar_expect_tx(&full[s], stage_bytes);
         if (A_KMAJOR) {
-          tma_load_2d(st, &mapA, &full[s], k0, (int)m0);
+          if constexpr (H16) {  // two 32-k boxes of 128-byte rows
+            tma_load_2d(st, &mapA, &full[s], k0, (int)m0);
+            tma_load_2d(st + BM * 128, &mapA, &full[s], k0 + 32, (int)m0);
+          } else {
+            tma_load_2d(st, &mapA, &full[s], k0, (int)m0);
+          }
         } else {
 #pragma unroll
           for (int b = 0; b < 4; ++b)
@@ -340,13 +356,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t bl = bh + b_bytes;
         const uint32_t d = tmem + (uint32_t)(buf * nc);
         if constexpr (H16) {
-          // two K=16 steps; A hi / lo in 16 TMEM columns each (fp16 pairs),
-          // B rows of 64 bytes (32 fp16), 64-byte swizzle
-          const uint32_t a_hi = tmem + kASlot + s * 32, a_lo = a_hi + 16;
+          // four K=16 steps; A hi / lo in 32 TMEM columns each (fp16 pairs),
+          // B rows of 128 bytes (64 fp16), 128-byte swizzle
+          const uint32_t a_hi = tmem + kASlot + s * 64, a_lo = a_hi + 32;
 #pragma unroll
-          for (int kk = 0; kk < 2; ++kk) {
-            const uint64_t dh = desc_kmajor_sw64(bh + kk * 32);
-            const uint64_t dl = desc_kmajor_sw64(bl + kk * 32);
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t dh = desc_kmajor_sw128(bh + kk * 32);
+            const uint64_t dl = desc_kmajor_sw128(bl + kk * 32);
             const uint32_t acc = (chunk_start && kk == 0) ? 0u : 1u;
             mma_f16_ts(d, a_lo + kk * 8, dh, idesc, acc);
             mma_f16_ts(d, a_hi + kk * 8, dl, idesc, 1u);
@@ -373,14 +389,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     // each stage, stage parity par (even / odd k-blocks, so each warp's
     // split -> tcgen05.st -> wait chain has two stages of MMA time), and a
     // quarter of the accumulator columns for the flushes and the epilogue.
+    // (H16: lane quadrant x k quarter of each 64-k stage, every stage.)
     const int idx = warp - 4;
     const int wq = idx & 3;
     const int half = (idx >> 2) & 1;
-    const int par = idx >> 3;
+    const int par = H16 ? 0 : idx >> 3;
+    const int qtr = idx >> 2;               // H16: k values 16 qtr .. + 15
+    const int kstep = H16 ? 1 : 2;
     const int r = wq * 32 + lane;
     const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
     const int hc = nc >> 2;                 // accumulator columns per warp
-    const int c0 = (2 * par + half) * hc;
+    const int c0 = (H16 ? qtr : 2 * par + half) * hc;
     float run[NH];
 #pragma unroll
     for (int j = 0; j < NH; ++j) run[j] = 0.f;
@@ -409,20 +428,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       rscale = (p.row_max != nullptr && grow < p.M) ? h16_scale(p.row_max[grow]) : 1.f;
     }
     int flushed = 0;
-    for (int kb = par; kb < nk; kb += 2) {
+    for (int kb = par; kb < nk; kb += kstep) {
       const int s = kb % STAGES;
       const uint32_t ph = (kb / STAGES) & 1;
       mbar_wait(&full[s], ph);
       const uint32_t sa = smem_base + (uint32_t)s * stage_bytes;
       if constexpr (H16) {
-        // 16 k values of row r: k = 16 half .. + 15
+        // 16 k values of row r: k = 16 qtr .. + 15
         float v[16];
         if (A_KMAJOR) {
-          // 128-byte rows; TMA 128B swizzle puts 16B chunk j of row r at j^(r&7)
-          const uint32_t row = sa + r * 128;
+          // two boxes of 128-byte rows (k 0-31, 32-63); TMA 128B swizzle puts
+          // 16B chunk j of row r at j^(r&7)
+          const uint32_t row = sa + (qtr >> 1) * (BM * 128) + r * 128;
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) {
-            const int j = 4 * half + jj;
+            const int j = 4 * (qtr & 1) + jj;
             const float4 x = lds128(row + ((j ^ (r & 7)) << 4));
             v[4 * jj + 0] = x.x;
             v[4 * jj + 1] = x.y;
@@ -430,10 +450,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             v[4 * jj + 3] = x.w;
           }
         } else {
-          // four (32 rows x 32 k) boxes, 32 consecutive rows per k
+          // four (32 rows x 64 k) boxes, 32 consecutive rows per k
           const uint32_t box = sa + wq * (32 * BKK * 4) + lane * 4;
 #pragma unroll
-          for (int k = 0; k < 16; ++k) v[k] = lds32(box + (16 * half + k) * 128);
+          for (int k = 0; k < 16; ++k) v[k] = lds32(box + (16 * qtr + k) * 128);
         }
         uint32_t hi[8], lo[8];
 #pragma unroll
@@ -443,8 +463,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float2 hf = unpack_h2(hi[i]);
           lo[i] = pack_h2(x0 - hf.x, x1 - hf.y);
         }
-        tmem_st8(tmem + lane_base + kASlot + s * 32 + 8 * half, hi);
-        tmem_st8(tmem + lane_base + kASlot + s * 32 + 16 + 8 * half, lo);
+        tmem_st8(tmem + lane_base + kASlot + s * 64 + 8 * qtr, hi);
+        tmem_st8(tmem + lane_base + kASlot + s * 64 + 32 + 8 * qtr, lo);
       } else {
         float v[8];
         if (A_KMAJOR) {
@@ -768,7 +788,7 @@ inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, 
   const bool h16m = h16_enabled();
   const uint32_t bka = h16m ? BK_H16 : BK;
   const CUtensorMap mapA =
-      kmajor ? make_map(A, inner, outer, (uint64_t)lda * 4, bka, BM,
+      kmajor ? make_map(A, inner, outer, (uint64_t)lda * 4, h16m ? 32u : bka, BM,
                         h16m ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)
              : make_map(A, inner, outer, (uint64_t)lda * 4, 32, bka, CU_TENSOR_MAP_SWIZZLE_NONE);
   Params p;
@@ -803,10 +823,10 @@ inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, 
         reinterpret_cast<uint16_t*>(lo.p), cinv.p);
     BRSVD_CHECK_LAUNCH();
     mapBhi = make_map(hi.p, (uint64_t)kld, (uint64_t)g.npad, (uint64_t)kld * 2, BK_H16,
-                      (uint32_t)g.rows_c, CU_TENSOR_MAP_SWIZZLE_64B,
+                      (uint32_t)g.rows_c, CU_TENSOR_MAP_SWIZZLE_128B,
                       CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
     mapBlo = make_map(lo.p, (uint64_t)kld, (uint64_t)g.npad, (uint64_t)kld * 2, BK_H16,
-                      (uint32_t)g.rows_c, CU_TENSOR_MAP_SWIZZLE_64B,
+                      (uint32_t)g.rows_c, CU_TENSOR_MAP_SWIZZLE_128B,
                       CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
     p.row_max = opa_max;
     p.col_inv = cinv.p;
