@@ -648,7 +648,6 @@ int brsvd_chol_basis(brsvd_ctx* ctx, double* G, int64_t l, double shift, double 
     Ctx& c = ctx->c;
     BRSVD_CUDA(cudaSetDevice(c.device));
     BRSVD_REQUIRE(l >= 1 && l <= kCholMaxL, kErrShape, "chol_basis supports 1 <= l <= 320");
-    set_chol_attrs(c);
     const int li = (int)l;
     DBuf<double> Wd(c, (size_t)l * l), info(c, 3), Tm(c, (size_t)l * l);
     DBuf<int> keep(c, l);

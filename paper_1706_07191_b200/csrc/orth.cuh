@@ -77,15 +77,6 @@ CholInfo chol_basis(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double sh
   return ci;
 }
 
-inline void set_chol_attrs(Ctx& c) {
-  static bool done = false;
-  if (done) return;
-  const int lim = (int)c.max_smem_optin - 2048;  // leave room for static smem
-  BRSVD_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
-  BRSVD_CUDA(cudaFuncSetAttribute(trinv_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  lim));
-  done = true;
-}
 
 // Basis change for the power iteration: Xout spans range(X) with restored
 // conditioning.  Shifted Cholesky QR (shift ~ l*eps of the unit diagonal,
@@ -97,7 +88,6 @@ void normalize_sketch(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, T* Xout
                       int64_t ldo) {
   DBuf<double> Tm(c, (size_t)l * l);
   if (l <= kCholMaxL) {
-    set_chol_attrs(c);
     chol_basis<T>(c, X, r, l, ldx, 16.0 * l * 2.220446049250313e-16, Tm.p, false);
   } else {
     DBuf<double> E(c, (size_t)l * l), lam(c, l), s(c, l);
@@ -224,7 +214,6 @@ int orth_full_f64(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* Q,
   int total = 0, rank = 0;
   double normx2 = 0.0;
   if (l <= kCholMaxL) {
-    set_chol_attrs(c);
     DBuf<int> keep(c, l);
     DBuf<double> info(c, 3), Tm(c, (size_t)l * l), Tc(c, (size_t)l * l);
     const CholInfo ci = chol_basis<T>(c, X, r, l, ldx, 0.0, Tm.p, true, drop, l * eps_data,
@@ -296,7 +285,6 @@ inline int orth_full_f32(Ctx& c, const float* X, int64_t r, int l, int64_t ldx, 
                          uint64_t seed) {
   const double eps_data = 1.1920928955078125e-07;
   const double drop = 4.0 * l * eps_data;  // the reference's rank cut, kernels.py:155-157
-  set_chol_attrs(c);
   DBuf<int> keep(c, l);
   DBuf<double> info(c, 3), Tm(c, (size_t)l * l), Tc(c, (size_t)l * l);
   const CholInfo ci = chol_basis<float>(c, X, r, l, ldx, 0.0, Tm.p, true, drop, l * eps_data,

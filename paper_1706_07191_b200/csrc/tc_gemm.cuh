@@ -554,20 +554,6 @@ __global__ void tc_split_kernel(const float* __restrict__ X, int64_t K, int n_sr
   }
 }
 
-// fp16 split of the sketch: per column j a power-of-two scale s_j from
-// max |X[:, j]| (colmax, 32-bit patterns of |x|), hi = f16(s_j x),
-// lo = f16(s_j x - hi); col_inv[j] = 1 / s_j (1 for padding columns).
-__global__ void tc_colmax_kernel(const float* __restrict__ X, int64_t K, int n_src,
-                                 int64_t ldx, unsigned* __restrict__ cmax) {
-  const int j = blockIdx.y;
-  unsigned m = 0;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K;
-       k += (int64_t)gridDim.x * blockDim.x)
-    m = max(m, __float_as_uint(fabsf(X[k + j * ldx])));
-  m = __reduce_max_sync(0xffffffffu, m);
-  if ((threadIdx.x & 31) == 0) atomicMax(&cmax[j], m);
-}
-
 // One CTA per (padded) column: max |X[:, j]| by a block reduction, then the
 // scaled fp16 (hi, lo) split of that column -- one pass, no atomics.
 __global__ void __launch_bounds__(256)
@@ -600,24 +586,6 @@ __global__ void __launch_bounds__(256)
     const __half hh = __float2half_rn(x);
     h[k] = __half_as_ushort(hh);
     l[k] = __half_as_ushort(__float2half_rn(x - __half2float(hh)));
-  }
-}
-
-__global__ void tc_split16_kernel(const float* __restrict__ X, int64_t K, int n_src,
-                                  int64_t ldx, int npad, int64_t kld,
-                                  const unsigned* __restrict__ cmax,
-                                  uint16_t* __restrict__ hi, uint16_t* __restrict__ lo,
-                                  float* __restrict__ col_inv) {
-  const int64_t total = (int64_t)npad * kld;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = idx % kld, j = idx / kld;
-    const float sc = j < n_src ? h16_scale(__uint_as_float(cmax[j])) : 1.f;
-    const float x = (j < n_src && k < K) ? X[k + j * ldx] * sc : 0.f;
-    const __half h = __float2half_rn(x);
-    hi[idx] = __half_as_ushort(h);
-    lo[idx] = __half_as_ushort(__float2half_rn(x - __half2float(h)));
-    if (k == 0) col_inv[j] = 1.f / sc;
   }
 }
 
