@@ -150,7 +150,9 @@ __host__ __device__ __forceinline__ float h16_scale(float mx) {
   if (!(mx > 0.f) || !(mx < 3.0e38f)) return 1.f;
   int e;
   frexpf(mx, &e);  // mx = f * 2^e, f in [0.5, 1)
-  return ldexpf(1.f, 14 - e);
+  // capped so the scale and its inverse stay normal floats (rows whose max is
+  // below 2^-112 keep fewer than 22 bits, as their inputs already do)
+  return ldexpf(1.f, min(14 - e, 126));
 }
 __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
   // a -> low half (lower k), b -> high half
@@ -509,7 +511,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int j = 0; j < NH; ++j) {
         const int col = n0 + c0 + j;
-        if (j < hc && col < p.n_out) run[j] *= rinv * p.col_inv[col];
+        // power-of-two unscale in fp64: exact, one rounding, no spurious
+        // over/underflow of the combined factor
+        if (j < hc && col < p.n_out)
+          run[j] = (float)((double)run[j] * ((double)rinv * (double)p.col_inv[col]));
       }
     }
     if (row < p.M) {

@@ -43,3 +43,39 @@ def test_fp64_product(trans):
     C = sketch_product(A, X, trans=trans)
     ref = (A.t() if trans else A) @ X
     assert torch.allclose(C, ref, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("trans", [False, True])
+@pytest.mark.parametrize("h16", ["1"])
+def test_fp32_product_dynamic_range(trans, h16, monkeypatch):
+    """Rows and sketch columns spanning 1e-38..1e25 (plus zero and subnormal
+    rows): the fp16-split path scales each row/column by a power of two, so
+    every output entry stays accurate relative to its own |A||X| bound.  (The
+    unscaled 3xTF32 path behind BRSVD_TC_H16=0 is a diagnostic switch only: its
+    low-part terms underflow for tiny-magnitude rows, so it is not held to
+    this.)"""
+    import torch
+    from paper_1706_07191_b200.rsvd import sketch_product
+    monkeypatch.setenv("BRSVD_TC_H16", h16)
+    m, n, l = 1024, 640, 24
+    g = torch.Generator(device="cuda").manual_seed(11)
+    A = torch.randn(m, n, generator=g, device="cuda", dtype=torch.float64)
+    exps = torch.linspace(-38, 25, m, device="cuda", dtype=torch.float64)
+    A = A * torch.pow(10.0, exps)[:, None]
+    A[5] = 0
+    A[7] = A[7].sign() * 1e-41          # subnormal fp32 row
+    if trans:
+        A = A.t().contiguous()
+    A = A.float()
+    X = torch.randn(A.shape[0] if trans else A.shape[1], l, generator=g,
+                    device="cuda", dtype=torch.float64)
+    X = (X * torch.pow(10.0, torch.linspace(-20, 6, l, device="cuda",
+                                            dtype=torch.float64))[None, :]).float()
+    C = sketch_product(A, X, trans=trans)
+    A64, X64 = A.double(), X.double()
+    ref = (A64.t() if trans else A64) @ X64
+    bound = (A64.abs().t() if trans else A64.abs()) @ X64.abs()
+    ok = bound > 1e-36                   # fp32-representable outputs
+    assert torch.isfinite(C).all()
+    err = ((C.double() - ref).abs() / bound.clamp_min(1e-300))[ok].max().item()
+    assert err <= 2e-6, err
