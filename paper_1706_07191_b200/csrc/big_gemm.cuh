@@ -12,6 +12,10 @@ namespace brsvd {
 
 // amax (optional): max |A| per row (big_nn) / per column (big_tn), float,
 // for the fp16-split products (absmax_rows_cols once per decomposition).
+// out_scale (big_tn, power of two): the fp16-split product returns
+// out_scale * A^T Y, rounded once -- the power iteration uses it to keep
+// A^T Y in fp32 range for inputs of extreme magnitude (other paths ignore it;
+// the sample is renormalised right after, so the factor never shows).
 template <typename T>
 void big_nn(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool row_major,
             const T* X, int64_t ldx, int l, T* Y, int64_t ldy, const float* amax = nullptr) {
@@ -27,11 +31,12 @@ void big_nn(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool row_majo
 
 template <typename T>
 void big_tn(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool row_major,
-            const T* Yin, int64_t ldy, int l, T* Z, int64_t ldz, const float* amax = nullptr) {
+            const T* Yin, int64_t ldy, int l, T* Z, int64_t ldz, const float* amax = nullptr,
+            double out_scale = 1.0) {
   ProfScope ps(c, 2.0 * m * n * l, (double)m * n * sizeof(T));
   if (tc_gemm_supported<T>(c, A, lda, m, n, l)) {
     tc_gemm_launch<T>(c, A, m, n, lda, row_major, /*trans=*/true, Yin, ldy, l, Z, ldz, 0,
-                      nullptr, amax);
+                      nullptr, amax, nullptr, out_scale);
     return;
   }
   const int64_t sam = row_major ? 1 : lda, sak = row_major ? lda : 1;

@@ -236,9 +236,20 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
     info.log10_peak = INFINITY;
     return info;
   }
+  // A^T Y scaled by 2^-e (e = exponent of max |Y0|): Y and A^T Y of inputs
+  // far from unit magnitude stay in fp32 range (Z is renormalised next)
+  double zscale = 1.0;
+  if (sizeof(T) == 4 && p0.peak > 0.0) {
+    int e;
+    std::frexp(p0.peak, &e);
+    zscale = std::ldexp(1.0, -e);
+    // the feed's fused A_i^T Y_i ran unscaled: keep it only when Y0 is of
+    // ordinary magnitude, else recompute A^T Y scaled (A is resident now)
+    if (e < -40 || e > 40) z_ready = false;
+  }
   for (int it = 0; it < (paper ? 0 : q); ++it) {
     if (!(it == 0 && z_ready))
-      big_tn<T>(c, A, m, n, lda, row_major, Y.p, m, l, Z.p, n, acol.p);
+      big_tn<T>(c, A, m, n, lda, row_major, Y.p, m, l, Z.p, n, acol.p, zscale);
     normalize_sketch<T>(c, Z.p, n, l, n, Zn.p, n);
     big_nn<T>(c, A, m, n, lda, row_major, Zn.p, n, l, Y.p, m, arow.p);
   }
@@ -246,6 +257,9 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
   info.block_reads += 2 * q + 1;
   if (q > 0) {
     const MaxAbs pq = maxabs<T>(c, Y.p, m, l, m);
+    if (std::getenv("BRSVD_DEBUG"))
+      std::fprintf(stderr, "[brsvd] sample peak %.3e -> after %d passes %.3e%s\n", p0.peak, q,
+                   pq.peak, pq.nonfinite ? " (non-finite)" : "");
     if (pq.nonfinite) {
       info.overflow = true;
       info.log10_peak = INFINITY;

@@ -59,6 +59,8 @@ struct Params {
   // epilogue), col_inv[npad] = inverse power-of-two scales of the B columns
   const float* row_max;
   const float* col_inv;
+  int keep_scaled;  // H16: leave the row/column scales in (caller unscales)
+  double out_scale;  // H16: output multiplied by this power of two (range control)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -506,7 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     while (flushed < nchunk) flush(flushed++);
     const int64_t row = m0 + r;
-    if constexpr (H16) {
+    if (H16 && !p.keep_scaled) {
       const float rinv = 1.f / rscale;
 #pragma unroll
       for (int j = 0; j < NH; ++j) {
@@ -514,7 +516,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // power-of-two unscale in fp64: exact, one rounding, no spurious
         // over/underflow of the combined factor
         if (j < hc && col < p.n_out)
-          run[j] = (float)((double)run[j] * ((double)rinv * (double)p.col_inv[col]));
+          run[j] = (float)((double)run[j] *
+                           ((double)rinv * (double)p.col_inv[col] * p.out_scale));
       }
     }
     if (row < p.M) {
@@ -740,16 +743,29 @@ inline void absmax_rows_cols(Ctx& c, const float* A, int64_t m, int64_t n, int64
   BRSVD_CHECK_LAUNCH();
 }
 
+namespace tc {
+// out[0..M) = 1 / (row scale of opA), out[M..M+l) = column inverse scales
+__global__ void export_scales_kernel(const float* __restrict__ row_max, int64_t M,
+                                     const float* __restrict__ col_inv, int l,
+                                     float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M + l;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = i < M ? 1.f / h16_scale(row_max[i]) : col_inv[i - M];
+}
+}  // namespace tc
+
 template <typename T>
 void tc_gemm_launch(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool row_major,
                     bool trans, const T* X, int64_t ldx, int l, T* C, int64_t ldc,
-                    int splits = 0, float* part = nullptr, const float* opa_max = nullptr);
+                    int splits = 0, float* part = nullptr, const float* opa_max = nullptr,
+                    float* scales_out = nullptr, double out_scale = 1.0);
 
 template <>
 inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, int64_t lda,
                                   bool row_major, bool trans, const float* X, int64_t ldx,
                                   int l, float* C, int64_t ldc, int splits, float* part,
-                                  const float* opa_max) {
+                                  const float* opa_max, float* scales_out,
+                                  double out_scale) {
   using namespace tc;
   const int64_t M = trans ? n : m, K = trans ? m : n;
   const bool kmajor = row_major != trans;
@@ -776,6 +792,8 @@ inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, 
   p.part = part;
   p.row_max = nullptr;
   p.col_inv = nullptr;
+  p.keep_scaled = 0;
+  p.out_scale = out_scale;
   DBuf<float> hi, lo, opmax, cinv;
   CUtensorMap mapBhi, mapBlo;
   if (h16) {
@@ -803,6 +821,12 @@ inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, 
                       CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
     p.row_max = opa_max;
     p.col_inv = cinv.p;
+    if (scales_out != nullptr) {  // scaled output: export the inverse scales
+      p.keep_scaled = 1;
+      export_scales_kernel<<<grid_for(M + l), 256, 0, c.stream>>>(opa_max, M, cinv.p, l,
+                                                                   scales_out);
+      BRSVD_CHECK_LAUNCH();
+    }
   } else {
     const int64_t kld = ceil_div(K, 4) * 4;
     hi.alloc(c, (size_t)g.npad * kld);
@@ -861,19 +885,25 @@ inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, 
 template <>
 inline void tc_gemm_launch<double>(Ctx&, const double*, int64_t, int64_t, int64_t, bool, bool,
                                    const double*, int64_t, int, double*, int64_t, int, float*,
-                                   const float*) {
+                                   const float*, float*, double) {
   throw Error(kErrArg, "tcgen05 path is fp32-only");
 }
 
-// Fixed-order sum of the split-K partials (deterministic), fp64 output.
+// Fixed-order sum of the split-K partials (deterministic), fp64 output;
+// scales (optional) = [row inverse scales (M), column inverse scales (N)] of
+// a keep_scaled product, applied in fp64 so Grams of tiny or huge fp32 data
+// neither underflow nor overflow.
 __global__ void splitk_sum_kernel(const float* __restrict__ part, int64_t M, int64_t N,
-                                  int splits, double* __restrict__ C, int64_t ldc) {
+                                  int splits, double* __restrict__ C, int64_t ldc,
+                                  const float* __restrict__ scales = nullptr) {
   const int64_t total = M * N;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int z = 0; z < splits; ++z) s += (double)part[(int64_t)z * total + idx];
-    C[(idx % M) + (idx / M) * ldc] = s;
+    const int64_t i = idx % M, j = idx / M;
+    if (scales) s *= (double)scales[i] * (double)scales[M + j];
+    C[i + j * ldc] = s;
   }
 }
 
@@ -888,12 +918,14 @@ inline bool tc_gram(Ctx& c, const float* X, int64_t r, int a, int64_t ldx, const
   const int64_t tiles = ceil_div(a, tc::BM) * g.nchunks;
   int splits = (int)std::max<int64_t>(1, ceil_div(2 * c.num_sms, tiles));
   splits = (int)std::min<int64_t>(splits, ceil_div(r, 512));
-  DBuf<float> part(c, (size_t)splits * a * b);
-  // Z = A^T Y with A = X (r x a, column-major): trans=true
+  DBuf<float> part(c, (size_t)splits * a * b), scales;
+  if (tc::h16_enabled()) scales.alloc(c, (size_t)a + b);
+  // Z = A^T Y with A = X (r x a, column-major): trans=true; the fp16-split
+  // partials stay in scaled units and are unscaled in fp64 by the sum
   tc_gemm_launch<float>(c, X, r, a, ldx, /*row_major=*/false, /*trans=*/true, Y, ldy, b,
-                        nullptr, 0, splits, part.p);
+                        nullptr, 0, splits, part.p, nullptr, scales.p);
   splitk_sum_kernel<<<grid_for((int64_t)a * b), 256, 0, c.stream>>>(part.p, a, b, splits, C,
-                                                                    ldc);
+                                                                    ldc, scales.p);
   BRSVD_CHECK_LAUNCH();
   return true;
 }

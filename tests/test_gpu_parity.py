@@ -339,3 +339,25 @@ def test_paper_mode_with_reference_omega_is_bit_close():
         np.testing.assert_allclose(f.sigma[:k], g["sigma"][:k], rtol=1e-10)
         s_ang = sin_theta(f.U[:, :k], g["U"][:, :k])
         assert s_ang <= 1e-8
+
+
+@pytest.mark.parametrize("scale,q", [(1e-30, 2), (1e-20, 1), (1e-12, 2), (1e12, 0),
+                                     (1e30, 0)])
+def test_f32_scale_invariance(scale, q):
+    """fp32 inputs far from unit magnitude: the fp16-split product rescales
+    rows/columns by powers of two, A^T Y of the power iteration is taken at a
+    power-of-two scale, and the Grams/Cholesky/Jacobi run in fp64, so the
+    factorization of s*A is s times that of A (to fp32 accuracy).  (Large s
+    with q > 0 trips the reference's overflow guard by design.)"""
+    from paper_1706_07191_b200 import SketchConfig, rsvd_incore
+    a = ref_cpu.lowrank_plus_noise(2048, 1536, 64, 1e-3, seed=4, dtype=np.float32)
+    omega = ref_cpu.normal_sketch(1536, 80, 0, dtype=np.float32)
+    f1 = rsvd_incore(a, SketchConfig(64, 16, q), omega=omega)
+    As = (a.astype(np.float64) * scale).astype(np.float32)
+    import torch
+    for inp in (As, torch.from_numpy(As).cuda()):      # host feed and device paths
+        fs = rsvd_incore(inp, SketchConfig(64, 16, q), omega=omega)
+        sig = np.asarray(fs.sigma.cpu() if hasattr(fs.sigma, "cpu") else fs.sigma)
+        np.testing.assert_allclose(sig[:64] / scale, f1.sigma[:64], rtol=1e-5)
+        U = np.asarray(fs.U.cpu() if hasattr(fs.U, "cpu") else fs.U)
+        assert sin_theta(U[:, :64], f1.U[:, :64]) <= 1e-3
