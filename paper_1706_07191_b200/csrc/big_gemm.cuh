@@ -7,6 +7,7 @@
 #pragma once
 #include "runtime.cuh"
 #include "tc_gemm.cuh"
+#include "skinny64.cuh"
 
 namespace brsvd {
 
@@ -25,6 +26,12 @@ void big_nn(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool row_majo
                       nullptr, amax);
     return;
   }
+  if constexpr (sizeof(T) == 8) {
+    if (skinny_f64(c, row_major, reinterpret_cast<const double*>(A), m, n, lda,
+                   reinterpret_cast<const double*>(X), ldx, l,
+                   reinterpret_cast<double*>(Y), ldy))
+      return;
+  }
   const int64_t sam = row_major ? lda : 1, sak = row_major ? 1 : lda;
   gemm<T, T, T, T>(c, m, l, n, A, sam, sak, X, 1, ldx, Y, 1, ldy);
 }
@@ -38,6 +45,12 @@ void big_tn(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool row_majo
     tc_gemm_launch<T>(c, A, m, n, lda, row_major, /*trans=*/true, Yin, ldy, l, Z, ldz, 0,
                       nullptr, amax, nullptr, out_scale);
     return;
+  }
+  if constexpr (sizeof(T) == 8) {
+    if (skinny_f64(c, !row_major, reinterpret_cast<const double*>(A), n, m, lda,
+                   reinterpret_cast<const double*>(Yin), ldy, l,
+                   reinterpret_cast<double*>(Z), ldz))
+      return;
   }
   const int64_t sam = row_major ? 1 : lda, sak = row_major ? lda : 1;
   gemm<T, T, T, T>(c, n, l, m, A, sam, sak, Yin, 1, ldy, Z, 1, ldz);

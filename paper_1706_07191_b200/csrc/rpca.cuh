@@ -87,6 +87,12 @@ __global__ void matvec_reduce_kernel(const double* __restrict__ part, int64_t O,
 template <typename T>
 void matvec(Ctx& c, const T* X, int64_t O, int64_t Kd, int64_t so, int64_t sk,
             const double* x, double* out) {
+  if constexpr (sizeof(T) == 8) {  // fp64: the streaming skinny product, l = 1
+    if ((sk == 1 || so == 1) &&
+        skinny_f64(c, sk == 1, reinterpret_cast<const double*>(X), O, Kd, sk == 1 ? so : sk,
+                   x, Kd, 1, out, O))
+      return;
+  }
   if (sk == 1) {
     matvec_dot_kernel<T><<<grid_for(O * 32, 256, 148 * 32), 256, 0, c.stream>>>(
         X, O, Kd, so, x, out);
@@ -182,17 +188,35 @@ __global__ void fro_max_kernel(const T* __restrict__ X, int64_t total,
   }
 }
 
-__global__ void sum_max_finalize_kernel(const double* __restrict__ part_sq,
-                                        const double* __restrict__ part_max, int nb,
-                                        double* __restrict__ out) {
-  if (threadIdx.x == 0) {
-    double a = 0.0, b = 0.0;
-    for (int i = 0; i < nb; ++i) {
-      a += part_sq[i];
-      if (part_max) b = fmax(b, part_max[i]);
+// Sum (and max) of nb block partials: one CTA of 1024 threads, each thread a
+// fixed strided subset, then a fixed-shape tree -- deterministic.
+__global__ void __launch_bounds__(1024)
+    sum_max_finalize_kernel(const double* __restrict__ part_sq,
+                            const double* __restrict__ part_max, int nb,
+                            double* __restrict__ out) {
+  __shared__ double r1[32], r2[32];
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    a += part_sq[i];
+    if (part_max) b = fmax(b, part_max[i]);
+  }
+  a = warp_sum(a);
+  b = warp_max(b);
+  if ((threadIdx.x & 31) == 0) {
+    r1[threadIdx.x >> 5] = a;
+    r2[threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int nw = blockDim.x >> 5;
+    a = threadIdx.x < nw ? r1[threadIdx.x] : 0.0;
+    b = threadIdx.x < nw ? r2[threadIdx.x] : 0.0;
+    a = warp_sum(a);
+    b = warp_max(b);
+    if (threadIdx.x == 0) {
+      out[0] = a;
+      out[1] = b;
     }
-    out[0] = a;
-    out[1] = b;
   }
 }
 
@@ -219,6 +243,7 @@ __global__ void rpca_init_kernel(const T* __restrict__ Mx, int64_t total, double
 //   mode 1: L = F diag(shrink(sigma)) G^T only (written to Lout)
 constexpr int kStepLMax = 32;
 constexpr int kStepTS = 16;
+constexpr int kStepGS = 8;  // rows whose loads are batched
 
 template <typename T, int LMAX>
 __global__ void __launch_bounds__(256)
@@ -251,30 +276,44 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   double zz = 0.0;
   if (f < nf) {
-    for (int si = 0; si < kStepTS; ++si) {
-      const int64_t s = s0 + si;
-      if (s >= ns) break;
-      double L = 0.0;
+    // groups of kStepGS rows: all loads of a group issued before any use
+    for (int g0 = 0; g0 < kStepTS; g0 += kStepGS) {
+      T mvs[kStepGS], yvs[kStepGS];
+      if (mode == 0) {
 #pragma unroll
-      for (int r = 0; r < LMAX; ++r) L = fma(fr[r], Gs[si][r], L);
-      const int64_t idx = s * ld + f;
-      if (mode == 1) {
-        Lout[idx] = (T)L;
-        continue;
+        for (int j = 0; j < kStepGS; ++j) {
+          const int64_t s = s0 + g0 + j;
+          const bool ok = s < ns;
+          mvs[j] = ok ? __ldcs(Mx + s * ld + f) : T(0);
+          yvs[j] = ok ? __ldcs(Y + s * ld + f) : T(0);
+        }
       }
-      // the reference evaluates these in the array dtype (rpca.py:195-198)
-      const T Lt = (T)L;
-      const T mv = Mx[idx];
-      const T yv = Y[idx];
-      const T arg = mv - Lt + yv * (T)inv_mu;
-      const T th = (T)lam_over_mu;
-      const T sv = arg > th ? arg - th : (arg < -th ? arg + th : T(0));
-      const T z = mv - Lt - sv;
-      const T yn = yv + (T)mu * z;
-      S[idx] = sv;
-      Y[idx] = yn;
-      W[idx] = mv - sv + yn * (T)inv_mu_next;
-      zz = fma((double)z, (double)z, zz);
+#pragma unroll
+      for (int j = 0; j < kStepGS; ++j) {
+        const int64_t s = s0 + g0 + j;
+        if (s >= ns) break;
+        double L = 0.0;
+#pragma unroll
+        for (int r = 0; r < LMAX; ++r) L = fma(fr[r], Gs[g0 + j][r], L);
+        const int64_t idx = s * ld + f;
+        if (mode == 1) {
+          Lout[idx] = (T)L;
+          continue;
+        }
+        // the reference evaluates these in the array dtype (rpca.py:195-198)
+        const T Lt = (T)L;
+        const T mv = mvs[j];
+        const T yv = yvs[j];
+        const T arg = mv - Lt + yv * (T)inv_mu;
+        const T th = (T)lam_over_mu;
+        const T sv = arg > th ? arg - th : (arg < -th ? arg + th : T(0));
+        const T z = mv - Lt - sv;
+        const T yn = yv + (T)mu * z;
+        __stcs(S + idx, sv);
+        __stcs(Y + idx, yn);
+        __stcs(W + idx, mv - sv + yn * (T)inv_mu_next);
+        zz = fma((double)z, (double)z, zz);
+      }
     }
   }
   if (mode == 1) return;
@@ -300,7 +339,10 @@ void rpca_step(Ctx& c, int mode, int64_t nf, int64_t ns, int64_t ld, int l, cons
   rpca_step_kernel<T, LM><<<grid, 256, 0, c.stream>>>(                              \
       mode, nf, ns, ld, l, F, ldf, G, ldg, sigma, inv_mu, lm, mu, inv_next, Mx, Y, \
       S, W, Lout, part)
-  if (l <= 32) BRSVD_STEP(32);
+  if (l <= 8) BRSVD_STEP(8);
+  else if (l <= 16) BRSVD_STEP(16);
+  else if (l <= 24) BRSVD_STEP(24);
+  else if (l <= 32) BRSVD_STEP(32);
   else if (l <= 64) BRSVD_STEP(64);
   else throw Error(kErrConfig, "ialm_rpca on the GPU supports k + p <= 64");
 #undef BRSVD_STEP
@@ -335,7 +377,7 @@ IalmOut ialm_device(Ctx& c, const T* Mx, int64_t m, int64_t n, bool row_major, i
   DBuf<double> psq(c, nb), pmx(c, nb), sc(c, 2);
   fro_max_kernel<T><<<nb, 256, 0, c.stream>>>(Mx, total, psq.p, pmx.p);
   BRSVD_CHECK_LAUNCH();
-  sum_max_finalize_kernel<<<1, 32, 0, c.stream>>>(psq.p, pmx.p, nb, sc.p);
+  sum_max_finalize_kernel<<<1, 1024, 0, c.stream>>>(psq.p, pmx.p, nb, sc.p);
   BRSVD_CHECK_LAUNCH();
   double hs[2];
   readback(c, sc.p, hs, sizeof(hs));
@@ -374,7 +416,7 @@ IalmOut ialm_device(Ctx& c, const T* Mx, int64_t m, int64_t n, bool row_major, i
     int64_t np = 0;
     rpca_step<T>(c, 0, nf, ns, ld, l, F, ldf, G, ldg, sig.p, mu, lam, rho, Mx, Y.p, S,
                  W.p, nullptr, part.p, &np);
-    sum_max_finalize_kernel<<<1, 32, 0, c.stream>>>(part.p, nullptr, (int)np, zsum.p);
+    sum_max_finalize_kernel<<<1, 1024, 0, c.stream>>>(part.p, nullptr, (int)np, zsum.p);
     BRSVD_CHECK_LAUNCH();
     double z2[2];
     readback(c, zsum.p, z2, sizeof(z2));

@@ -121,12 +121,11 @@ def video_matrix(m, n, seed=0):
     Rb = torch.rand(3, n, generator=g, device="cuda", dtype=torch.float64)
     M = Lb @ Rb
     side = 240                                         # frame 320 x 240 = 76800
-    for j in range(n):
-        x0 = (j * 3) % (320 - 16)
-        rows = torch.arange(100, 116, device="cuda")
-        cols = torch.arange(x0, x0 + 16, device="cuda")
-        idx = (cols[None, :] * side + rows[:, None]).reshape(-1)
-        M[idx, j] = 1.0
+    j = torch.arange(n, device="cuda")
+    x0 = (j * 3) % (320 - 16)                          # moving 16 x 16 block
+    d = torch.arange(16, device="cuda")
+    idx = ((x0[:, None, None] + d[None, :, None]) * side + 100 + d[None, None, :])
+    M[idx.reshape(n, -1), j[:, None]] = 1.0
     return M
 
 
@@ -136,7 +135,9 @@ def bench_c5(steps):
     from paper_1706_07191_b200 import RpcaConfig, ialm_rpca
     M = video_matrix(76800, 20000)
     cfg = RpcaConfig(target_rank=10, oversampling=10, power_exponent=1, tol=1e-7)
-    ialm_rpca(M[:, :2000].contiguous(), cfg)   # warm-up on a slice
+    # warm-up at full size (module load + the device pool's first growth)
+    ialm_rpca(M, RpcaConfig(target_rank=10, oversampling=10, power_exponent=1, tol=1e-7,
+                            max_iterations=1))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     res = ialm_rpca(M, cfg)

@@ -32,17 +32,27 @@ def test_fp32_product_accuracy(m, n, l, layout, trans):
     assert torch.equal(C, C2)
 
 
+@pytest.mark.parametrize("m,n,l", [(700, 300, 30), (1000, 2999, 1), (4097, 517, 8),
+                                   (333, 5000, 13), (2048, 1024, 20), (513, 700, 48),
+                                   (1500, 1300, 64), (300, 200, 100)])
+@pytest.mark.parametrize("layout", ["row", "col"])
 @pytest.mark.parametrize("trans", [False, True])
-def test_fp64_product(trans):
+def test_fp64_product(m, n, l, layout, trans):
+    """fp64 skinny products (kc/mc kernels, l <= 64; generic tiles above),
+    both storage orders, ragged sizes, deterministic."""
     import torch
     from paper_1706_07191_b200.rsvd import sketch_product
-    g = torch.Generator(device="cuda").manual_seed(5)
-    A = torch.randn(700, 300, generator=g, device="cuda", dtype=torch.float64)
-    X = torch.randn(700 if trans else 300, 30, generator=g, device="cuda",
-                    dtype=torch.float64)
+    g = torch.Generator(device="cuda").manual_seed(m + 3 * n + 7 * l)
+    A = torch.randn(m, n, generator=g, device="cuda", dtype=torch.float64)
+    if layout == "col":
+        A = A.t().contiguous().t()
+    X = torch.randn(m if trans else n, l, generator=g, device="cuda", dtype=torch.float64)
     C = sketch_product(A, X, trans=trans)
     ref = (A.t() if trans else A) @ X
-    assert torch.allclose(C, ref, rtol=1e-12, atol=1e-12)
+    bound = (A.abs().t() if trans else A.abs()) @ X.abs()
+    err = ((C - ref).abs() / bound).max().item()
+    assert err <= 1e-14, err
+    assert torch.equal(C, sketch_product(A, X, trans=trans))
 
 
 @pytest.mark.parametrize("trans", [False, True])
