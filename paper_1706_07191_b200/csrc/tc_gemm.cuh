@@ -629,6 +629,61 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Vectorised variant (sr % 4 == 0, ld % 4 == 0, 16-byte aligned S): each
+// thread takes 4 consecutive rows as one float4 per column, so a warp covers
+// 128 rows per 512-byte load and one warp reduction serves 128 rows.  CTA
+// tile: 1024 rows x 64 columns.
+__global__ void __launch_bounds__(256)
+    absmax_rc4_kernel(const float* __restrict__ S, int64_t sr, int64_t sc, int64_t ld,
+                      unsigned* __restrict__ rmax, unsigned* __restrict__ cmax) {
+  __shared__ unsigned wmax[8][64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 4;
+  const int64_t j0 = (int64_t)blockIdx.y * 64;
+  const bool ok = row < sr;
+  unsigned r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+  for (int jb = 0; jb < 64; jb += 16) {
+    float4 v[16];  // all 16 loads in flight before the reductions
+    if (ok && j0 + jb + 16 <= sc) {
+      const float* p = S + row + (j0 + jb) * ld;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = __ldcs(reinterpret_cast<const float4*>(p + u * ld));
+    } else {
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int64_t j = j0 + jb + u;
+        v[u] = (ok && j < sc) ? __ldcs(reinterpret_cast<const float4*>(S + row + j * ld))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const unsigned a = __float_as_uint(fabsf(v[u].x)), b = __float_as_uint(fabsf(v[u].y)),
+                     e = __float_as_uint(fabsf(v[u].z)), d = __float_as_uint(fabsf(v[u].w));
+      r0 = max(r0, a);
+      r1 = max(r1, b);
+      r2 = max(r2, e);
+      r3 = max(r3, d);
+      const unsigned cm = __reduce_max_sync(0xffffffffu, max(max(a, b), max(e, d)));
+      if (lane == 0) wmax[warp][jb + u] = cm;
+    }
+  }
+  if (ok) {
+    atomicMax(&rmax[row], r0);
+    atomicMax(&rmax[row + 1], r1);
+    atomicMax(&rmax[row + 2], r2);
+    atomicMax(&rmax[row + 3], r3);
+  }
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int64_t j = j0 + threadIdx.x;
+    unsigned m = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) m = max(m, wmax[w][threadIdx.x]);
+    if (j < sc && m) atomicMax(&cmax[j], m);
+  }
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                   const cuuint32_t*, CUtensorMapInterleave,
@@ -738,8 +793,13 @@ inline void absmax_rows_cols(Ctx& c, const float* A, int64_t m, int64_t n, int64
     BRSVD_CUDA(cudaMemsetAsync(S_c, 0, sizeof(unsigned) * sc, c.stream));
   }
   if (sr < 1 || sc < 1) return;
-  const dim3 grid((unsigned)ceil_div(sr, 256), (unsigned)ceil_div(sc, 128));
-  tc::absmax_rc_kernel<<<grid, 256, 0, c.stream>>>(A, sr, sc, lda, S_r, S_c);
+  if (sr % 4 == 0 && lda % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) {
+    const dim3 grid((unsigned)ceil_div(sr, 1024), (unsigned)ceil_div(sc, 64));
+    tc::absmax_rc4_kernel<<<grid, 256, 0, c.stream>>>(A, sr, sc, lda, S_r, S_c);
+  } else {
+    const dim3 grid((unsigned)ceil_div(sr, 256), (unsigned)ceil_div(sc, 128));
+    tc::absmax_rc_kernel<<<grid, 256, 0, c.stream>>>(A, sr, sc, lda, S_r, S_c);
+  }
   BRSVD_CHECK_LAUNCH();
 }
 

@@ -89,3 +89,21 @@ def test_fp32_product_dynamic_range(trans, h16, monkeypatch):
     assert torch.isfinite(C).all()
     err = ((C.double() - ref).abs() / bound.clamp_min(1e-300))[ok].max().item()
     assert err <= 2e-6, err
+
+
+@pytest.mark.parametrize("m,n", [(1024, 640), (1027, 333), (4096, 130), (3, 5000)])
+@pytest.mark.parametrize("layout", ["row", "col"])
+def test_absmax_rows_cols(m, n, layout):
+    """Row/column maxima of |A| (the fp16-split scales): vectorised and scalar
+    kernels, both storage orders, ragged sizes, a NaN-free exact match."""
+    import torch
+    from paper_1706_07191_b200.distributed import GpuOps
+    g = torch.Generator(device="cuda").manual_seed(m * 5 + n)
+    A = torch.randn(m, n, generator=g, device="cuda", dtype=torch.float32)
+    A[m // 2] *= 1e20
+    A[:, n // 3] *= 1e-30
+    if layout == "col":
+        A = A.t().contiguous().t()
+    rmax, cmax = GpuOps().absmax(A)
+    assert torch.equal(rmax, A.abs().amax(dim=1))
+    assert torch.equal(cmax, A.abs().amax(dim=0))
