@@ -22,6 +22,7 @@ template <int BT> struct Cfg {
   static constexpr int LDS = BT + 4;                       // padded k-major row (doubles)
   static constexpr int TY = BT / 8, TX = BT / 4;           // 8 x 4 outputs per thread
   static constexpr int NT = TX * TY;
+  static_assert(TX % 8 == 0 && TY % 4 == 0, "warp patches of 8 x 4 threads");
   static constexpr int PER = (BT * BK + NT - 1) / NT;      // loader elements per thread
   static constexpr size_t SMEM = (size_t)2 * 2 * BK * LDS * sizeof(double);
 };
@@ -37,7 +38,11 @@ __global__ void __launch_bounds__(Cfg<BT>::NT, Cfg<BT>::NT <= 288 ? 2 : 1)
   double(*As)[BK][LDS] = reinterpret_cast<double(*)[BK][LDS]>(gsm);
   double(*Bs)[BK][LDS] = reinterpret_cast<double(*)[BK][LDS]>(gsm + 2 * BK * LDS);
   const int tid = threadIdx.x;
-  const int tx = tid % NTX, ty = tid / NTX;
+  // each warp covers an 8 (tx) x 4 (ty) patch of threads, so its 16-byte
+  // shared loads touch 8 (B) / 4 (A) contiguous addresses: one wavefront each
+  const int lane = tid & 31, wid = tid >> 5;
+  const int tx = (wid % (NTX / 8)) * 8 + (lane & 7);
+  const int ty = (wid / (NTX / 8)) * 4 + (lane >> 3);
   // tile index -> (ti, tj)
   int ti, tj;
   const int t = blockIdx.x;

@@ -240,6 +240,10 @@ __host__ __device__ inline size_t jacobi_cluster_smem(int l, int bw) {
   return (size_t)2 * 2 * bw * 2 * lp * sizeof(R);
 }
 
+// Cycle split of the last launch (CTA 0, thread 0): rotations, cluster
+// barriers, block pulls, rounds (BRSVD_JC_TIMING=1 prints it).
+__device__ long long g_jc_t[4];
+
 template <typename R, int NP2>
 __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
   namespace cg = cooperative_groups;
@@ -303,6 +307,7 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
   int r = 0;  // global round counter; tournament round = r % (nb - 1)
   int sweep = 0;
   int my_rot = 0;
+  long long t_rot = 0, t_sync = 0, t_pull = 0, t0 = clock64();
   for (;;) {
     const int tr = r % (nb - 1);
     R* cur = buf + (size_t)(r & 1) * bufsz;
@@ -374,7 +379,11 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
     // Hazards: the pull below reads the peers' buf[r&1] (rotated in this
     // round, before this barrier) and writes our buf[(r+1)&1], which the peers
     // last read while pulling for round r (before this barrier).
+    long long t1 = clock64();
+    t_rot += t1 - t0;
     cluster.sync();
+    t0 = clock64();
+    t_sync += t0 - t1;
     if (sweep_end) {
       if (tid == 0) {
         int tot = 0;
@@ -417,7 +426,16 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
         }
       }
     }
+    t1 = clock64();
+    t_pull += t1 - t0;
+    t0 = t1;
     ++r;
+  }
+  if (me == 0 && tid == 0) {
+    g_jc_t[0] = t_rot;
+    g_jc_t[1] = t_sync;
+    g_jc_t[2] = t_pull;
+    g_jc_t[3] = r;
   }
   // converged: our current pair is in buf[r&1]; write it back
   {

@@ -312,6 +312,13 @@ inline int jacobi(Ctx& c, R* G, int nrow, int ncol, int64_t ldg, R* V, int64_t l
         const int nsw = read_int(c, sw.p);
         std::fprintf(stderr, "[brsvd] jacobi(cluster) %dx%d tol %.1e: %d sweeps\n", nrow,
                      ncol, tol_eff, nsw);
+        if (std::getenv("BRSVD_JC_TIMING")) {
+          long long t[4];
+          BRSVD_CUDA(cudaMemcpyFromSymbol(t, g_jc_t, sizeof(t)));
+          std::fprintf(stderr,
+                       "[brsvd]   cycles: rotations %lld  cluster barriers %lld  pulls %lld"
+                       "  (%lld rounds)\n", t[0], t[1], t[2], t[3]);
+        }
       }
       return 0;
     }
