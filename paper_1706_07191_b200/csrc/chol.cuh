@@ -221,14 +221,22 @@ __global__ void __launch_bounds__(kCiThreads, 1)
     // over the cluster
     const int R2 = rows - nb;
     if (R2 > 0) {
+      // one warp per super-tile of 8 (i) x 4 (j) tiles, lane = 4 ty + tx, so
+      // the 16-byte PT reads of a warp touch 8 / 4 distinct addresses
+      // (2 / 1 wavefronts) instead of 32; super-tiles on or below the
+      // diagonal, row si holding min(nsj, 2 si + 2) of them
       const int nti = (R2 + 3) / 4;
-      const int ntiles = nti * (nti + 1) / 2;
-      for (int t = gt; t < ntiles; t += gnt) {
-        // t -> (ti, tj), tj <= ti, row-major over the lower triangle of tiles
-        int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-        while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-        while (ti * (ti + 1) / 2 > t) --ti;
-        const int tj = t - ti * (ti + 1) / 2;
+      const int nsi = (nti + 7) / 8, nsj = (nti + 3) / 4;
+      int nst = 0;
+      for (int si = 0; si < nsi; ++si) nst += min(nsj, 2 * si + 2);
+      for (int st = gw; st < nst; st += gnw) {
+        int si = 0, rem = st;
+        while (rem >= min(nsj, 2 * si + 2)) {
+          rem -= min(nsj, 2 * si + 2);
+          ++si;
+        }
+        const int ti = si * 8 + (lane >> 2), tj = rem * 4 + (lane & 3);
+        if (ti >= nti || tj > ti) continue;
         const int i0 = nb + 4 * ti, j0 = nb + 4 * tj;
         double acc[4][4];
 #pragma unroll
