@@ -38,6 +38,10 @@ struct JacobiClusterArgs {
   double tol;        // rotate while |x.y| > tol ||x|| ||y||
   double floor_rel;  // columns below floor_rel * ||G||_F are numerically null
   int* sweeps_done;  // optional
+  // > 0: also stop after a sweep whose largest rotated |cos(x, y)| stayed
+  // below stop_cos (quadratic convergence: the next sweep would find nothing
+  // above ~stop_cos^2); the fp32 preconditioning phase uses sqrt(tol)
+  double stop_cos;
 };
 
 __device__ __forceinline__ int tourn_pos(int pos, int r, int n) {
@@ -66,7 +70,7 @@ template <> struct Vec2<double> { using type = double2; };
 template <typename R, int NP2>
 __device__ __forceinline__ bool jc_rotate(R* __restrict__ x, R* __restrict__ y,
                                           R* __restrict__ vx, R* __restrict__ vy, int lp,
-                                          R tol2, R floor2, int lane) {
+                                          R tol2, R floor2, int lane, R& c2max) {
   using V2 = typename Vec2<R>::type;
   V2 xr[NP2], yr[NP2];
   R a = 0, b = 0, g = 0;
@@ -97,6 +101,7 @@ __device__ __forceinline__ bool jc_rotate(R* __restrict__ x, R* __restrict__ y,
   }
   if (!(a > floor2 && b > floor2)) return false;
   if (!(g * g > tol2 * a * b)) return false;
+  c2max = max(c2max, (R)((g * g) / (a * b)));
   R t;
   if (sizeof(R) == 4) {
     // fp32 phase (a preconditioner for the fp64 sweeps): approximate
@@ -152,7 +157,7 @@ template <typename R, int NP2>
 __device__ __forceinline__ bool jc_rotate_x(typename Vec2<R>::type (&xr)[NP2],
                                             typename Vec2<R>::type (&xv)[NP2],
                                             R* __restrict__ y, R* __restrict__ vy, int lp,
-                                            R tol2, R floor2, int lane) {
+                                            R tol2, R floor2, int lane, R& c2max) {
   using V2 = typename Vec2<R>::type;
   V2 yr[NP2];
   R g = 0, aa = 0, b = 0;
@@ -180,6 +185,7 @@ __device__ __forceinline__ bool jc_rotate_x(typename Vec2<R>::type (&xr)[NP2],
   const R a = aa;   // exact norms: cached ones drift and cost a sweep
   if (!(a > floor2 && b > floor2)) return false;
   if (!(g * g > tol2 * a * b)) return false;
+  c2max = max(c2max, (R)((g * g) / (a * b)));
   R t;
   if (sizeof(R) == 4) {
     const float zeta = __fdividef((float)(b - a), 2.0f * (float)g);
@@ -251,6 +257,7 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
   extern __shared__ __align__(16) unsigned char jc_raw[];
   R* buf = reinterpret_cast<R*>(jc_raw);
   __shared__ int s_cnt[2];     // rotations of the current sweep, by sweep parity
+  __shared__ float s_c2[2];    // largest rotated cos^2 of the sweep, by parity
   __shared__ double s_red[32];
   __shared__ int s_stop;
 
@@ -276,7 +283,10 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
       }
     f = warp_sum(f);
     if (lane == 0) s_red[warp] = f;
-    if (tid < 2) s_cnt[tid] = 0;
+    if (tid < 2) {
+      s_cnt[tid] = 0;
+      s_c2[tid] = 0.f;
+    }
     __syncthreads();
     if (tid == 0) {
       double t = 0.0;
@@ -307,6 +317,7 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
   int r = 0;  // global round counter; tournament round = r % (nb - 1)
   int sweep = 0;
   int my_rot = 0;
+  R my_c2 = 0;
   long long t_rot = 0, t_sync = 0, t_pull = 0, t0 = clock64();
   for (;;) {
     const int tr = r % (nb - 1);
@@ -327,7 +338,7 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
           if (!oka || !okb) continue;
           R* x = cur + (size_t)(ca / bw) * slotsz + (size_t)ja * colsz;
           R* y = cur + (size_t)(cb / bw) * slotsz + (size_t)jb * colsz;
-          if (jc_rotate<R, NP2>(x, y, x + lp, y + lp, lp, tol2, floor2, lane)) ++my_rot;
+          if (jc_rotate<R, NP2>(x, y, x + lp, y + lp, lp, tol2, floor2, lane, my_c2)) ++my_rot;
         }
         __syncthreads();
       }
@@ -357,7 +368,8 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
           const int jb = p + st < bw ? p + st : p + st - bw;
           if (jb < vb) {
             R* y = cur + slotsz + (size_t)jb * colsz;
-            if (jc_rotate_x<R, NP2>(xr, xv, y, y + lp, lp, tol2, floor2, lane)) ++my_rot;
+            if (jc_rotate_x<R, NP2>(xr, xv, y, y + lp, lp, tol2, floor2, lane, my_c2))
+              ++my_rot;
           }
         }
         __syncthreads();
@@ -374,8 +386,14 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
       }
     }
     const bool sweep_end = (tr == nb - 2);
-    if (sweep_end && lane == 0 && my_rot) atomicAdd(&s_cnt[sweep & 1], my_rot);
-    if (sweep_end) my_rot = 0;
+    if (sweep_end && lane == 0 && my_rot) {
+      atomicAdd(&s_cnt[sweep & 1], my_rot);
+      atomicMax(reinterpret_cast<int*>(&s_c2[sweep & 1]), __float_as_int((float)my_c2));
+    }
+    if (sweep_end) {
+      my_rot = 0;
+      my_c2 = 0;
+    }
     // Hazards: the pull below reads the peers' buf[r&1] (rotated in this
     // round, before this barrier) and writes our buf[(r+1)&1], which the peers
     // last read while pulling for round r (before this barrier).
@@ -387,9 +405,15 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
     if (sweep_end) {
       if (tid == 0) {
         int tot = 0;
-        for (int q = 0; q < C; ++q) tot += *cluster.map_shared_rank(&s_cnt[sweep & 1], q);
-        s_stop = (tot == 0) || (sweep + 1 >= a.max_sweeps);
+        float c2 = 0.f;
+        for (int q = 0; q < C; ++q) {
+          tot += *cluster.map_shared_rank(&s_cnt[sweep & 1], q);
+          c2 = fmaxf(c2, *cluster.map_shared_rank(&s_c2[sweep & 1], q));
+        }
+        s_stop = (tot == 0) || (sweep + 1 >= a.max_sweeps) ||
+                 (a.stop_cos > 0.0 && (double)c2 < a.stop_cos * a.stop_cos);
         s_cnt[(sweep + 1) & 1] = 0;
+        s_c2[(sweep + 1) & 1] = 0.f;
       }
       __syncthreads();
       if (s_stop) break;

@@ -350,7 +350,9 @@ int small_svd_device(Ctx& c, const T* Bt, int64_t n, int l, int64_t ldb, double*
                                                                                 M32.p, l);
     eye_kernel<float><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(V32.p, l);
     BRSVD_CHECK_LAUNCH();
-    jacobi<float>(c, M32.p, l, l, l, V32.p, l, 1e-5, 40, 16.0 * l * 2.220446049250313e-16);
+    // predicted stop at sqrt(tol): this phase only preconditions the fp64 one
+    jacobi<float>(c, M32.p, l, l, l, V32.p, l, 1e-5, 40, 16.0 * l * 2.220446049250313e-16,
+                  /*stop_cos=*/std::sqrt(1.6e-5));
     copy2d_kernel<float, double><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(V32.p, l, l, l,
                                                                                 Vj.p, l);
     BRSVD_CHECK_LAUNCH();
@@ -365,8 +367,11 @@ int small_svd_device(Ctx& c, const T* Bt, int64_t n, int l, int64_t ldb, double*
   }
   // fp32 data: singular vectors orthogonal to 1e-7 (the output precision) and
   // singular values to ~1e-14 relative; fp64 data: tight.
+  // fp32 data: a sweep whose rotations all stayed below cos 1e-6 leaves
+  // O(1e-12 / gap) behind, so its confirmation sweep is skipped; fp64 data
+  // always confirms.
   const double tol = sizeof(T) == 8 ? jacobi_tol_tight(l) : 1e-7;
-  jacobi(c, M.p, l, l, l, Vj.p, l, tol);
+  jacobi(c, M.p, l, l, l, Vj.p, l, tol, 40, -1.0, sizeof(T) == 8 ? 0.0 : 10.0 * tol);
   jacobi_finish(c, M.p, l, l, l, Vj.p, l, sigma, W, l, Zj.p, l);
   complete_null_columns_kernel<<<1, 1024, (size_t)l * sizeof(double), c.stream>>>(
       W, l, l, l, sigma, 16.0 * l * 2.220446049250313e-16);

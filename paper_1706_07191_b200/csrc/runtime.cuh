@@ -262,7 +262,7 @@ bool jacobi_cluster_launch(Ctx& c, const JacobiClusterArgs<R>& args, int csize,
 
 template <typename R>
 bool jacobi_cluster(Ctx& c, R* G, int l, int64_t ldg, R* V, int64_t ldv, double tol,
-                    double floor_rel, int max_sweeps, int* sweeps_done) {
+                    double floor_rel, int max_sweeps, int* sweeps_done, double stop_cos = 0.0) {
   if (l > 512 || l < 64 || std::getenv("BRSVD_NO_CLUSTER_JACOBI")) return false;
   const size_t lim = c.max_smem_optin > 4096 ? c.max_smem_optin - 4096 : 0;
   for (int csize : {16, 8}) {
@@ -280,6 +280,7 @@ bool jacobi_cluster(Ctx& c, R* G, int l, int64_t ldg, R* V, int64_t ldv, double 
     a.tol = tol;
     a.floor_rel = floor_rel;
     a.sweeps_done = sweeps_done;
+    a.stop_cos = stop_cos;
     const int threads = std::min(1024, std::max(256, 32 * bw));
     const int np2 = (int)ceil_div((l + 3) & ~3, 64);  // row pairs per lane
     bool ok;
@@ -299,7 +300,8 @@ bool jacobi_cluster(Ctx& c, R* G, int l, int64_t ldg, R* V, int64_t ldv, double 
 // columns (noise-level singular values of fp32 data) converge already in fp32.
 template <typename R = double>
 inline int jacobi(Ctx& c, R* G, int nrow, int ncol, int64_t ldg, R* V, int64_t ldv,
-                  double tol, int max_sweeps = 40, double floor_rel = -1.0) {
+                  double tol, int max_sweeps = 40, double floor_rel = -1.0,
+                  double stop_cos = 0.0) {
   BRSVD_REQUIRE(ncol >= 1 && ncol <= 1024 && nrow >= 1, kErrShape,
                 "jacobi: unsupported small-problem shape");
   const double eps_r0 = sizeof(R) == 8 ? 2.220446049250313e-16 : 1.1920928955078125e-07;
@@ -307,7 +309,8 @@ inline int jacobi(Ctx& c, R* G, int nrow, int ncol, int64_t ldg, R* V, int64_t l
   const double floor_eff = floor_rel >= 0.0 ? floor_rel : 16.0 * nrow * eps_r0;
   if (nrow == ncol) {
     DBuf<int> sw(c, 1);
-    if (jacobi_cluster<R>(c, G, nrow, ldg, V, ldv, tol_eff, floor_eff, max_sweeps, sw.p)) {
+    if (jacobi_cluster<R>(c, G, nrow, ldg, V, ldv, tol_eff, floor_eff, max_sweeps, sw.p,
+                          stop_cos)) {
       if (std::getenv("BRSVD_DEBUG")) {
         const int nsw = read_int(c, sw.p);
         std::fprintf(stderr, "[brsvd] jacobi(cluster) %dx%d tol %.1e: %d sweeps\n", nrow,
