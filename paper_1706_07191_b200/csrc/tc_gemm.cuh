@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tfull[s]);
       // earlier chunks' accumulators are complete once this chunk started
-      while (flushed < kb / CHUNK) flush(flushed++);
+      while (flushed < kb / CHUNK - 1) flush(flushed++);
     }
     while (flushed < nchunk) flush(flushed++);
     const int64_t row = m0 + r;
