@@ -106,4 +106,29 @@ __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int splits,
   }
 }
 
+// Same sum for small outputs with many splits: one warp per output, lanes
+// take a fixed strided subset of the splits, then a fixed butterfly --
+// deterministic, and ~splits/32 dependent adds instead of splits.
+template <typename TAcc, typename TC>
+__global__ void splitk_reduce_warp_kernel(int64_t M, int64_t N, int splits,
+                                          const TAcc* __restrict__ part, TC* C, int64_t scm,
+                                          int64_t scn, TAcc alpha, TAcc beta, const TC* C0,
+                                          int64_t sc0m, int64_t sc0n) {
+  const int64_t total = M * N;
+  const int lane = threadIdx.x & 31;
+  for (int64_t idx = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; idx < total;
+       idx += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    TAcc s = TAcc(0);
+    for (int z = lane; z < splits; z += 32) s += part[(int64_t)z * total + idx];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      const int64_t i = idx % M, j = idx / M;
+      TAcc v = alpha * s;
+      if (C0 != nullptr) v += beta * (TAcc)C0[i * sc0m + j * sc0n];
+      C[i * scm + j * scn] = (TC)v;
+    }
+  }
+}
+
 }  // namespace brsvd

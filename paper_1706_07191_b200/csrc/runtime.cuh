@@ -130,8 +130,12 @@ void gemm(Ctx& c, int64_t M, int64_t N, int64_t K, const TA* A, int64_t sam,
   }
   BRSVD_CHECK_LAUNCH();
   if (splits > 1) {
-    splitk_reduce_kernel<TAcc, TC><<<grid_for(M * N), 256, 0, c.stream>>>(
-        M, N, (int)splits, part.p, C, scm, scn, alpha, beta, C0, sc0m, sc0n);
+    if (splits >= 32 && M * N <= 32768)
+      splitk_reduce_warp_kernel<TAcc, TC><<<grid_for(M * N * 32), 256, 0, c.stream>>>(
+          M, N, (int)splits, part.p, C, scm, scn, alpha, beta, C0, sc0m, sc0n);
+    else
+      splitk_reduce_kernel<TAcc, TC><<<grid_for(M * N), 256, 0, c.stream>>>(
+          M, N, (int)splits, part.p, C, scm, scn, alpha, beta, C0, sc0m, sc0n);
     BRSVD_CHECK_LAUNCH();
   }
 }

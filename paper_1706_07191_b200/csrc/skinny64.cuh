@@ -14,8 +14,9 @@
 //       reads of k pairs);
 //   MC  op(A)(i, k) = A[i + k*lda]  (row-major A^T y, column-major A x):
 //       tile As[k][row].
-// Long K is split over grid.y so the units fill >= 16 waves (fp64 partials,
-// summed in a fixed order by splitk_reduce_kernel): deterministic.
+// Long K is split over grid.y so the units fill up to 16 waves while the
+// partials stay within ~1/8 of the A bytes (fp64 partials, summed in a fixed
+// order by splitk_reduce_kernel): deterministic.
 #pragma once
 #include "runtime.cuh"
 
@@ -232,6 +233,8 @@ void launch(Ctx& c, const double* A, int64_t M, int64_t K, int64_t lda, const do
   // >= 16 waves of (row tile, k split) units, k splits of >= 256
   int64_t splits = std::max<int64_t>(1, ceil_div(16 * (int64_t)c.num_sms, blocks));
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, K / 256));
+  // the fp64 partials (splits * M * l) stay within ~1/8 of the A stream
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, K / (8 * (int64_t)l)));
   int64_t kchunk = ceil_div(ceil_div(K, splits), (int64_t)kKT) * kKT;
   splits = std::max<int64_t>(1, ceil_div(K, kchunk));
   DBuf<double> part;
