@@ -181,13 +181,24 @@ __global__ void __launch_bounds__(kThreads)
       }
       const double2* b0 = reinterpret_cast<const double2*>(bs + kk * LB);
       const double2* b1 = reinterpret_cast<const double2*>(bs + (kk + 1) * LB);
+      // k then k + 1 over all columns: an accumulator's two updates are
+      // R * LB FMAs apart (no back-to-back dependent DFMAs)
 #pragma unroll
       for (int c2 = 0; c2 < LB / 2; ++c2) {
-        const double2 x0 = b0[c2], x1 = b1[c2];
+        const double2 x0 = b0[c2];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          acc[r][2 * c2] = fma(a1[r], x1.x, fma(a0[r], x0.x, acc[r][2 * c2]));
-          acc[r][2 * c2 + 1] = fma(a1[r], x1.y, fma(a0[r], x0.y, acc[r][2 * c2 + 1]));
+          acc[r][2 * c2] = fma(a0[r], x0.x, acc[r][2 * c2]);
+          acc[r][2 * c2 + 1] = fma(a0[r], x0.y, acc[r][2 * c2 + 1]);
+        }
+      }
+#pragma unroll
+      for (int c2 = 0; c2 < LB / 2; ++c2) {
+        const double2 x1 = b1[c2];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          acc[r][2 * c2] = fma(a1[r], x1.x, acc[r][2 * c2]);
+          acc[r][2 * c2 + 1] = fma(a1[r], x1.y, acc[r][2 * c2 + 1]);
         }
       }
     }
