@@ -107,3 +107,28 @@ def test_absmax_rows_cols(m, n, layout):
     rmax, cmax = GpuOps().absmax(A)
     assert torch.equal(rmax, A.abs().amax(dim=1))
     assert torch.equal(cmax, A.abs().amax(dim=0))
+
+
+@pytest.mark.parametrize("m,n,l", [(1, 1, 1), (1, 300, 5), (300, 1, 5), (17, 33, 64),
+                                   (129, 17, 2), (5, 4000, 12)])
+@pytest.mark.parametrize("layout", ["row", "col", "odd_ld"])
+@pytest.mark.parametrize("trans", [False, True])
+def test_fp64_product_edges(m, n, l, layout, trans):
+    """fp64 skinny products at degenerate and ragged shapes, and with an odd
+    leading dimension (not 16-byte aligned rows: the generic tiled kernel)."""
+    import torch
+    from paper_1706_07191_b200.rsvd import sketch_product
+    g = torch.Generator(device="cuda").manual_seed(m * 131 + n * 7 + l)
+    if layout == "odd_ld":
+        stride = n + 1 if (n + 1) % 2 else n + 2        # an odd row stride
+        A = torch.randn(m, stride, generator=g, device="cuda", dtype=torch.float64)[:, :n]
+    else:
+        A = torch.randn(m, n, generator=g, device="cuda", dtype=torch.float64)
+        if layout == "col":
+            A = A.t().contiguous().t()
+    X = torch.randn(m if trans else n, l, generator=g, device="cuda", dtype=torch.float64)
+    C = sketch_product(A, X, trans=trans)
+    ref = (A.t() if trans else A) @ X
+    bound = (A.abs().t() if trans else A.abs()) @ X.abs()
+    err = ((C - ref).abs() / bound.clamp_min(1e-300)).max().item()
+    assert err <= 1e-14, err
