@@ -481,13 +481,11 @@ inline void cholinv_launch(cudaStream_t st, size_t smem_limit, double* A, int n,
                            double rank_tol, double* X, double* T, double* s_out,
                            double* info, int* keep) {
   const size_t smem = cholinv_smem(n);
-  static size_t attr = 0;
-  if (attr < smem) {
+  {  // function attributes are per device: set on every call
     const cudaError_t e = cudaFuncSetAttribute(
         cholinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
       throw Error(kErrCuda, std::string("cholinv smem attribute: ") + cudaGetErrorString(e));
-    attr = smem;
   }
   (void)smem_limit;
   cudaLaunchConfig_t cfg = {};

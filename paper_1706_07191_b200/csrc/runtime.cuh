@@ -154,13 +154,10 @@ void gram_fp64_bt(Ctx& c, int64_t a, int64_t b, int64_t r, const TX* X, int64_t 
   int64_t kchunk = ceil_div(ceil_div(r, splits), BK) * BK;
   splits = ceil_div(r, kchunk);
   DBuf<double> part(c, (size_t)(splits * a * b));
-  static bool attr = false;
-  if (!attr) {
-    BRSVD_CUDA(cudaFuncSetAttribute(gram_tile_kernel<TX, TY, BT>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)Cfg<BT>::SMEM));
-    attr = true;
-  }
+  // (function attributes are per device: set on every call, ~1 us of host time)
+  BRSVD_CUDA(cudaFuncSetAttribute(gram_tile_kernel<TX, TY, BT>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)Cfg<BT>::SMEM));
   gram_tile_kernel<TX, TY, BT><<<dim3(tiles, (unsigned)splits), Cfg<BT>::NT, Cfg<BT>::SMEM,
                                  c.stream>>>(r, (int)a, (int)b, X, ldx, Y, ldy, sym ? 1 : 0,
                                              ntj, kchunk, part.p);
@@ -346,13 +343,8 @@ inline int jacobi(Ctx& c, R* G, int nrow, int ncol, int64_t ldg, R* V, int64_t l
   if (nb == 2) single = true;
   const int threads = std::min(1024, std::max(64, bw * 32));
   const size_t smem = (size_t)2 * bw * per_col;
-  static bool attr_set = false;
-  if (!attr_set) {
-    BRSVD_CUDA(cudaFuncSetAttribute(jacobi_block_kernel<R>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)budget));
-    attr_set = true;
-  }
+  BRSVD_CUDA(cudaFuncSetAttribute(jacobi_block_kernel<R>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget));
   DBuf<int> counters(c, (size_t)max_sweeps + 1);
   BRSVD_CUDA(cudaMemsetAsync(counters.p, 0, sizeof(int) * (max_sweeps + 1), c.stream));
   JacobiArgs<R> args;
