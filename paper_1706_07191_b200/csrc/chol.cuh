@@ -302,25 +302,35 @@ __global__ void __launch_bounds__(kCiThreads, 1)
     Xc[(size_t)bI * BB + r * kCiLd + cc] = ok ? A[(int64_t)(i0 + cc) * ld + (i0 + r)] : 0.0;
   }
   __syncthreads();
+  // Each diagonal block inverted by one warp, right-looking: lane c owns
+  // column c of X = L_II^-1 and the pending sums acc[j] of rows k + j (the
+  // array shifts by one row per step, so the loop body is compact);
+  // X[k][c] = (delta_kc - acc) / L[k][k] with the reciprocals formed up
+  // front by all lanes, then acc[j] += L[k+j][k] X[k][c] (broadcast reads).
+  // The dependent chain per row is one multiply and one FMA.
   for (int bI = warp; bI < nblk; bI += nw) {
     const int nbI = min(kCiNB, n - bI * kCiNB);
     const double* Lb = Xc + (size_t)bI * BB;
     double* Dv = Dinv + (size_t)bI * BB;
-    const int c = lane;   // column c of the inverse, rows r >= c
-    for (int r = 0; r < kCiNB; ++r) {
-      double v0 = (r == c) ? 1.0 : 0.0, v1 = 0.0;
-      if (c < r && r < nbI) {
-        int k = c;
-        for (; k + 1 < r; k += 2) {
-          v0 = fma(-Lb[r * kCiLd + k], Dv[k * kCiLd + c], v0);
-          v1 = fma(-Lb[r * kCiLd + k + 1], Dv[(k + 1) * kCiLd + c], v1);
-        }
-        if (k < r) v0 = fma(-Lb[r * kCiLd + k], Dv[k * kCiLd + c], v0);
+    const int c = lane;
+    const double dgl = Lb[c * kCiLd + c];
+    const double rl = (c < nbI && dgl != 0.0) ? 1.0 / dgl : 0.0;
+    double acc[kCiNB];
+#pragma unroll
+    for (int j = 0; j < kCiNB; ++j) acc[j] = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < kCiNB; ++k) {
+      const double rk = __shfl_sync(0xffffffffu, rl, k);
+      const double x = ((k == c ? 1.0 : 0.0) - acc[0]) * rk;
+      Dv[k * kCiLd + c] = x;
+#pragma unroll
+      for (int j = 1; j < kCiNB; ++j) {
+        const double l = (k + j < kCiNB) ? Lb[(k + j) * kCiLd + k] : 0.0;
+        acc[j] = fma(l, x, acc[j]);
       }
-      const double x = (r >= c && r < nbI && c < nbI) ? (v0 + v1) / Lb[r * kCiLd + r] : 0.0;
-      __syncwarp();
-      Dv[r * kCiLd + c] = x;
-      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < kCiNB - 1; ++j) acc[j] = acc[j + 1];
+      acc[kCiNB - 1] = 0.0;
     }
   }
   __syncthreads();
