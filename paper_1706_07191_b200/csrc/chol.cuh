@@ -88,7 +88,6 @@ __global__ void __launch_bounds__(kCiThreads, 1)
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   const int me = (int)cluster.block_rank(), C = (int)cluster.num_blocks();
-  const int gt = me * nt + tid, gnt = C * nt;      // cluster-wide thread index
   const int gw = me * nw + warp, gnw = C * nw;     // cluster-wide warp index
   const bool leader = (me == 0);
 
