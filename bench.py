@@ -66,9 +66,16 @@ def dist_setup(args):
     if world > 1:
         import torch
         import torch.distributed as dist
+        # BRSVD_BENCH_BACKEND=gloo (checks only): several ranks may then share
+        # one GPU, e.g. to exercise the sharded path on a 1-GPU box
+        backend = os.environ.get("BRSVD_BENCH_BACKEND", "nccl")
+        local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
 
 
@@ -77,7 +84,8 @@ def max_over_ranks(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -372,8 +380,8 @@ def run_ours(args, world, rank, local):
         A = torch.as_tensor(a_host).to(dev)
         del pinned
 
-    cpu = None
-    if rank == 0 and not args.no_cpu:
+    cpu = None   # the CPU oracle is timed on rank 0 of a 1-GPU run only
+    if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(A, 16384)
 
     if rank == 0:
