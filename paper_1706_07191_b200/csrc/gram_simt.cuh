@@ -18,22 +18,27 @@ namespace brsvd {
 namespace gram {
 
 constexpr int BK = 32;  // k slab
-template <int BT> struct Cfg {
+// NCG column groups of stride CS = BT / NCG: each thread owns 8 rows (two
+// halves) x 2 NCG columns (2 per group); NCG = 3 at BT = 96 gives 8 x 6
+// register tiles (48 FMAs per 7 16-byte shared loads)
+template <int BT, int NCG = 2> struct Cfg {
   static constexpr int LDS = BT + 4;                       // padded k-major row (doubles)
-  static constexpr int TY = BT / 8, TX = BT / 4;           // 8 x 4 outputs per thread
+  static constexpr int CS = BT / NCG;                      // column-group stride
+  static constexpr int TY = BT / 8, TX = CS / 2;           // 8 x (2 NCG) outputs per thread
   static constexpr int NT = TX * TY;
   static_assert(TX % 8 == 0 && TY % 4 == 0, "warp patches of 8 x 4 threads");
   static constexpr int PER = (BT * BK + NT - 1) / NT;      // loader elements per thread
   static constexpr size_t SMEM = (size_t)2 * 2 * BK * LDS * sizeof(double);
 };
 
-template <typename TX, typename TY, int BT>
-__global__ void __launch_bounds__(Cfg<BT>::NT, Cfg<BT>::NT <= 288 ? 2 : 1)
+template <typename TX, typename TY, int BT, int NCG>
+__global__ void __launch_bounds__(Cfg<BT, NCG>::NT, Cfg<BT, NCG>::NT <= 288 ? 2 : 1)
     gram_tile_kernel(int64_t r, int a, int b, const TX* __restrict__ X, int64_t ldx,
                      const TY* __restrict__ Y, int64_t ldy, int sym, int ntj, int64_t kchunk,
                      double* __restrict__ part) {
-  using C = Cfg<BT>;
+  using C = Cfg<BT, NCG>;
   constexpr int LDS = C::LDS, NTX = C::TX, NT = C::NT, PER = C::PER, H = BT / 2;
+  constexpr int CS = C::CS, NV = 2 * NCG;
   extern __shared__ __align__(16) double gsm[];
   double(*As)[BK][LDS] = reinterpret_cast<double(*)[BK][LDS]>(gsm);
   double(*Bs)[BK][LDS] = reinterpret_cast<double(*)[BK][LDS]>(gsm + 2 * BK * LDS);
@@ -87,11 +92,11 @@ __global__ void __launch_bounds__(Cfg<BT>::NT, Cfg<BT>::NT <= 288 ? 2 : 1)
       }
     }
   };
-  double acc[8][4];
+  double acc[8][NV];
 #pragma unroll
   for (int u = 0; u < 8; ++u)
 #pragma unroll
-    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+    for (int v = 0; v < NV; ++v) acc[u][v] = 0.0;
 
   int buf = 0;
   if (kb < ke) {
@@ -110,13 +115,18 @@ __global__ void __launch_bounds__(Cfg<BT>::NT, Cfg<BT>::NT <= 288 ? 2 : 1)
       const double2* pa = reinterpret_cast<const double2*>(&As[buf][kk][ty * 4]);
       const double2* pb = reinterpret_cast<const double2*>(&Bs[buf][kk][tx * 2]);
       const double2 a01 = pa[0], a23 = pa[1], a45 = pa[H / 2], a67 = pa[H / 2 + 1];
-      const double2 b01 = pb[0], b23 = pb[H / 2];
       const double av[8] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y};
-      const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+      double bv[NV];
+#pragma unroll
+      for (int q = 0; q < NCG; ++q) {
+        const double2 bq = pb[q * (CS / 2)];
+        bv[2 * q] = bq.x;
+        bv[2 * q + 1] = bq.y;
+      }
 #pragma unroll
       for (int u = 0; u < 8; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
+        for (int v = 0; v < NV; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
     }
     if (more) {
       store(buf ^ 1);
@@ -131,8 +141,8 @@ __global__ void __launch_bounds__(Cfg<BT>::NT, Cfg<BT>::NT <= 288 ? 2 : 1)
     const int i = i0 + (u < 4 ? ty * 4 + u : H + ty * 4 + u - 4);
     if (i >= a) continue;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int j = j0 + (v < 2 ? tx * 2 + v : H + tx * 2 + v - 2);
+    for (int v = 0; v < NV; ++v) {
+      const int j = j0 + (v >> 1) * CS + tx * 2 + (v & 1);
       if (j < b) P[i + (int64_t)j * a] = acc[u][v];
     }
   }

@@ -142,24 +142,24 @@ void gemm(Ctx& c, int64_t M, int64_t N, int64_t K, const TA* A, int64_t sam,
 
 // Tall-skinny fp64 Gram C (a x b) = X^T Y (gram_simt.cuh), deterministic
 // split-K; symmetric when X is Y.
-template <typename TX, typename TY, int BT>
+template <typename TX, typename TY, int BT, int NCG = 2>
 void gram_fp64_bt(Ctx& c, int64_t a, int64_t b, int64_t r, const TX* X, int64_t ldx,
                   const TY* Y, int64_t ldy, double* C, int64_t ldc, bool sym) {
   using namespace gram;
   const int nti = (int)ceil_div(a, BT), ntj = (int)ceil_div(b, BT);
   const int tiles = sym ? nti * (nti + 1) / 2 : nti * ntj;
-  const int per_sm = Cfg<BT>::NT <= 288 ? 2 : 1;
+  const int per_sm = Cfg<BT, NCG>::NT <= 288 ? 2 : 1;
   int64_t splits = std::max<int64_t>(1, ceil_div((int64_t)per_sm * c.num_sms, tiles));
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, r / (4 * BK)));
   int64_t kchunk = ceil_div(ceil_div(r, splits), BK) * BK;
   splits = ceil_div(r, kchunk);
   DBuf<double> part(c, (size_t)(splits * a * b));
   // (function attributes are per device: set on every call, ~1 us of host time)
-  BRSVD_CUDA(cudaFuncSetAttribute(gram_tile_kernel<TX, TY, BT>,
+  BRSVD_CUDA(cudaFuncSetAttribute(gram_tile_kernel<TX, TY, BT, NCG>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)Cfg<BT>::SMEM));
-  gram_tile_kernel<TX, TY, BT><<<dim3(tiles, (unsigned)splits), Cfg<BT>::NT, Cfg<BT>::SMEM,
-                                 c.stream>>>(r, (int)a, (int)b, X, ldx, Y, ldy, sym ? 1 : 0,
+                                  (int)Cfg<BT, NCG>::SMEM));
+  gram_tile_kernel<TX, TY, BT, NCG><<<dim3(tiles, (unsigned)splits), Cfg<BT, NCG>::NT,
+                                      Cfg<BT, NCG>::SMEM, c.stream>>>(r, (int)a, (int)b, X, ldx, Y, ldy, sym ? 1 : 0,
                                              ntj, kchunk, part.p);
   BRSVD_CHECK_LAUNCH();
   gram_reduce_kernel<<<grid_for(a * b), 256, 0, c.stream>>>(part.p, (int)a, (int)b,
@@ -177,7 +177,8 @@ void gram_fp64(Ctx& c, int64_t a, int64_t b, int64_t r, const TX* X, int64_t ldx
   const int64_t w96 = ceil_div(a, 96) * ceil_div(b, 96) * 96 * 96;
   const int64_t w128 = ceil_div(a, 128) * ceil_div(b, 128) * 128 * 128;
   if (w96 < w128)
-    gram_fp64_bt<TX, TY, 96>(c, a, b, r, X, ldx, Y, ldy, C, ldc, sym);
+    gram_fp64_bt<TX, TY, 96, (sizeof(TX) == 4 && sizeof(TY) == 4) ? 3 : 2>(c, a, b, r, X, ldx,
+                                                                           Y, ldy, C, ldc, sym);
   else
     gram_fp64_bt<TX, TY, 128>(c, a, b, r, X, ldx, Y, ldy, C, ldc, sym);
 }
