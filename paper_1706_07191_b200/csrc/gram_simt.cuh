@@ -32,7 +32,8 @@ template <int BT, int NCG = 2> struct Cfg {
 };
 
 template <typename TX, typename TY, int BT, int NCG>
-__global__ void __launch_bounds__(Cfg<BT, NCG>::NT, Cfg<BT, NCG>::NT <= 288 ? 2 : 1)
+__global__ void __launch_bounds__(Cfg<BT, NCG>::NT,
+                                  (Cfg<BT, NCG>::NT <= 288 && sizeof(TX) == 4) ? 2 : 1)
     gram_tile_kernel(int64_t r, int a, int b, const TX* __restrict__ X, int64_t ldx,
                      const TY* __restrict__ Y, int64_t ldy, int sym, int ntj, int64_t kchunk,
                      double* __restrict__ part) {

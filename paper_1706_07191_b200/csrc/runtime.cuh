@@ -148,7 +148,7 @@ void gram_fp64_bt(Ctx& c, int64_t a, int64_t b, int64_t r, const TX* X, int64_t 
   using namespace gram;
   const int nti = (int)ceil_div(a, BT), ntj = (int)ceil_div(b, BT);
   const int tiles = sym ? nti * (nti + 1) / 2 : nti * ntj;
-  const int per_sm = Cfg<BT, NCG>::NT <= 288 ? 2 : 1;
+  const int per_sm = (Cfg<BT, NCG>::NT <= 288 && sizeof(TX) == 4) ? 2 : 1;
   int64_t splits = std::max<int64_t>(1, ceil_div((int64_t)per_sm * c.num_sms, tiles));
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, r / (4 * BK)));
   int64_t kchunk = ceil_div(ceil_div(r, splits), BK) * BK;
