@@ -70,7 +70,7 @@ __device__ __forceinline__ bool jacobi_rotate_pair(R* x, R* y, R* vx, R* vy, int
     t = copysign(R(1), zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, R(1))));
   }
   if (t == R(0)) return false;
-  const R c = R(1) / sqrt(fma(t, t, R(1)));
+  const R c = rsqrt(fma(t, t, R(1)));  // 1 ulp; s = c t keeps c^2 + s^2 = 1 to ~2 ulp
   const R s = c * t;
   if (nrow == ncol) {
     for (int i = lane; i < nrow; i += 32) {

@@ -57,7 +57,7 @@ __device__ __forceinline__ R jc_rsqrt(R x);
 template <>
 __device__ __forceinline__ float jc_rsqrt<float>(float x) { return rsqrtf(x); }
 template <>
-__device__ __forceinline__ double jc_rsqrt<double>(double x) { return 1.0 / sqrt(x); }
+__device__ __forceinline__ double jc_rsqrt<double>(double x) { return rsqrt(x); }  // 1 ulp
 
 template <typename R> struct Vec2;
 template <> struct Vec2<float> { using type = float2; };
