@@ -564,24 +564,36 @@ __global__ void tc_split_kernel(const float* __restrict__ X, int64_t K, int n_sr
 
 // One CTA per (padded) column: max |X[:, j]| by a block reduction, then the
 // scaled fp16 (hi, lo) split of that column -- one pass, no atomics.
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(512)
     tc_split16_col_kernel(const float* __restrict__ X, int64_t K, int n_src, int64_t ldx,
                           int64_t kld, uint16_t* __restrict__ hi, uint16_t* __restrict__ lo,
                           float* __restrict__ col_inv) {
-  __shared__ unsigned red[8];
+  __shared__ unsigned red[16];
   const int j = blockIdx.x;
   const float* col = X + (int64_t)j * ldx;
   const bool real = j < n_src;
+  // 16-byte loads / 8-byte stores when the column allows it (kld % 8 == 0)
+  const bool vec = ((reinterpret_cast<uintptr_t>(col) & 15) == 0) && (K % 4 == 0);
   unsigned m = 0;
-  if (real)
-    for (int64_t k = threadIdx.x; k < K; k += blockDim.x)
-      m = max(m, __float_as_uint(fabsf(col[k])));
+  if (real) {
+    if (vec) {
+      const float4* c4 = reinterpret_cast<const float4*>(col);
+      for (int64_t k = threadIdx.x; k < K / 4; k += blockDim.x) {
+        const float4 v = c4[k];
+        m = max(m, max(max(__float_as_uint(fabsf(v.x)), __float_as_uint(fabsf(v.y))),
+                       max(__float_as_uint(fabsf(v.z)), __float_as_uint(fabsf(v.w)))));
+      }
+    } else {
+      for (int64_t k = threadIdx.x; k < K; k += blockDim.x)
+        m = max(m, __float_as_uint(fabsf(col[k])));
+    }
+  }
   m = __reduce_max_sync(0xffffffffu, m);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned t = 0;
-    for (int w = 0; w < 8; ++w) t = max(t, red[w]);
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = max(t, red[w]);
     red[0] = t;
   }
   __syncthreads();
@@ -589,11 +601,31 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) col_inv[j] = 1.f / sc;
   uint16_t* h = hi + (int64_t)j * kld;
   uint16_t* l = lo + (int64_t)j * kld;
-  for (int64_t k = threadIdx.x; k < kld; k += blockDim.x) {
-    const float x = (real && k < K) ? col[k] * sc : 0.f;
-    const __half hh = __float2half_rn(x);
-    h[k] = __half_as_ushort(hh);
-    l[k] = __half_as_ushort(__float2half_rn(x - __half2float(hh)));
+  if (vec) {
+    const float4* c4 = reinterpret_cast<const float4*>(col);
+    for (int64_t q = threadIdx.x; q < kld / 4; q += blockDim.x) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (real && 4 * q < K) v = c4[q];
+      const float xs[4] = {v.x * sc, v.y * sc, v.z * sc, v.w * sc};
+      uint16_t hh[4], ll[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const __half hv = __float2half_rn(xs[e]);
+        hh[e] = __half_as_ushort(hv);
+        ll[e] = __half_as_ushort(__float2half_rn(xs[e] - __half2float(hv)));
+      }
+      reinterpret_cast<uint2*>(h)[q] =
+          make_uint2(hh[0] | ((uint32_t)hh[1] << 16), hh[2] | ((uint32_t)hh[3] << 16));
+      reinterpret_cast<uint2*>(l)[q] =
+          make_uint2(ll[0] | ((uint32_t)ll[1] << 16), ll[2] | ((uint32_t)ll[3] << 16));
+    }
+  } else {
+    for (int64_t k = threadIdx.x; k < kld; k += blockDim.x) {
+      const float x = (real && k < K) ? col[k] * sc : 0.f;
+      const __half hh = __float2half_rn(x);
+      h[k] = __half_as_ushort(hh);
+      l[k] = __half_as_ushort(__float2half_rn(x - __half2float(hh)));
+    }
   }
 }
 
@@ -869,7 +901,7 @@ inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, 
     cinv.alloc(c, (size_t)g.npad);
     hi.alloc(c, (size_t)g.npad * kld / 2 + 8);
     lo.alloc(c, (size_t)g.npad * kld / 2 + 8);
-    tc_split16_col_kernel<<<(unsigned)g.npad, 256, 0, c.stream>>>(
+    tc_split16_col_kernel<<<(unsigned)g.npad, 512, 0, c.stream>>>(
         X, K, l, ldx, kld, reinterpret_cast<uint16_t*>(hi.p),
         reinterpret_cast<uint16_t*>(lo.p), cinv.p);
     BRSVD_CHECK_LAUNCH();
