@@ -113,10 +113,24 @@ RsvdInfo rsvd_stream(Ctx& c, const T* Ah, int64_t m, int64_t n, int64_t lda, boo
       const T* Xin = it == 0 ? X : Zn.p;
       const bool more = it < q;
       if (more) BRSVD_CUDA(cudaMemsetAsync(Z.p, 0, sizeof(T) * n * l, c.stream));
+      // A^T Y is accumulated at a power-of-two scale fixed by the first
+      // panel's max |Y_i| (fp32 inputs far from unit magnitude would
+      // otherwise underflow / overflow in Z; Z is renormalised right after)
+      double zscale = 1.0;
+      bool zscale_set = false;
       ps.pass([&](const T* Ap, int64_t ld, int64_t r0, int64_t r1) {
         big_nn<T>(c, Ap, r1 - r0, n, ld, true, Xin, n, l, Y.p + r0, m);
         if (more) {
-          big_tn<T>(c, Ap, r1 - r0, n, ld, true, Y.p + r0, m, l, tmpZ.p, n);
+          if (sizeof(T) == 4 && !zscale_set) {
+            const MaxAbs pk = maxabs<T>(c, Y.p + r0, r1 - r0, l, m);
+            if (pk.peak > 0.0 && std::isfinite(pk.peak)) {
+              int e;
+              std::frexp(pk.peak, &e);
+              zscale = std::ldexp(1.0, -e);
+            }
+            zscale_set = true;
+          }
+          big_tn<T>(c, Ap, r1 - r0, n, ld, true, Y.p + r0, m, l, tmpZ.p, n, nullptr, zscale);
           axpy<T>(c, tmpZ.p, n, l, n, Z.p, n);
         }
       });
@@ -140,8 +154,23 @@ RsvdInfo rsvd_stream(Ctx& c, const T* Ah, int64_t m, int64_t n, int64_t lda, boo
       T* acc = it == 0 ? Y.p : Ynew.p;
       BRSVD_CUDA(cudaMemsetAsync(acc, 0, sizeof(T) * m * l, c.stream));
       if (it > 0) normalize_sketch<T>(c, Y.p, m, l, m, Yn.p, m);
+      // A_J^T Yn at a power-of-two scale fixed by the first block (fp32
+      // inputs far from unit magnitude would under/overflow A_J A_J^T Yn;
+      // the sum is renormalised in the next iteration)
+      double zscale = 1.0;
+      bool zscale_set = false;
       ps.pass([&](const T* Ap, int64_t ld, int64_t j0, int64_t j1) {
         const int64_t w = j1 - j0;
+        if (it > 0 && sizeof(T) == 4 && !zscale_set) {
+          big_tn<T>(c, Ap, m, w, ld, false, Yn.p, m, l, tmpZ.p, pmax);
+          const MaxAbs pk = maxabs<T>(c, tmpZ.p, w, l, pmax);
+          if (pk.peak > 0.0 && std::isfinite(pk.peak)) {
+            int e;
+            std::frexp(pk.peak, &e);
+            zscale = std::ldexp(1.0, -e);
+          }
+          zscale_set = true;
+        }
         if (it == 0) {
           big_nn<T>(c, Ap, m, w, ld, false, X + j0, n, l, tmpY.p, m);
           for (int pw = 0; block_power && pw < q; ++pw) {
@@ -149,7 +178,7 @@ RsvdInfo rsvd_stream(Ctx& c, const T* Ah, int64_t m, int64_t n, int64_t lda, boo
             big_nn<T>(c, Ap, m, w, ld, false, tmpZ.p, pmax, l, tmpY.p, m);
           }
         } else {
-          big_tn<T>(c, Ap, m, w, ld, false, Yn.p, m, l, tmpZ.p, pmax);
+          big_tn<T>(c, Ap, m, w, ld, false, Yn.p, m, l, tmpZ.p, pmax, nullptr, zscale);
           big_nn<T>(c, Ap, m, w, ld, false, tmpZ.p, pmax, l, tmpY.p, m);
         }
         axpy<T>(c, tmpY.p, m, l, m, acc, m);

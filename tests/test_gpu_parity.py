@@ -361,3 +361,23 @@ def test_f32_scale_invariance(scale, q):
         np.testing.assert_allclose(sig[:64] / scale, f1.sigma[:64], rtol=1e-5)
         U = np.asarray(fs.U.cpu() if hasattr(fs.U, "cpu") else fs.U)
         assert sin_theta(U[:, :64], f1.U[:, :64]) <= 1e-3
+
+
+@pytest.mark.parametrize("order", ["C", "F"])
+@pytest.mark.parametrize("scale", [1e-30, 1e-20])
+def test_streamed_scale_invariance(order, scale):
+    """The panel streamer (row panels for C order, column panels for F order)
+    accumulates A^T Y / A_J^T Y at a power-of-two scale set by its first
+    panel, so tiny fp32 inputs factor like the unit-scale ones."""
+    from paper_1706_07191_b200 import SketchConfig
+    from paper_1706_07191_b200.rsvd import run_rsvd, run_rsvd_stream
+    a = ref_cpu.lowrank_plus_noise(3000, 1200, 20, 1e-3, seed=21, dtype=np.float32)
+    omega = ref_cpu.normal_sketch(1200, 30, 0, dtype=np.float32)
+    cfg = SketchConfig(20, 10, 2)
+    base = run_rsvd(np.asarray(a, order=order), cfg, omega=omega, warn=False)
+    st = run_rsvd_stream(np.asarray((a.astype(np.float64) * scale).astype(np.float32),
+                                    order=order), cfg, panel=257, nbuf=3, omega=omega,
+                         warn=False)
+    np.testing.assert_allclose(st.factors.sigma[:20] / scale, base.factors.sigma[:20],
+                               rtol=1e-5)
+    assert sin_theta(st.factors.U[:, :20], base.factors.U[:, :20]) <= 1e-4
