@@ -135,12 +135,21 @@ __global__ void maxabs_kernel(const T* __restrict__ x, int64_t rows,
   double m = 0.0;
   int bad = 0;
   const int64_t total = rows * cols;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-       idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = idx % rows, j = idx / rows;
-    const double v = (double)x[i + j * ld];
-    if (!isfinite(v)) bad = 1;
-    else m = fmax(m, fabs(v));
+  if (ld == rows) {  // contiguous: a flat scan (no 64-bit index division)
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+      const double v = (double)x[idx];
+      if (!isfinite(v)) bad = 1;
+      else m = fmax(m, fabs(v));
+    }
+  } else {
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+         idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t i = idx % rows, j = idx / rows;
+      const double v = (double)x[i + j * ld];
+      if (!isfinite(v)) bad = 1;
+      else m = fmax(m, fabs(v));
+    }
   }
   m = warp_max(m);
   bad = __reduce_or_sync(0xffffffffu, bad);
