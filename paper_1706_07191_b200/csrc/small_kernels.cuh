@@ -240,6 +240,15 @@ template <typename T>
 __global__ void scale_cols_kernel(T* __restrict__ X, int64_t rows, int64_t cols,
                                   int64_t ld, const T* __restrict__ sign) {
   const int64_t total = rows * cols;
+  if (total < (1ll << 31)) {  // 32-bit index arithmetic (cheaper division)
+    const uint32_t r32 = (uint32_t)rows;
+    for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < (uint32_t)total;
+         idx += gridDim.x * blockDim.x) {
+      const uint32_t i = idx % r32, j = idx / r32;
+      X[i + (int64_t)j * ld] *= sign[j];
+    }
+    return;
+  }
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
        idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = idx % rows, j = idx / rows;
@@ -252,6 +261,15 @@ __global__ void copy2d_kernel(const TS* __restrict__ src, int64_t rows,
                               int64_t cols, int64_t lds, TD* __restrict__ dst,
                               int64_t ldd) {
   const int64_t total = rows * cols;
+  if (total < (1ll << 31)) {  // 32-bit index arithmetic (cheaper division)
+    const uint32_t r32 = (uint32_t)rows;
+    for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < (uint32_t)total;
+         idx += gridDim.x * blockDim.x) {
+      const uint32_t i = idx % r32, j = idx / r32;
+      dst[i + (int64_t)j * ldd] = (TD)src[i + (int64_t)j * lds];
+    }
+    return;
+  }
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
        idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = idx % rows, j = idx / rows;
