@@ -251,7 +251,8 @@ __global__ void jacobi_finish_kernel(const double* __restrict__ G, int64_t ldg,
     perm[rank] = c;
   }
   __syncthreads();
-  for (int j = warp; j < ncol; j += nwarps) {
+  // the permuted copies are split over the CTAs (every CTA ranks redundantly)
+  for (int j = blockIdx.x * nwarps + warp; j < ncol; j += gridDim.x * nwarps) {
     const int c = perm[j];
     const double s = nrm[c];
     if (lane == 0 && sv != nullptr) sv[j] = s;

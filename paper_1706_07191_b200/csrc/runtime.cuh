@@ -389,8 +389,9 @@ inline void jacobi_finish(Ctx& c, const double* G, int nrow, int ncol, int64_t l
                           const double* V, int64_t ldv, double* sv, double* Uout,
                           int64_t ldu, double* Vout, int64_t ldvo) {
   const size_t smem = (size_t)ncol * (sizeof(double) + sizeof(int));
-  jacobi_finish_kernel<<<1, 1024, smem, c.stream>>>(G, ldg, nrow, ncol, V, ldv, sv,
-                                                    Uout, ldu, Vout, ldvo);
+  const int ctas = std::max(1, std::min(c.num_sms / 4, ncol / 32));
+  jacobi_finish_kernel<<<ctas, 1024, smem, c.stream>>>(G, ldg, nrow, ncol, V, ldv, sv, Uout,
+                                                       ldu, Vout, ldvo);
   BRSVD_CHECK_LAUNCH();
 }
 
