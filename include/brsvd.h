@@ -129,6 +129,20 @@ BRSVD_API int brsvd_rsvd_blocked(brsvd_ctx* ctx, const void* A, int64_t m, int64
                                  void* U, void* sigma, void* Vt, int out_where,
                                  brsvd_stats* stats);
 
+/* Range finder (block_range_finder, rsvd.py:150-185): the sample of
+ * brsvd_rsvd_blocked (global power iteration when nblocks <= 1, else the
+ * per-block iteration over the column blocks) and its orthonormal basis,
+ * with no core projection.  Q is m x l column-major (out_where); it spans the
+ * range of the sample like the reference's tsqr Q (a different orthonormal
+ * basis of the same span).  stats: words_read / block_reads of the sample
+ * pass(es), detected_rank, the exact overflow peak.  Other arguments as
+ * brsvd_rsvd_blocked. */
+BRSVD_API int brsvd_range_finder(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n,
+                                 int64_t lda, int dtype, int layout, int a_where, int k,
+                                 int p, int q, const void* omega, int omega_where,
+                                 uint64_t seed, const int64_t* col_bounds, int nblocks,
+                                 void* Q, int out_where, brsvd_stats* stats);
+
 /* One pass over A -- the A-streaming product of the power iteration and of
  * the core projection (a @ omega, a.T @ y: rsvd.py:94-102, :140):
  *   trans = 0:  C (m x l) = A X,    X (n x l)

@@ -48,6 +48,87 @@ def rsvd_case(name, a, k, p, q, seed):
     print(f"rsvd_{name}: sigma[:3]={f.sigma[:3]} relerr={err:.3e} ranks={ranks}")
 
 
+def naive_ooc_case():
+    """rsvd_naive_ooc (rsvd.py:218-284), global power iteration over column
+    blocks; the global sketch is stored too (the per-block slices
+    gaussian_matrix(|J|, l, seed, 0, row_offset=j0) are its rows,
+    kernels.py:98-118)."""
+    import tempfile
+    a = lowrank(150, 100, 5, 14, noise=1e-6)
+    with tempfile.TemporaryDirectory() as d:
+        st = ref.MatrixStore.from_array(os.path.join(d, "a.oocm"), a)
+        cfg = ref.SketchConfig(target_rank=5, power_exponent=2, partitions=5,
+                               master_seed=3)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            fn, stats = ref.rsvd_naive_ooc(st, cfg)
+        st.close()
+    omega = ref.gaussian_matrix(100, 15, 3, stream_index=0)
+    np.savez_compressed(os.path.join(OUT, "naive_ooc.npz"), a=a, U=fn.U,
+                        sigma=fn.sigma, Vt=fn.Vt, passes=float(stats.full_passes),
+                        omega=omega, k=5, p=10, q=2, s=5, seed=3,
+                        block_reads=stats.block_reads)
+
+
+def range_finder_case():
+    """block_range_finder (rsvd.py:150-185): Q of the per-block sample."""
+    import tempfile
+    a = lowrank(240, 180, 6, 17, noise=1e-3)
+    out = {}
+    for s, q in ((1, 1), (3, 2)):
+        with tempfile.TemporaryDirectory() as d:
+            st = ref.MatrixStore.from_array(os.path.join(d, "a.oocm"), a)
+            cfg = ref.SketchConfig(target_rank=6, oversampling=6, power_exponent=q,
+                                   partitions=s, master_seed=11)
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                Q, plan = ref.block_range_finder(st, cfg)
+            out[f"Q_s{s}_q{q}"] = Q
+            out[f"blocks_s{s}_q{q}"] = np.array(list(plan), dtype=np.int64)
+            out[f"block_reads_s{s}_q{q}"] = st.stats.block_reads
+            st.close()
+    omega = ref.gaussian_matrix(180, 12, 11, stream_index=0)
+    np.savez_compressed(os.path.join(OUT, "range_finder.npz"), a=a, omega=omega, **out)
+    print("range_finder", sorted(out))
+
+
+def rpca_video_case():
+    """BASELINE config 5 structure at 1/10 of its columns and 1/10 of its
+    pixels: a 96 x 80 video of 2000 frames (7680 x 2000 fp64, rank-3
+    background + moving 8 x 8 foreground), k = p = 10, q = 1, tol 1e-7, run
+    by the reference's ialm_rpca (rpca.py:168-213).  M is regenerated from
+    oracle/ref_cpu.video_matrix (numpy default_rng; pinned by its checksum
+    here); L and S are stored as probes (L @ P, P2^T L, norms) and the exact
+    support and values of S."""
+    from oracle import ref_cpu
+    M = ref_cpu.video_matrix(96, 80, 2000, seed=0)
+    cfg = ref.RpcaConfig(target_rank=10, oversampling=10, power_exponent=1, tol=1e-7)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = ref.ialm_rpca(M, cfg)
+    omega = ref.gaussian_matrix(M.shape[1], 20, 0, stream_index=0)
+    rng = np.random.default_rng(99)
+    P = rng.standard_normal((M.shape[1], 4))
+    P2 = rng.standard_normal((M.shape[0], 4))
+    L, S = res.L, res.S
+    nz = np.flatnonzero(S.ravel(order="F"))
+    np.savez_compressed(os.path.join(OUT, "rpca_video_slice.npz"),
+                        width=96, height=80, frames=2000, seed=0, k=10, p=10, q=1,
+                        tol=1e-7, M_sum=M.sum(), M_sq=float((M * M).sum()), omega=omega,
+                        P=P, P2=P2, LP=L @ P, P2L=P2.T @ L,
+                        L_fro=np.linalg.norm(L), S_fro=np.linalg.norm(S),
+                        S_idx=nz.astype(np.int64), S_val=S.ravel(order="F")[nz],
+                        iterations=res.iterations,
+                        residuals=np.array(res.residual_history),
+                        mus=np.array([h["mu"] for h in res.history]),
+                        converged=res.converged)
+    print("rpca video slice iterations", res.iterations, "S nnz", nz.size)
+
+
+CASES = {"naive_ooc": naive_ooc_case, "range_finder": range_finder_case,
+         "rpca_video": rpca_video_case}
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     # rsvd_incore cases (rsvd.py:126-141)
@@ -94,19 +175,7 @@ def main():
     np.savez_compressed(os.path.join(OUT, "small_svd.npz"), b=b, W=f.U, sigma=f.sigma,
                         Vt=f.Vt, b_def=bd, sigma_def=fd.sigma)
 
-    # naive out-of-core, global power iteration (rsvd.py:218-284)
     import tempfile
-    a = lowrank(150, 100, 5, 14, noise=1e-6)
-    with tempfile.TemporaryDirectory() as d:
-        st = ref.MatrixStore.from_array(os.path.join(d, "a.oocm"), a)
-        cfg = ref.SketchConfig(target_rank=5, power_exponent=2, partitions=5,
-                               master_seed=3)
-        with warnings.catch_warnings():
-            warnings.simplefilter("ignore")
-            fn, stats = ref.rsvd_naive_ooc(st, cfg)
-        st.close()
-    np.savez_compressed(os.path.join(OUT, "naive_ooc.npz"), a=a, U=fn.U,
-                        sigma=fn.sigma, Vt=fn.Vt, passes=float(stats.full_passes))
 
     # paper-literal two-pass BRSVD: brsvd_run with s > 1, q >= 1 computes the
     # per-block power iteration (rsvd.py:150-215)
@@ -171,4 +240,11 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+    if len(sys.argv) > 1:       # e.g. make_golden.py rpca_video naive_ooc
+        for name in sys.argv[1:]:
+            CASES[name]()
+    else:
+        main()
+        for fn in CASES.values():
+            fn()

@@ -185,6 +185,20 @@ def randomized_svd_paper(a, k, p, q, blocks, seed=0, omega=None):
     return dict(U=u, sigma=s, Vt=vt, rank_y=rank_y, rank_b=rank_b)
 
 
+def range_basis_paper(a, k, p, q, blocks, seed=0, omega=None):
+    """block_range_finder (rsvd.py:150-185): Q = tsqr of the per-block sample
+    sum_J (A_J A_J^T)^q A_J Omega_J (rsvd.py:169-175, kernels.py:167-170)."""
+    l = k + p
+    y = None
+    for j0, j1 in [(int(j0), int(j1)) for j0, j1 in blocks]:
+        om = (omega[j0:j1] if omega is not None
+              else normal_sketch(j1 - j0, l, seed, 0, j0, a.dtype))
+        contrib = power_sample(a[:, j0:j1], om, q)
+        y = contrib if y is None else y + contrib
+    q_basis, _, rank = orthonormal_range(y)
+    return q_basis, rank
+
+
 def frob_rel_error(a, u, sigma, vt):
     """||A - U diag(s) Vt||_F / ||A||_F (rsvd.py:396-432, in-memory branch)."""
     d = a - (u * sigma) @ vt
@@ -273,3 +287,20 @@ def lowrank_plus_noise(m, n, rank, noise, seed, dtype=np.float64):
     if noise:
         a += noise * rng.standard_normal((m, n))
     return a.astype(dtype, copy=False)
+
+
+def video_matrix(width, height, frames, seed=0, block=8, dtype=np.float64):
+    """Synthetic surveillance video (BASELINE config 5 structure): each column
+    is a width x height frame (column-major pixels), M = rank-3 nonnegative
+    background + a block x block foreground square of value 1.0 that moves
+    3 pixels per frame (wrapping), ~block^2 / (width*height) density."""
+    rng = np.random.default_rng(seed)
+    m = width * height
+    M = rng.random((m, 3)) @ rng.random((3, frames))
+    d = np.arange(block)
+    y0 = height // 3
+    for j in range(frames):
+        x0 = (3 * j) % (width - block)
+        rows = ((x0 + d)[:, None] * height + y0 + d[None, :]).ravel()
+        M[rows, j] = 1.0
+    return M.astype(dtype, copy=False)

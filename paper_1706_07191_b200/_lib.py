@@ -28,7 +28,7 @@ EXPORTED = (
     "brsvd_chol_basis", "brsvd_apply", "brsvd_normalize", "brsvd_colmax",
     "brsvd_scale_cols", "brsvd_rsvd_stream", "brsvd_residual", "brsvd_rsvd_blocked",
     "brsvd_rsvd_stream_blocked", "brsvd_ialm_blocked", "brsvd_sketch_product_scaled",
-    "brsvd_absmax",
+    "brsvd_absmax", "brsvd_range_finder",
 )
 
 
@@ -85,6 +85,9 @@ def _declare(lib):
     lib.brsvd_rsvd_blocked.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, c_int,
                                        c_int, c_int, vp, c_int, u64, vp, c_int, vp, vp, vp,
                                        c_int, ctypes.POINTER(BrsvdStats)]
+    lib.brsvd_range_finder.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, c_int,
+                                       c_int, c_int, vp, c_int, u64, vp, c_int, vp, c_int,
+                                       ctypes.POINTER(BrsvdStats)]
     lib.brsvd_tsqr.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, vp, vp,
                                ctypes.POINTER(i32)]
     lib.brsvd_small_svd.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, vp, vp, vp,
@@ -213,7 +216,15 @@ def check(rc):
     if rc == ERR_OVERFLOW:
         raise FloatingPointError(msg)
     if rc == ERR_BUDGET:
-        raise ValueError(msg)
+        from .store import BudgetError
+        # the C side reports "... minimum_feasible=<bytes>" (store.py:42-47)
+        need = None
+        if "minimum_feasible=" in msg:
+            try:
+                need = int(msg.rsplit("minimum_feasible=", 1)[1].split()[0])
+            except ValueError:
+                need = None
+        raise BudgetError(msg, need)
     if rc in (ERR_CUDA, ERR_NCCL):
         raise RuntimeError(f"CUDA error: {msg}")
     raise ValueError(msg)

@@ -229,11 +229,38 @@ int brsvd_rsvd(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda,
                             omega_where, seed, nullptr, 0, U, sigma, Vt, out_where, stats);
 }
 
+namespace {
+int rsvd_entry(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda, int dtype,
+               int layout, int a_where, int k, int p, int q, const void* omega,
+               int omega_where, uint64_t seed, const int64_t* col_bounds, int nblocks, void* U,
+               void* sigma, void* Vt, int out_where, brsvd_stats* stats, bool range_only);
+}
+
 int brsvd_rsvd_blocked(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda,
                        int dtype, int layout, int a_where, int k, int p, int q,
                        const void* omega, int omega_where, uint64_t seed,
                        const int64_t* col_bounds, int nblocks, void* U, void* sigma,
                        void* Vt, int out_where, brsvd_stats* stats) {
+  return rsvd_entry(ctx, A, m, n, lda, dtype, layout, a_where, k, p, q, omega, omega_where,
+                    seed, col_bounds, nblocks, U, sigma, Vt, out_where, stats, false);
+}
+
+int brsvd_range_finder(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda,
+                       int dtype, int layout, int a_where, int k, int p, int q,
+                       const void* omega, int omega_where, uint64_t seed,
+                       const int64_t* col_bounds, int nblocks, void* Q, int out_where,
+                       brsvd_stats* stats) {
+  return rsvd_entry(ctx, A, m, n, lda, dtype, layout, a_where, k, p, q, omega, omega_where,
+                    seed, col_bounds, nblocks, Q, nullptr, nullptr, out_where, stats, true);
+}
+
+}  // extern "C"
+
+namespace {
+int rsvd_entry(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda, int dtype,
+               int layout, int a_where, int k, int p, int q, const void* omega,
+               int omega_where, uint64_t seed, const int64_t* col_bounds, int nblocks, void* U,
+               void* sigma, void* Vt, int out_where, brsvd_stats* stats, bool range_only) {
   return guarded([&] {
     if (nblocks > 0) {
       BRSVD_REQUIRE(col_bounds != nullptr, kErrArg, "col_bounds is NULL");
@@ -274,6 +301,8 @@ int brsvd_rsvd_blocked(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int6
       feed.ldh = lda;
     }
     InView ov(c, omega, n, l, n, es, omega ? omega_where : BRSVD_DEVICE);
+    BRSVD_REQUIRE(U != nullptr && (range_only || (sigma != nullptr && Vt != nullptr)),
+                  kErrArg, "output pointer is NULL");
     OutView uo(c, U, (size_t)m * l * es, out_where);
     OutView so(c, sigma, (size_t)l * es, out_where);
     OutView vo(c, Vt, (size_t)n * l * es, out_where);
@@ -282,12 +311,12 @@ int brsvd_rsvd_blocked(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int6
       info = rsvd_device<double>(c, (const double*)aptr, m, n, ald, row_major, k, p, q,
                                  (const double*)ov.dptr, seed, (double*)uo.dptr,
                                  (double*)so.dptr, (double*)vo.dptr,
-                                 on_host ? &feed : nullptr, col_bounds, nblocks);
+                                 on_host ? &feed : nullptr, col_bounds, nblocks, range_only);
     } else {
       info = rsvd_device<float>(c, (const float*)aptr, m, n, ald, row_major, k, p, q,
                                 (const float*)ov.dptr, seed, (float*)uo.dptr,
                                 (float*)so.dptr, (float*)vo.dptr, on_host ? &feed : nullptr,
-                                col_bounds, nblocks);
+                                col_bounds, nblocks, range_only);
     }
     uo.flush();
     so.flush();
@@ -297,6 +326,9 @@ int brsvd_rsvd_blocked(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int6
     return (int)kOk;
   });
 }
+}  // namespace
+
+extern "C" {
 
 int brsvd_rsvd_stream(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda,
                       int dtype, int layout, int k, int p, int q, const void* omega,

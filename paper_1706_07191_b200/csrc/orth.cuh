@@ -83,9 +83,11 @@ CholInfo chol_basis(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double sh
 // never breaks down) when l fits the Cholesky kernel, else the regularised
 // Gram-eigen basis X S E Lam^-1/2 (eigenvalues floored at tau*lam_0).  No
 // host synchronisation either way.
+// Tout (optional, l x l fp64): the transform actually applied, Xout = X Tout
+// (for fp32 data its fp32-rounded entries), for the exact overflow guard.
 template <typename T>
 void normalize_sketch(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, T* Xout,
-                      int64_t ldo) {
+                      int64_t ldo, double* Tout = nullptr) {
   DBuf<double> Tm(c, (size_t)l * l);
   if (l <= kCholMaxL) {
     chol_basis<T>(c, X, r, l, ldx, 16.0 * l * 2.220446049250313e-16, Tm.p, false);
@@ -97,6 +99,36 @@ void normalize_sketch(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, T* Xout
     BRSVD_CHECK_LAUNCH();
   }
   apply_basis<T>(c, X, r, l, ldx, Tm.p, l, l, Xout, ldo);
+  if (Tout) {
+    if (sizeof(T) == 4 && tc_gemm_supported<T>(c, X, ldx, r, l, l)) {
+      DBuf<float> T32(c, (size_t)l * l);
+      copy2d_kernel<double, float><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(
+          Tm.p, l, l, l, T32.p, l);
+      copy2d_kernel<float, double><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(
+          T32.p, l, l, l, Tout, l);
+      BRSVD_CHECK_LAUNCH();
+    } else {
+      BRSVD_CUDA(cudaMemcpyAsync(Tout, Tm.p, sizeof(double) * l * l,
+                                 cudaMemcpyDeviceToDevice, c.stream));
+    }
+  }
+}
+
+// Inverse of an upper-triangular l x l matrix (column-major, fp64), one
+// column per thread by back substitution.  Serves the exact overflow guard
+// only (rare path), so it is written for clarity, not speed.
+__global__ void triu_inverse_kernel(const double* __restrict__ T, int l,
+                                    double* __restrict__ X) {
+  for (int j = threadIdx.x; j < l; j += blockDim.x) {
+    double* x = X + (int64_t)j * l;
+    for (int i = l - 1; i > j; --i) x[i] = 0.0;
+    for (int i = j; i >= 0; --i) {
+      double v = i == j ? 1.0 : 0.0;
+      for (int k = i + 1; k <= j; ++k) v -= T[(int64_t)k * l + i] * x[k];
+      const double d = T[(int64_t)i * l + i];
+      x[i] = d != 0.0 ? v / d : 0.0;
+    }
+  }
 }
 
 // Block projection X <- X - Qb (Qb^T X), applied twice ("twice is enough").

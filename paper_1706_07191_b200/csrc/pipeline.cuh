@@ -177,11 +177,40 @@ void paper_sketch(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool ro
   }
 }
 
+// Exact overflow guard of the global power iteration (rsvd.py:84-91).  The
+// sample the reference tests is Y_ref = (A A^T)^q A Omega; ours is
+// Y_q = Y_ref C with C = prod_i (z_i T_i) (z_i the power-of-two scale of
+// A^T Y, T_i the upper-triangular Cholesky basis change actually applied),
+// so max |Y_ref| = max |Y_q C^-1|, formed in fp64 (its entries may exceed
+// the data's range -- that is what the guard detects).  Ts holds the q
+// transforms (l x l each); returns the exact peak.
+template <typename T>
+double unnormalised_peak(Ctx& c, const T* Yq, int64_t m, int l, int q, const double* Ts,
+                         const double* zfac) {
+  DBuf<double> P(c, (size_t)l * l), Ti(c, (size_t)l * l), Pn(c, (size_t)l * l);
+  eye_kernel<double><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(P.p, l);
+  BRSVD_CHECK_LAUNCH();
+  double scale = 1.0;
+  for (int it = 0; it < q; ++it) {   // P <- T_it^-1 P  (C^-1 = T_q^-1 ... T_1^-1)
+    triu_inverse_kernel<<<1, 512, 0, c.stream>>>(Ts + (size_t)it * l * l, l, Ti.p);
+    BRSVD_CHECK_LAUNCH();
+    gemm_nn_cm<double, double, double>(c, l, l, l, Ti.p, l, P.p, l, Pn.p, l);
+    std::swap(P.p, Pn.p);
+    scale *= zfac[it];
+  }
+  DBuf<double> Yr(c, (size_t)m * l);
+  gemm_nn_cm<T, double, double>(c, m, l, l, Yq, m, P.p, l, Yr.p, m);
+  const MaxAbs pk = maxabs<double>(c, Yr.p, m, l, m);
+  return pk.nonfinite ? INFINITY : pk.peak / scale;
+}
+
+// range_only: stop after the orthonormal basis of the sample (block_range_finder,
+// rsvd.py:150-185); Q (m x l) is written to U.
 template <typename T>
 RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
                      bool row_major, int k, int p, int q, const T* omega,
                      uint64_t seed, T* U, T* sigma, T* V, const HostFeed* feed = nullptr,
-                     const int64_t* blocks = nullptr, int nblk = 0) {
+                     const int64_t* blocks = nullptr, int nblk = 0, bool range_only = false) {
   const bool paper = blocks != nullptr && nblk > 1 && q > 0;
   const int l = k + p;
   RsvdInfo info;
@@ -247,10 +276,17 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
     // ordinary magnitude, else recompute A^T Y scaled (A is resident now)
     if (e < -40 || e > 40) z_ready = false;
   }
+  // the applied basis changes, for the exact overflow guard (Cholesky route)
+  const bool track = !paper && q > 0 && l <= kCholMaxL;
+  DBuf<double> Ts;
+  std::vector<double> zfac;
+  if (track) Ts.alloc(c, (size_t)q * l * l);
   for (int it = 0; it < (paper ? 0 : q); ++it) {
-    if (!(it == 0 && z_ready))
+    const bool fused = it == 0 && z_ready;   // the feed's A^T Y ran unscaled
+    if (!fused)
       big_tn<T>(c, A, m, n, lda, row_major, Y.p, m, l, Z.p, n, acol.p, zscale);
-    normalize_sketch<T>(c, Z.p, n, l, n, Zn.p, n);
+    zfac.push_back(fused ? 1.0 : zscale);
+    normalize_sketch<T>(c, Z.p, n, l, n, Zn.p, n, track ? Ts.p + (size_t)it * l * l : nullptr);
     big_nn<T>(c, A, m, n, lda, row_major, Zn.p, n, l, Y.p, m, arow.p);
   }
   info.words_read += (int64_t)(2 * q + 1) * m * n;
@@ -272,7 +308,19 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
   const int ns = sizeof(T) == 8 ? 2 : 1;
   DBuf<T> Qw(c, (size_t)m * l);
   info.rank_y = orth_full<T>(c, Y.p, m, l, m, Qw.p, seed ^ 0x7153ull, ns);
-  Y.release();
+  const double lim = 0.01 * finfo_max<T>();
+  if (range_only) {
+    BRSVD_CUDA(cudaMemcpyAsync(U, Qw.p, sizeof(T) * m * l, cudaMemcpyDeviceToDevice,
+                               c.stream));
+    ev.rec(2, c.stream);
+    double peak = info.max_abs_y0;            // paper mode: the sample is unnormalised
+    if (track) peak = unnormalised_peak<T>(c, Y.p, m, l, q, Ts.p, zfac.data());
+    info.log10_peak = peak > 0.0 ? std::log10(peak) : -400.0;
+    info.overflow = !(peak <= lim);
+    info.ms_sketch = ev.ms(0, 1);
+    info.ms_orth = ev.ms(1, 2);
+    return info;
+  }
   const T* Qop = Qw.p;
   ev.rec(2, c.stream);
   DBuf<T> Bt(c, (size_t)n * l);
@@ -296,16 +344,33 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
   info.ms_orth = ev.ms(1, 2);
   info.ms_core = ev.ms(2, 3);
   info.ms_svd = ev.ms(3, 4);
-  // Overflow guard of the unnormalised reference iteration: its sample is
-  // (A A^T)^q A Omega, whose peak grows like max|A Omega| * sigma_1^(2q).
-  const double lim = std::log10(0.01 * finfo_max<T>());
-  // (the paper-mode sample is already the powered, unnormalised one)
+  // Overflow guard of the unnormalised reference iteration (rsvd.py:84-91):
+  // its sample (A A^T)^q A Omega peaks below max|A Omega| sqrt(m) s_1^(2q).
+  // Far below the threshold that bound settles it; near or above it the
+  // peak is formed exactly (unnormalised_peak).  The paper-mode sample is the
+  // unnormalised one already, so its max is exact.
+  const double loglim = std::log10(lim);
   const int qg = paper ? 0 : q;
   if (info.max_abs_y0 > 0.0 && s0 > 0.0)
     info.log10_peak = std::log10(info.max_abs_y0) + 2.0 * qg * std::log10(s0);
   else
     info.log10_peak = info.max_abs_y0 > 0.0 ? std::log10(info.max_abs_y0) : -400.0;
-  info.overflow = nonfinite || !std::isfinite(s0) || info.log10_peak > lim;
+  bool over = nonfinite || !std::isfinite(s0);
+  if (!over && qg > 0) {
+    const double bound = info.log10_peak + 0.5 * std::log10((double)m) + 0.05;
+    if (bound > loglim) {
+      if (track) {
+        const double peak = unnormalised_peak<T>(c, Y.p, m, l, q, Ts.p, zfac.data());
+        info.log10_peak = peak > 0.0 ? std::log10(peak) : -400.0;
+        over = !(peak <= lim);
+      } else {
+        over = info.log10_peak > loglim;   // l > kCholMaxL: estimate
+      }
+    }
+  } else if (!over) {
+    over = info.max_abs_y0 > lim;
+  }
+  info.overflow = over;
   return info;
 }
 

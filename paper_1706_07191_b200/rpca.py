@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _lib
 from ._arrays import DeviceMatrix, HostMatrix, is_torch, torch_stream_ptr
-from .store import MatrixStore, plan_blocks
+from .store import BudgetError, MatrixStore, plan_blocks
 
 __all__ = ["RpcaConfig", "RpcaResult", "shrink", "spectral_norm_estimate",
            "ialm_rpca"]
@@ -115,6 +115,23 @@ def spectral_norm_estimate(source, seed=0, tol=1e-10, max_iterations=100):
     return float(out.value)
 
 
+# device residency of the IALM loop: M, S, Y, W and the L/S outputs, plus slack
+_IALM_RESIDENT_COPIES = 6
+
+
+def _require_device_room(payload_bytes):
+    """The IALM iterates stay in HBM (no host-streamed IALM is built): a store
+    whose iterates cannot be held on the device raises BudgetError up front
+    (store.py:42-47 semantics) instead of failing inside the loop."""
+    import torch
+    free, _ = torch.cuda.mem_get_info(_lib.context().device)
+    need = _IALM_RESIDENT_COPIES * int(payload_bytes)
+    if need > free:
+        raise BudgetError(
+            f"IALM iterates of a {payload_bytes} B matrix need ~{need} B of device memory, "
+            f"{free} B free (host-streamed IALM is not implemented)", need)
+
+
 def ialm_rpca(m_input, cfg, omega=None):
     """Inexact-ALM robust PCA with a randomized inner SVD (rpca.py:153-213).
 
@@ -140,6 +157,7 @@ def ialm_rpca(m_input, cfg, omega=None):
             plan = plan_blocks(m_input.n, m_input.m, l_, m_input.element_size,
                                memory_budget_bytes=budget)
             blocks = list(plan)
+        _require_device_room(m_input.payload_bytes)
         m_input = m_input.read_full()
     device = is_torch(m_input)
     mat = DeviceMatrix(m_input) if device else HostMatrix(m_input, "M")

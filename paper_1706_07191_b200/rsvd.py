@@ -7,14 +7,13 @@ B = Q^T A, one-sided Jacobi SVD of the core, canonical signs.  This is the
 semantics of ``rsvd_incore`` (rsvd.py:126-141) and ``rsvd_naive_ooc``
 (rsvd.py:218-284) at any partition count.
 
-Intentional deltas:
-  * ``brsvd_run`` with s > 1 and q >= 1 computes the global power iteration
-    (same answer as s = 1), not the per-block iteration of rsvd.py:169-175.
-  * A store is read across the boundary once per decomposition when it fits
-    in HBM, so ``stats.full_passes`` is 1 (reference: 2 for brsvd_run,
-    2(q+1) for rsvd_naive_ooc).  With a ``memory_budget_bytes`` below the
-    payload, the budget's column blocks are streamed from host memory and a
-    decomposition costs q + 2 passes.
+Store entry points:
+  * ``brsvd_run`` computes the reference's per-block power iteration
+    (rsvd.py:169-175) by default; ``mode="global"`` gives the global one.
+  * ``PassStats`` follows the reference's accounting (2 passes for
+    brsvd_run, 2(q+1) for rsvd_naive_ooc); ``stats.boundary_words_read`` is
+    the true host->device traffic: one pass when the store fits in HBM, the
+    streamed passes (2 paper / q + 2 global) when it exceeds the budget.
 """
 
 import ctypes
@@ -185,7 +184,19 @@ def rsvd_incore(a, cfg, omega=None):
 
 
 def _load_store_to_device(store, plan):
-    """Read every block of the plan once and land it in HBM (column-major)."""
+    """Read every block of the plan once and land it in HBM (column-major).
+
+    The store's own read counters are left unchanged: the entry points book
+    the reference's per-algorithm accounting and the boundary traffic
+    themselves (_account)."""
+    w0, b0 = store.stats.words_read, store.stats.block_reads
+    try:
+        return _land_blocks(store, plan)
+    finally:
+        store.stats.words_read, store.stats.block_reads = w0, b0
+
+
+def _land_blocks(store, plan):
     import torch
     tdt = torch.float64 if store.dtype == np.float64 else torch.float32
     ctx = _lib.context()
@@ -249,9 +260,82 @@ def _store_payload(store):
 _MODES = ("global", "paper")
 
 
-def _run_store(store, cfg, memory_budget_bytes, stage_names, mode="global"):
-    if mode not in _MODES:
-        raise ValueError(f"mode must be one of {_MODES}, got {mode!r}")
+def run_range(a, cfg, omega=None, blocks=None, warn=True):
+    """Sketch + orthonormal basis only (C ABI ``brsvd_range_finder``): Q (m x l)
+    spanning the sample -- global power iteration, or the per-block iteration
+    over ``blocks`` (the paper's block_range_finder, rsvd.py:150-185).
+    Returns (Q, stats); Q matches ``a``'s kind (numpy host / torch device)."""
+    device = is_torch(a)
+    mat = DeviceMatrix(a) if device else HostMatrix(a)
+    m, n = mat.shape
+    cfg.validate(m, n)
+    k, p, q = cfg.target_rank, cfg.oversampling, cfg.power_exponent
+    l = k + p
+    lib = _lib.load_library()
+    if device:
+        import torch
+        ctx = _lib.context(mat.device)
+        ctx.set_stream(torch_stream_ptr(mat.t))
+        Q = torch.empty((l, m), dtype=mat.t.dtype, device=mat.t.device)
+        npdt = np.float64 if mat.t.dtype == torch.float64 else np.float32
+        qptr, where = ctypes.c_void_p(Q.data_ptr()), _lib.DEVICE
+    else:
+        ctx = _lib.context()
+        npdt = mat.dtype
+        Q = np.empty((m, l), dtype=npdt, order="F")
+        qptr, where = ctypes.c_void_p(Q.ctypes.data), _lib.HOST
+    keep, optr, owhere = _omega_arg(omega, n, l, npdt, device)
+    bounds, nblk = None, 0
+    if blocks is not None and len(blocks) > 1:
+        edges = [int(blocks[0][0])] + [int(j1) for _, j1 in blocks]
+        bounds = (ctypes.c_int64 * len(edges))(*edges)
+        nblk = len(edges) - 1
+    stats = _lib.BrsvdStats()
+    rc = lib.brsvd_range_finder(ctx.handle, mat.ptr, m, n, mat.ld, mat.code, mat.layout,
+                                where, k, p, q, optr, owhere,
+                                ctypes.c_uint64(int(cfg.master_seed) & (2 ** 64 - 1)),
+                                bounds, nblk, qptr, where, ctypes.byref(stats))
+    del keep
+    _lib.check(rc)
+    if warn:
+        warn_rank(stats.detected_rank, l)
+    return (Q.t() if device else Q), stats
+
+
+def _host_factors(f):
+    return SvdFactors(U=f.U.cpu().numpy(), sigma=f.sigma.cpu().numpy(),
+                      Vt=f.Vt.cpu().numpy(), target_rank=f.target_rank,
+                      effective_l=f.effective_l)
+
+
+def _account(stats, store, plan, cfg, algorithm, seconds, boundary_passes):
+    """Pass accounting of the reference's algorithm (store.py:50-79 counters as
+    rsvd.py:150-284 increments them): the passes the algorithm makes over A --
+    on the B200 they are HBM passes when the store fits the device -- plus the
+    true host->device traffic in ``stats.boundary_words_read``."""
+    m, n, l, q, s = store.m, store.n, cfg.l, cfg.power_exponent, plan.s
+    mn = m * n
+    if algorithm in ("paper", "global_brsvd"):   # brsvd_run: sketch pass + core pass
+        stages = (("sketch", mn, 2 * mn * l * (1 + 2 * q)), ("orthonormalize", 0, 2 * m * l * l),
+                  ("form_core", mn, 2 * mn * l), ("svd", 0, 2 * n * l * l + 2 * m * l * l))
+        reads = 2 * s
+    elif algorithm == "naive":        # rsvd_naive_ooc: 2(q + 1) passes
+        stages = (("sketch", mn, 2 * mn * l), ("power", 2 * q * mn, 4 * mn * l * q),
+                  ("orthonormalize", 0, 2 * m * l * l), ("form_core", mn, 2 * mn * l),
+                  ("svd", 0, 2 * n * l * l + 2 * m * l * l))
+        reads = 2 * (q + 1) * s
+    else:                             # block_range_finder: one sketch pass
+        stages = (("sketch", mn, 2 * mn * l * (1 + 2 * q)), ("orthonormalize", 0, 2 * m * l * l))
+        reads = s
+    for name, words, flops in stages:
+        stats.words_read += words
+        stats.flop_estimate += flops
+        stats.log_stage(name, words, 0, seconds.get(name, 0.0))
+    stats.block_reads += reads
+    stats.boundary_words_read += int(boundary_passes * mn)
+
+
+def _run_store(store, cfg, memory_budget_bytes, algorithm, omega=None):
     m, n = store.m, store.n
     cfg.validate(m, n)
     s = None if cfg.partitions == "auto" else int(cfg.partitions)
@@ -259,87 +343,93 @@ def _run_store(store, cfg, memory_budget_bytes, stage_names, mode="global"):
                        memory_budget_bytes=memory_budget_bytes, s=s)
     store.reset_stats()
     stats = store.stats
+    paper = algorithm == "paper"
     if memory_budget_bytes is not None and store.payload_bytes > memory_budget_bytes:
-        # Out of core: the budget's column blocks are the streamed panels;
-        # q + 2 passes over the store cross the boundary.
-        t0 = time.perf_counter()
+        # Out of core: the budget's column blocks are the streamed panels.
+        # paper: each block's power iteration runs while it is resident, then
+        # the core pass (2 passes over PCIe); global: q + 2 passes.
         run = run_rsvd_stream(_store_payload(store), cfg, panel=plan.n_prime, nbuf=3,
-                              block_power=(mode == "paper"))
+                              omega=omega, block_power=paper)
         st = run.stats
-        passes = st.words_read // (m * n)
-        stats.words_read += int(st.words_read)
-        stats.block_reads += int(passes * plan.s)
-        stats.flop_estimate += int(st.flop_estimate)
-        seconds = {"sketch": st.seconds_sketch, "power": 0.0,
-                   "orthonormalize": st.seconds_orthonormalize,
-                   "form_core": st.seconds_form_core, "svd": st.seconds_svd}
-        words = {"sketch": (passes - 1) * m * n, "form_core": m * n}
-        for name in stage_names:
-            stats.log_stage(name, words.get(name, 0), 0, seconds[name])
-        del t0
-        return run.factors, stats, plan
-    t0 = time.perf_counter()
-    a_dev = _load_store_to_device(store, plan)
-    load_s = time.perf_counter() - t0
-    run = run_rsvd(a_dev, cfg, blocks=list(plan) if mode == "paper" else None)
-    f = run.factors
-    factors = SvdFactors(U=f.U.cpu().numpy(), sigma=f.sigma.cpu().numpy(),
-                         Vt=f.Vt.cpu().numpy(), target_rank=f.target_rank,
-                         effective_l=f.effective_l)
-    st = run.stats
-    l, q = cfg.l, cfg.power_exponent
-    stats.flop_estimate += int(st.flop_estimate)
-    seconds = {
-        "sketch": load_s + st.seconds_sketch,
-        "power": 0.0,
-        "orthonormalize": st.seconds_orthonormalize,
-        "form_core": st.seconds_form_core,
-        "svd": st.seconds_svd,
-    }
-    for name in stage_names:
-        stats.log_stage(name, m * n if name == "sketch" else 0, 0, seconds[name])
-    del a_dev
+        crossed = st.words_read // (m * n)
+        factors = run.factors
+    else:
+        t0 = time.perf_counter()
+        a_dev = _load_store_to_device(store, plan)
+        load_s = time.perf_counter() - t0
+        run = run_rsvd(a_dev, cfg, omega=omega, blocks=list(plan) if paper else None)
+        st = run.stats
+        st.seconds_sketch += load_s
+        crossed = 1
+        factors = _host_factors(run.factors)
+        del a_dev
+    seconds = {"sketch": st.seconds_sketch, "orthonormalize": st.seconds_orthonormalize,
+               "form_core": st.seconds_form_core, "svd": st.seconds_svd}
+    _account(stats, store, plan, cfg, algorithm, seconds, crossed)
     return factors, stats, plan
 
 
-def brsvd_run(store, cfg, memory_budget_bytes=None, mode="global"):
+def brsvd_run(store, cfg, memory_budget_bytes=None, mode="paper", omega=None):
     """Block randomized SVD of a stored matrix (rsvd.py:188-215) on the GPU.
 
-    Returns (factors, stats).  A store that fits the budget is streamed across
-    the boundary once into HBM and every pass runs from HBM; a larger one is
-    streamed in the budget's column blocks.
+    Returns (factors, stats) with the reference's pass accounting
+    (``stats.full_passes == 2``, ``block_reads == 2 s``; rsvd.py:188-193);
+    ``stats.boundary_words_read`` is what actually crossed PCIe -- one pass
+    when the store fits the budget (it is landed in HBM once and every pass
+    runs from HBM), two when its column blocks are streamed.
 
-    mode="global" (default): global power iteration, the semantics of
-    rsvd_incore / rsvd_naive_ooc (q + 2 passes when streamed).
-    mode="paper": the reference's per-block power iteration (Alg. 2,
-    rsvd.py:169-175) -- each column block's (A_J A_J^T)^q A_J Omega_J summed --
-    two passes for any q; identical to "global" when s = 1 or q = 0.
+    mode="paper" (default, the reference's semantics): the per-block power
+    iteration of block_range_finder (rsvd.py:169-175) -- each column block's
+    (A_J A_J^T)^q A_J Omega_J, unnormalised, summed; identical to the global
+    iteration when s = 1 or q = 0.  mode="global": the global power iteration
+    of rsvd_incore / rsvd_naive_ooc at any s (q + 2 passes when streamed).
+    ``omega`` (n x l) injects the sketch, e.g. the reference's
+    gaussian_matrix(n, l, seed, 0), whose rows are the per-block slices the
+    reference draws (kernels.py:98-118, row_offset).
     """
+    if mode not in _MODES:
+        raise ValueError(f"mode must be one of {_MODES}, got {mode!r}")
     factors, stats, _ = _run_store(store, cfg, memory_budget_bytes,
-                                   ("sketch", "orthonormalize", "form_core", "svd"), mode)
+                                   "paper" if mode == "paper" else "global_brsvd", omega)
     return factors, stats
 
 
-def rsvd_naive_ooc(store, cfg, memory_budget_bytes=None):
+def rsvd_naive_ooc(store, cfg, memory_budget_bytes=None, omega=None):
     """Global-power-iteration SVD of a stored matrix (rsvd.py:218-284).
 
-    Same GPU computation as brsvd_run; kept for API parity.
+    Reference pass accounting: 2(q + 1) passes, 2(q + 1) s block reads
+    (tests/test_rsvd.py:173-179); ``stats.boundary_words_read`` is the true
+    PCIe traffic (1 pass from HBM, q + 2 when streamed).
     """
-    factors, stats, _ = _run_store(store, cfg, memory_budget_bytes,
-                                   ("sketch", "power", "orthonormalize", "form_core",
-                                    "svd"))
+    factors, stats, _ = _run_store(store, cfg, memory_budget_bytes, "naive", omega)
     return factors, stats
 
 
-def block_range_finder(store, cfg, memory_budget_bytes=None, plan=None, mode="global"):
-    """Orthonormal basis of the sample range (rsvd.py:150-185); returns (Q, plan).
+def block_range_finder(store, cfg, memory_budget_bytes=None, plan=None, omega=None):
+    """Orthonormal range basis from one blocked pass over the store
+    (rsvd.py:150-185); returns (Q, plan).
 
-    Q is the left factor U of the GPU decomposition: an orthonormal basis of
-    range(Y) (U = Q W with W orthogonal).  ``mode`` as in brsvd_run.
+    The sample is the reference's per-block power iteration over the plan's
+    column blocks, then its orthonormal basis (no core projection).  Q spans
+    the same range as the reference's tsqr Q (a different orthonormal basis of
+    that span).  Like the reference, it adds its pass to ``store.stats``
+    without resetting it.  The store is landed in HBM once (one pass across
+    the boundary, as the reference reads it once).
     """
-    factors, stats, plan_used = _run_store(store, cfg, memory_budget_bytes,
-                                           ("sketch", "orthonormalize"), mode)
-    return factors.U, (plan if plan is not None else plan_used)
+    m, n = store.m, store.n
+    cfg.validate(m, n)
+    if plan is None:
+        s = None if cfg.partitions == "auto" else int(cfg.partitions)
+        plan = plan_blocks(n, m, cfg.l, store.element_size,
+                           memory_budget_bytes=memory_budget_bytes, s=s)
+    t0 = time.perf_counter()
+    a_dev = _load_store_to_device(store, plan)
+    Q, st = run_range(a_dev, cfg, omega=omega, blocks=list(plan))
+    Qh = Q.cpu().numpy()
+    seconds = {"sketch": time.perf_counter() - t0 - st.seconds_orthonormalize,
+               "orthonormalize": st.seconds_orthonormalize}
+    _account(store.stats, store, plan, cfg, "range", seconds, 1)
+    return np.asfortranarray(Qh), plan
 
 
 def _residual_sums(a_dev, U_col, sig, Vt, j0=0):

@@ -269,29 +269,33 @@ def test_streamed_out_of_core_matches_in_core(order, dtype):
 
 
 def test_brsvd_run_budget_streams_store(tmp_path):
-    """brsvd_run with a budget below the payload streams the plan's blocks."""
+    """brsvd_run with a budget below the payload streams the plan's blocks;
+    PassStats keeps the reference's accounting (rsvd.py:188-193: two passes,
+    2 s block reads) and boundary_words_read the true PCIe traffic."""
     from paper_1706_07191_b200 import MatrixStore, SketchConfig, brsvd_run, rsvd_incore
     a = ref_cpu.lowrank_plus_noise(2000, 600, 8, 1e-4, seed=22)
     st = MatrixStore.from_array(tmp_path / "a.oocm", a)
     cfg = SketchConfig(target_rank=8, oversampling=8, power_exponent=1)
-    f, stats = brsvd_run(st, cfg, memory_budget_bytes=4 * 1024 * 1024)
-    assert stats.full_passes == 3                              # q + 2
-    assert stats.block_reads > 3
+    f, stats = brsvd_run(st, cfg, memory_budget_bytes=4 * 1024 * 1024, mode="global")
+    assert stats.full_passes == 2 and stats.words_read == 2 * a.size
+    assert stats.boundary_words_read == 3 * a.size              # q + 2 streamed passes
     assert [e["stage"] for e in stats.stage_log] == ["sketch", "orthonormalize",
                                                      "form_core", "svd"]
     g = rsvd_incore(a, cfg)
     np.testing.assert_allclose(f.sigma[:8], g.sigma[:8], rtol=1e-10)
-    f2, stats2 = brsvd_run(st, cfg)                            # fits: read once
-    assert stats2.full_passes == 1
+    f2, stats2 = brsvd_run(st, cfg, mode="global")             # fits: landed once
+    assert stats2.full_passes == 2 and stats2.block_reads == 2
+    assert stats2.boundary_words_read == a.size
     np.testing.assert_allclose(f2.sigma[:8], g.sigma[:8], rtol=1e-10)
     st.close()
 
 
 @pytest.mark.parametrize("name", ["brsvd_paper_s4_q2.npz", "brsvd_paper_s3_q1.npz"])
-def test_brsvd_run_paper_mode_matches_reference(name, tmp_path):
-    """mode="paper": the reference's per-block power iteration of brsvd_run
-    (rsvd.py:150-215), in HBM and streamed in the plan's column blocks (two
-    passes for any q, like the reference)."""
+def test_brsvd_run_matches_reference_through_public_api(name, tmp_path):
+    """brsvd_run (default: the reference's per-block power iteration,
+    rsvd.py:150-215) with the reference's Omega injected reproduces the
+    reference's factors, in HBM and streamed in the plan's column blocks, with
+    the reference's pass law (full_passes == 2, block_reads == 2 s)."""
     from paper_1706_07191_b200 import MatrixStore, SketchConfig, brsvd_run
     g = load(name)
     a = g["a"]
@@ -299,26 +303,75 @@ def test_brsvd_run_paper_mode_matches_reference(name, tmp_path):
     st = MatrixStore.from_array(tmp_path / "a.oocm", a)
     cfg = SketchConfig(target_rank=k, oversampling=p, power_exponent=q, partitions=s,
                        master_seed=int(g["seed"]))
-    with warnings.catch_warnings():
-        warnings.simplefilter("ignore")
-        # the reference's sketch: rows of the same global Omega per block
-        f, stats = brsvd_run(st, cfg, mode="paper")
-        budget = 3 * a.shape[0] * (k + p) * 8 + 10 * a.shape[0] * 8
-        fs, ss = brsvd_run(st, cfg, memory_budget_bytes=budget, mode="paper")
-    st.close()
-    ref_sig = g["sigma"][:k]
-    # the GPU sketch generator is not numpy's ziggurat stream: the in-HBM and
-    # streamed runs agree with each other, and (below) with the reference
-    # when its Omega is injected
-    np.testing.assert_allclose(fs.sigma[:k], f.sigma[:k], rtol=1e-10)
-    assert ss.full_passes == 2                    # rsvd.py:188-193
-    # same-semantics check: both are the per-block approximation, which for
-    # these inputs differs from the global one by far more than the tolerance
-    glob, _ = brsvd_run(MatrixStore.from_array(tmp_path / "b.oocm", a), cfg)
+    budget = 3 * a.shape[0] * (k + p) * 8 + 10 * a.shape[0] * 8
+    for bud in (None, budget):
+        f, stats = brsvd_run(st, cfg, memory_budget_bytes=bud, omega=g["omega"])
+        assert stats.full_passes == 2
+        if bud is None:
+            assert stats.block_reads == 2 * len(g["blocks"])
+        np.testing.assert_allclose(f.sigma[:k], g["sigma"][:k], rtol=1e-10)
+        assert sin_theta(f.U[:, :k], g["U"][:, :k]) <= 1e-8
+        assert sin_theta(f.Vt[:k].T, g["Vt"][:k].T) <= 1e-8
+        np.testing.assert_allclose(f.U[:, :k], g["U"][:, :k], atol=1e-8)
+    assert stats.boundary_words_read == 2 * a.size           # streamed: 2 passes
+    # the per-block sample is a different approximation from the global one
+    glob, _ = brsvd_run(st, cfg, mode="global", omega=g["omega"])
     gap = np.max(np.abs(glob.sigma[:k] - f.sigma[:k]) / f.sigma[:k])
     assert gap > (1e-6 if "s4_q2" in name else 0.0)
-    # the approximation quality matches the reference's per-block result
-    assert np.max(np.abs(f.sigma[:k] - ref_sig) / ref_sig) < 0.05
+    st.close()
+
+
+def test_naive_ooc_matches_reference_golden(tmp_path):
+    """rsvd_naive_ooc (rsvd.py:218-284) with the reference's sketch: global
+    power iteration, factors to 1e-10, pass law 2(q + 1) (test_rsvd.py:173-179)."""
+    from paper_1706_07191_b200 import MatrixStore, SketchConfig, rsvd_naive_ooc
+    g = load("naive_ooc.npz")
+    a = g["a"]
+    k, p, q, s = int(g["k"]), int(g["p"]), int(g["q"]), int(g["s"])
+    st = MatrixStore.from_array(tmp_path / "a.oocm", a)
+    cfg = SketchConfig(target_rank=k, oversampling=p, power_exponent=q, partitions=s,
+                       master_seed=int(g["seed"]))
+    f, stats = rsvd_naive_ooc(st, cfg, omega=g["omega"])
+    st.close()
+    assert stats.full_passes == float(g["passes"]) == 2 * (q + 1)
+    assert stats.block_reads == int(g["block_reads"])
+    assert [e["stage"] for e in stats.stage_log] == ["sketch", "power", "orthonormalize",
+                                                     "form_core", "svd"]
+    np.testing.assert_allclose(f.sigma[:k], g["sigma"][:k], rtol=1e-10)
+    assert sin_theta(f.U[:, :k], g["U"][:, :k]) <= 1e-8
+    np.testing.assert_allclose(f.U[:, :k], g["U"][:, :k], atol=1e-8)
+
+
+@pytest.mark.parametrize("s,q", [(1, 1), (3, 2)])
+def test_block_range_finder_matches_reference(s, q, tmp_path):
+    """block_range_finder (rsvd.py:150-185): the orthonormal basis of the
+    per-block sample, no core projection; one pass added to the store's
+    counters (not reset)."""
+    from paper_1706_07191_b200 import MatrixStore, SketchConfig, block_range_finder
+    g = load("range_finder.npz")
+    a = g["a"]
+    st = MatrixStore.from_array(tmp_path / "a.oocm", a)
+    cfg = SketchConfig(target_rank=6, oversampling=6, power_exponent=q, partitions=s,
+                       master_seed=11)
+    Q, plan = block_range_finder(st, cfg, omega=g["omega"])
+    assert [tuple(b) for b in plan] == [tuple(b) for b in g[f"blocks_s{s}_q{q}"]]
+    assert st.stats.block_reads == int(g[f"block_reads_s{s}_q{q}"]) == s
+    assert st.stats.full_passes == 1
+    Qr = g[f"Q_s{s}_q{q}"]
+    assert Q.shape == Qr.shape and np.linalg.norm(Q.T @ Q - np.eye(12)) <= 1e-12
+    # the leading columns span the same nested subspaces as the reference's
+    # Householder Q (both orthonormalise in column order) ...
+    assert np.linalg.norm(Q[:, :6] @ Q[:, :6].T - Qr[:, :6] @ Qr[:, :6].T) <= 1e-10
+    # ... and Q captures the reference's sample (range residual as in the
+    # reference's tests/test_kernels.py:100-108)
+    y = None
+    for j0, j1 in plan:
+        c = ref_cpu.power_sample(a[:, j0:j1], g["omega"][j0:j1], q)
+        y = c if y is None else y + c
+    assert np.linalg.norm(y - Q @ (Q.T @ y)) <= 1e-12 * np.linalg.norm(y)
+    block_range_finder(st, cfg, omega=g["omega"])
+    assert st.stats.full_passes == 2                        # accumulates like the reference
+    st.close()
 
 
 def test_paper_mode_with_reference_omega_is_bit_close():
@@ -381,3 +434,32 @@ def test_streamed_scale_invariance(order, scale):
     np.testing.assert_allclose(st.factors.sigma[:20] / scale, base.factors.sigma[:20],
                                rtol=1e-5)
     assert sin_theta(st.factors.U[:, :20], base.factors.U[:, :20]) <= 1e-4
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("q", [0, 1, 2])
+@pytest.mark.parametrize("frac", [0.99, 1.01])
+def test_overflow_guard_is_exact_at_threshold(dtype, q, frac):
+    """_check_overflow (rsvd.py:84-91): the reference raises iff its
+    unnormalised sample peaks above 0.01 * finfo.max.  Inputs scaled to put
+    that peak at 0.99x and 1.01x of the threshold: the GPU path (which
+    never forms the unnormalised sample in the data's precision) decides
+    exactly as the reference does."""
+    from paper_1706_07191_b200 import SketchConfig, rsvd_incore
+    a = ref_cpu.lowrank_plus_noise(300, 200, 5, 1e-2, seed=8)
+    omega = ref_cpu.normal_sketch(200, 10, 0, dtype=np.float64)
+    peak1 = float(np.max(np.abs(ref_cpu.power_sample(a, omega, q))))
+    lim = 0.01 * float(np.finfo(dtype).max)
+    c = (frac * lim / peak1) ** (1.0 / (2 * q + 1))
+    ac = (a * c).astype(dtype)
+    om = omega.astype(dtype)
+    with np.errstate(over="ignore", invalid="ignore"):
+        _, ref_fires = ref_cpu.overflow_peak(ref_cpu.power_sample(ac, om, q))
+    assert ref_fires == (frac > 1.0)
+    cfg = SketchConfig(target_rank=5, oversampling=5, power_exponent=q)
+    if ref_fires:
+        with pytest.raises(FloatingPointError):
+            rsvd_incore(ac, cfg, omega=om)
+    else:
+        f = rsvd_incore(ac, cfg, omega=om)
+        assert np.isfinite(f.sigma).all()
