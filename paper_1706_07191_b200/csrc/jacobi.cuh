@@ -217,7 +217,7 @@ __global__ void jacobi_block_kernel(JacobiArgs<R> a) {
 // Column norms of G*V, descending rank sort, permuted outputs.
 //   sv[j]  = ||(G V)_{:, perm j}||,  Vout[:, j] = V[:, perm j],
 //   Uout[:, j] = (G V)[:, perm j] / sv[j]   (zero column if sv == 0).
-// One CTA; ncol <= 1024.
+// Any grid: the columns are split over the CTAs' warps (grid-stride).
 __global__ void jacobi_finish_kernel(const double* __restrict__ G, int64_t ldg,
                                      int nrow, int ncol,
                                      const double* __restrict__ V, int64_t ldv,

@@ -345,11 +345,37 @@ inline int orth_full_f32(Ctx& c, const float* X, int64_t r, int l, int64_t ldx, 
   return std::min(ci.rank_ref, k1);
 }
 
+// fp64 data near the ends of the exponent range: Cholesky QR and the Jacobi
+// sweeps square magnitudes, which the reference's Householder QR and gesdd
+// never do (LAPACK's norms are scale-safe), so such operands are brought to
+// unit order by a power of two first (exact; Q and the rank cut are
+// scale-invariant).  Returns e with X * 2^-e of unit order, or 0 when X is
+// within 2^+-400 already (fp32 data: Grams are fp64, always 0).
+template <typename T>
+int unit_exponent(Ctx& c, const T* X, int64_t rows, int cols, int64_t ld) {
+  if (sizeof(T) != 8 || rows * cols == 0) return 0;
+  const MaxAbs pk = maxabs<T>(c, X, rows, cols, ld);
+  if (pk.nonfinite || !(pk.peak > 0.0)) return 0;
+  int e;
+  std::frexp(pk.peak, &e);
+  return (e > 400 || e < -400) ? e : 0;
+}
+
 template <typename T>
 int orth_full(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, T* Q, uint64_t seed,
-              int ns_iters) {
-  if (sizeof(T) == 8)
+              int ns_iters, bool scale_check = true) {
+  if (sizeof(T) == 8) {
+    const int e = scale_check ? unit_exponent<T>(c, X, r, l, ldx) : 0;
+    if (e != 0) {
+      DBuf<T> Xs(c, (size_t)r * l);
+      scale_copy_kernel<T><<<grid_for(r * l), 256, 0, c.stream>>>(X, r, l, ldx, Xs.p, r,
+                                                                  std::ldexp(1.0, -e));
+      BRSVD_CHECK_LAUNCH();
+      return orth_full_f64<T>(c, Xs.p, r, l, r, reinterpret_cast<double*>(Q), seed,
+                              ns_iters);
+    }
     return orth_full_f64<T>(c, X, r, l, ldx, reinterpret_cast<double*>(Q), seed, ns_iters);
+  }
   if (l <= kCholMaxL)
     return orth_full_f32(c, reinterpret_cast<const float*>(X), r, l, ldx,
                          reinterpret_cast<float*>(Q), seed);
@@ -367,9 +393,20 @@ int orth_full(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, T* Q, uint64_t 
 template <typename T>
 int small_svd_device(Ctx& c, const T* Bt, int64_t n, int l, int64_t ldb, double* W,
                      double* sigma, T* Vout, int64_t ldv, int ns_iters) {
+  // fp64 B near the range limits: factor 2^-e B, scale sigma back at the end
+  const int e = unit_exponent<T>(c, Bt, n, l, ldb);
+  DBuf<T> Bs;
+  if (e != 0) {
+    Bs.alloc(c, (size_t)n * l);
+    scale_copy_kernel<T><<<grid_for(n * l), 256, 0, c.stream>>>(Bt, n, l, ldb, Bs.p, n,
+                                                                std::ldexp(1.0, -e));
+    BRSVD_CHECK_LAUNCH();
+    Bt = Bs.p;
+    ldb = n;
+  }
   DBuf<T> Qb(c, (size_t)n * l);
   DBuf<double> M(c, (size_t)l * l), Vj(c, (size_t)l * l), Zj(c, (size_t)l * l);
-  const int rank = orth_full<T>(c, Bt, n, l, ldb, Qb.p, 0x5eedb5ull, ns_iters);
+  const int rank = orth_full<T>(c, Bt, n, l, ldb, Qb.p, 0x5eedb5ull, ns_iters, false);
   // M = Bt^T Qb = R^T
   gemm_tn_cm<T, T, double>(c, l, l, n, Bt, ldb, Qb.p, n, M.p, l);
   if (l > 64) {
@@ -409,6 +446,11 @@ int small_svd_device(Ctx& c, const T* Bt, int64_t n, int l, int64_t ldb, double*
       W, l, l, l, sigma, 16.0 * l * 2.220446049250313e-16);
   BRSVD_CHECK_LAUNCH();
   apply_basis<T>(c, Qb.p, n, l, n, Zj.p, l, l, Vout, ldv);
+  if (e != 0) {
+    scale_copy_kernel<double><<<1, 256, 0, c.stream>>>(sigma, l, 1, l, sigma, l,
+                                                       std::ldexp(1.0, e));
+    BRSVD_CHECK_LAUNCH();
+  }
   return rank;
 }
 

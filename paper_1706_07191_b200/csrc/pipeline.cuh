@@ -291,8 +291,10 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
   }
   info.words_read += (int64_t)(2 * q + 1) * m * n;
   info.block_reads += 2 * q + 1;
+  double ypeak = p0.peak;   // max |Y| of the sample being orthonormalised
   if (q > 0) {
     const MaxAbs pq = maxabs<T>(c, Y.p, m, l, m);
+    ypeak = pq.peak;
     if (std::getenv("BRSVD_DEBUG"))
       std::fprintf(stderr, "[brsvd] sample peak %.3e -> after %d passes %.3e%s\n", p0.peak, q,
                    pq.peak, pq.nonfinite ? " (non-finite)" : "");
@@ -307,7 +309,8 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
   Z.release();
   const int ns = sizeof(T) == 8 ? 2 : 1;
   DBuf<T> Qw(c, (size_t)m * l);
-  info.rank_y = orth_full<T>(c, Y.p, m, l, m, Qw.p, seed ^ 0x7153ull, ns);
+  const bool y_extreme = ypeak > 0x1p400 || (ypeak > 0.0 && ypeak < 0x1p-400);
+  info.rank_y = orth_full<T>(c, Y.p, m, l, m, Qw.p, seed ^ 0x7153ull, ns, y_extreme);
   const double lim = 0.01 * finfo_max<T>();
   if (range_only) {
     BRSVD_CUDA(cudaMemcpyAsync(U, Qw.p, sizeof(T) * m * l, cudaMemcpyDeviceToDevice,

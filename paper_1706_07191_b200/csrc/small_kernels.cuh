@@ -203,7 +203,8 @@ __global__ void colmax_kernel(const T* __restrict__ U, int64_t rows, int64_t ldu
   double best = -1.0;
   int64_t bidx = 0;
   for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
-    const double v = fabs((double)U[i + j * ldu]);
+    double v = fabs((double)U[i + j * ldu]);
+    if (v != v) v = INFINITY;   // NaN propagates as non-finite (overflow guard)
     if (v > best) { best = v; bidx = i; }
   }
 #pragma unroll
@@ -274,6 +275,18 @@ __global__ void copy2d_kernel(const TS* __restrict__ src, int64_t rows,
        idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = idx % rows, j = idx / rows;
     dst[i + j * ldd] = (TD)src[i + j * lds];
+  }
+}
+
+// dst = src * s (s a power of two: exact), any leading dimensions.
+template <typename T>
+__global__ void scale_copy_kernel(const T* __restrict__ src, int64_t rows, int64_t cols,
+                                  int64_t lds, T* __restrict__ dst, int64_t ldd, double s) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % rows, j = idx / rows;
+    dst[i + j * ldd] = (T)((double)src[i + j * lds] * s);
   }
 }
 

@@ -355,6 +355,8 @@ def rsvd_sharded(A_local, cfg, row_offset, m_total, comm=None, ops=None, omega=N
                    signs)
     s0 = float(sigma[0])
     lim = math.log10(0.01 * np.finfo(npdt).max)
+    if not math.isfinite(s0):   # as pipeline.cuh: a non-finite sigma_1 is an overflow
+        raise FloatingPointError("sample matrix is not finite; the overflow guard fires")
     log_peak = (math.log10(peak0) + 2 * q * math.log10(s0)) if peak0 > 0 and s0 > 0 else -400.0
     if log_peak > lim:
         raise FloatingPointError("sample matrix magnitude exceeds the overflow guard")
