@@ -6,7 +6,7 @@
 // column-major; the tall-skinny operands are column-major.
 #pragma once
 #include "runtime.cuh"
-#include "tc_gemm.cuh"
+#include "tc_stream.cuh"
 #include "skinny64.cuh"
 
 namespace brsvd {
@@ -22,9 +22,10 @@ void big_nn(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool row_majo
             const T* X, int64_t ldx, int l, T* Y, int64_t ldy, const float* amax = nullptr) {
   ProfScope ps(c, 2.0 * m * n * l, (double)m * n * sizeof(T));
   if (tc_gemm_supported<T>(c, A, lda, m, n, l)) {
-    tc_gemm_launch<T>(c, A, m, n, lda, row_major, /*trans=*/false, X, ldx, l, Y, ldy, 0,
-                      nullptr, amax);
-    return;
+    if constexpr (sizeof(T) == 4) {
+      tc_product(c, A, m, n, lda, row_major, /*trans=*/false, X, ldx, l, Y, ldy, amax);
+      return;
+    }
   }
   if constexpr (sizeof(T) == 8) {
     if (skinny_f64(c, row_major, reinterpret_cast<const double*>(A), m, n, lda,
@@ -42,9 +43,11 @@ void big_tn(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool row_majo
             double out_scale = 1.0) {
   ProfScope ps(c, 2.0 * m * n * l, (double)m * n * sizeof(T));
   if (tc_gemm_supported<T>(c, A, lda, m, n, l)) {
-    tc_gemm_launch<T>(c, A, m, n, lda, row_major, /*trans=*/true, Yin, ldy, l, Z, ldz, 0,
-                      nullptr, amax, nullptr, out_scale);
-    return;
+    if constexpr (sizeof(T) == 4) {
+      tc_product(c, A, m, n, lda, row_major, /*trans=*/true, Yin, ldy, l, Z, ldz, amax,
+                 out_scale);
+      return;
+    }
   }
   if constexpr (sizeof(T) == 8) {
     if (skinny_f64(c, !row_major, reinterpret_cast<const double*>(A), n, m, lda,

@@ -22,8 +22,8 @@ void apply_basis(Ctx& c, const T* X, int64_t r, int li, int64_t ldx, const doubl
     copy2d_kernel<double, float><<<grid_for((int64_t)li * lo), 256, 0, c.stream>>>(
         Tm, li, lo, ldt, T32.p, li);
     BRSVD_CHECK_LAUNCH();
-    tc_gemm_launch<float>(c, reinterpret_cast<const float*>(X), r, li, ldx, false, false,
-                          T32.p, li, lo, reinterpret_cast<float*>(Out), ldo);
+    tc_product(c, reinterpret_cast<const float*>(X), r, li, ldx, false, false, T32.p, li, lo,
+               reinterpret_cast<float*>(Out), ldo);
     return;
   }
   gemm_nn_cm<T, double, T>(c, r, lo, li, X, ldx, Tm, ldt, Out, ldo);

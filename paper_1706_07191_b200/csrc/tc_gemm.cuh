@@ -564,10 +564,14 @@ __global__ void tc_split_kernel(const float* __restrict__ X, int64_t K, int n_sr
 
 // One CTA per (padded) column: max |X[:, j]| by a block reduction, then the
 // scaled fp16 (hi, lo) split of that column -- one pass, no atomics.
+// qw > 0: column j is written to row perm(j) of the planes, the layout of the
+// CTA-pair kernel (tc_stream.cuh): thirds of 2 qw columns, each split in two
+// qw-column halves, one per CTA; CTA r's halves stacked in rows
+// [r npad/2, (r+1) npad/2).
 __global__ void __launch_bounds__(512)
     tc_split16_col_kernel(const float* __restrict__ X, int64_t K, int n_src, int64_t ldx,
                           int64_t kld, uint16_t* __restrict__ hi, uint16_t* __restrict__ lo,
-                          float* __restrict__ col_inv) {
+                          float* __restrict__ col_inv, int qw = 0) {
   __shared__ unsigned red[16];
   const int j = blockIdx.x;
   const float* col = X + (int64_t)j * ldx;
@@ -599,8 +603,11 @@ __global__ void __launch_bounds__(512)
   __syncthreads();
   const float sc = real ? h16_scale(__uint_as_float(red[0])) : 1.f;
   if (threadIdx.x == 0) col_inv[j] = 1.f / sc;
-  uint16_t* h = hi + (int64_t)j * kld;
-  uint16_t* l = lo + (int64_t)j * kld;
+  const int prow = qw > 0 ? ((j % (2 * qw)) / qw) * (int)(gridDim.x / 2) + (j / (2 * qw)) * qw +
+                               j % qw
+                         : j;
+  uint16_t* h = hi + (int64_t)prow * kld;
+  uint16_t* l = lo + (int64_t)prow * kld;
   if (vec) {
     const float4* c4 = reinterpret_cast<const float4*>(col);
     for (int64_t q = threadIdx.x; q < kld / 4; q += blockDim.x) {
