@@ -299,6 +299,32 @@ BRSVD_API int brsvd_normalize(brsvd_ctx* ctx, const void* Z, int64_t n, int64_t 
 BRSVD_API int brsvd_colmax(brsvd_ctx* ctx, const void* U, int64_t r, int64_t l, int64_t ldu,
                            int dtype, int64_t row_offset, double* vals, int64_t* idx);
 
+/* brsvd_colmax plus the signed entry at each argmax, in one host array of
+ * 3*l doubles: [max |u_ij| (l) | global row index (l) | u at that index (l)]
+ * -- the per-rank candidates of _fix_signs (rsvd.py:105-115) for one
+ * all-gather, with no per-column device reads. */
+BRSVD_API int brsvd_colmax_entries(brsvd_ctx* ctx, const void* U, int64_t r, int64_t l,
+                                   int64_t ldu, int dtype, int64_t row_offset, double* out);
+
+/* One streamed pass over a host-resident row shard A (m x n, `layout`,
+ * pinned host memory for overlapped DMA), the per-rank unit of the sharded
+ * out-of-core decomposition (rsvd_naive_ooc's passes, rsvd.py:218-284, rows
+ * split over ranks).  Row panels of `panel` rows go through `nbuf` device
+ * buffers on a copy stream; per panel A_i:
+ *   X != NULL (device n x l):  Y_i = A_i X    -> Y rows (device m x l)
+ *   Z != NULL (device n x l, fp64):  Z = sum_i A_i^T Y_i  (Y as formed, or
+ *                                    as given when X == NULL: B^T = A^T Q)
+ * pass_ms (optional): device time of the pass. */
+BRSVD_API int brsvd_stream_rows_pass(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n,
+                                     int64_t lda, int dtype, int layout, const void* X,
+                                     int64_t ldx, int64_t l, void* Y, int64_t ldy, double* Z,
+                                     int64_t ldz, int64_t panel, int nbuf, double* pass_ms);
+
+/* brsvd_normalize of an fp64 Z (the all-reduced sum of brsvd_stream_rows_pass)
+ * into a basis in `dtype` (fp32: taken to unit order by a power of two first). */
+BRSVD_API int brsvd_normalize_f64(brsvd_ctx* ctx, const double* Z, int64_t n, int64_t l,
+                                  int64_t ldz, int dtype, void* Zout, int64_t ldo);
+
 /* X[:, j] *= scale[j] (scale: host array of l doubles). */
 BRSVD_API int brsvd_scale_cols(brsvd_ctx* ctx, void* X, int64_t r, int64_t l, int64_t ldx,
                                int dtype, const double* scale);

@@ -28,7 +28,8 @@ EXPORTED = (
     "brsvd_chol_basis", "brsvd_apply", "brsvd_normalize", "brsvd_colmax",
     "brsvd_scale_cols", "brsvd_rsvd_stream", "brsvd_residual", "brsvd_rsvd_blocked",
     "brsvd_rsvd_stream_blocked", "brsvd_ialm_blocked", "brsvd_sketch_product_scaled",
-    "brsvd_absmax", "brsvd_range_finder",
+    "brsvd_absmax", "brsvd_range_finder", "brsvd_colmax_entries", "brsvd_stream_rows_pass",
+    "brsvd_normalize_f64",
 )
 
 
@@ -125,6 +126,10 @@ def _declare(lib):
     lib.brsvd_normalize.argtypes = [vp, vp, i64, i64, i64, c_int, vp, i64]
     lib.brsvd_colmax.argtypes = [vp, vp, i64, i64, i64, c_int, i64, vp, vp]
     lib.brsvd_scale_cols.argtypes = [vp, vp, i64, i64, i64, c_int, vp]
+    lib.brsvd_colmax_entries.argtypes = [vp, vp, i64, i64, i64, c_int, i64, vp]
+    lib.brsvd_stream_rows_pass.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, vp, i64, i64,
+                                           vp, i64, vp, i64, i64, c_int, ctypes.POINTER(dbl)]
+    lib.brsvd_normalize_f64.argtypes = [vp, vp, i64, i64, i64, c_int, vp, i64]
     lib.brsvd_profile_begin.argtypes = [vp]
     lib.brsvd_profile_end.argtypes = [vp, ctypes.POINTER(BrsvdProfile)]
     for name in EXPORTED:

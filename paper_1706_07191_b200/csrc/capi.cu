@@ -760,6 +760,76 @@ int brsvd_colmax(brsvd_ctx* ctx, const void* U, int64_t r, int64_t l, int64_t ld
   });
 }
 
+int brsvd_colmax_entries(brsvd_ctx* ctx, const void* U, int64_t r, int64_t l, int64_t ldu,
+                         int dtype, int64_t row_offset, double* out) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && U != nullptr && out != nullptr, kErrArg, "NULL argument");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    esize(dtype);
+    DBuf<double> dv(c, (size_t)3 * l);
+    double* vals = dv.p;
+    int64_t* idx = reinterpret_cast<int64_t*>(dv.p + l);
+    double* ent = dv.p + 2 * l;
+    if (dtype == BRSVD_F64)
+      colmax_kernel<double><<<(unsigned)l, 256, 0, c.stream>>>((const double*)U, r, ldu,
+                                                               row_offset, vals, idx, ent);
+    else
+      colmax_kernel<float><<<(unsigned)l, 256, 0, c.stream>>>((const float*)U, r, ldu,
+                                                              row_offset, vals, idx, ent);
+    BRSVD_CHECK_LAUNCH();
+    // out = [vals (l) | idx as doubles (l) | signed entries (l)], one copy
+    idx_to_double_kernel<<<grid_for(l), 256, 0, c.stream>>>(idx, l);
+    BRSVD_CHECK_LAUNCH();
+    BRSVD_CUDA(cudaMemcpyAsync(out, dv.p, sizeof(double) * 3 * l, cudaMemcpyDeviceToHost,
+                               c.stream));
+    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+    return (int)kOk;
+  });
+}
+
+int brsvd_stream_rows_pass(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, int64_t lda,
+                           int dtype, int layout, const void* X, int64_t ldx, int64_t l,
+                           void* Y, int64_t ldy, double* Z, int64_t ldz, int64_t panel,
+                           int nbuf, double* pass_ms) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && A != nullptr && Y != nullptr, kErrArg, "NULL argument");
+    BRSVD_REQUIRE(X != nullptr || Z != nullptr, kErrArg, "nothing to compute");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    esize(dtype);
+    BRSVD_REQUIRE(m >= 0 && n >= 1 && l >= 1 && l <= 1024, kErrShape, "bad shape");
+    BRSVD_REQUIRE(panel >= 1 && nbuf >= 1, kErrArg, "panel and nbuf must be positive");
+    const bool row_major = layout == BRSVD_ROW_MAJOR;
+    BRSVD_REQUIRE(lda >= (row_major ? n : m), kErrShape, "lda too small");
+    PassInfo pi;
+    if (dtype == BRSVD_F64)
+      pi = stream_rows_pass<double>(c, (const double*)A, m, n, lda, row_major,
+                                    (const double*)X, ldx, (int)l, (double*)Y, ldy, Z, ldz,
+                                    panel, nbuf);
+    else
+      pi = stream_rows_pass<float>(c, (const float*)A, m, n, lda, row_major, (const float*)X,
+                                   ldx, (int)l, (float*)Y, ldy, Z, ldz, panel, nbuf);
+    if (pass_ms) *pass_ms = pi.ms;
+    return (int)kOk;
+  });
+}
+
+int brsvd_normalize_f64(brsvd_ctx* ctx, const double* Z, int64_t n, int64_t l, int64_t ldz,
+                        int dtype, void* Zout, int64_t ldo) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && Z != nullptr && Zout != nullptr, kErrArg, "NULL argument");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    esize(dtype);
+    if (dtype == BRSVD_F64)
+      normalize_from_f64<double>(c, Z, n, (int)l, ldz, (double*)Zout, ldo);
+    else
+      normalize_from_f64<float>(c, Z, n, (int)l, ldz, (float*)Zout, ldo);
+    return (int)kOk;
+  });
+}
+
 int brsvd_scale_cols(brsvd_ctx* ctx, void* X, int64_t r, int64_t l, int64_t ldx, int dtype,
                      const double* scale) {
   return guarded([&] {

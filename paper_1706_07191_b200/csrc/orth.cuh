@@ -29,6 +29,22 @@ void apply_basis(Ctx& c, const T* X, int64_t r, int li, int64_t ldx, const doubl
   gemm_nn_cm<T, double, T>(c, r, lo, li, X, ldx, Tm, ldt, Out, ldo);
 }
 
+// fp64 data near the ends of the exponent range: Cholesky QR and the Jacobi
+// sweeps square magnitudes, which the reference's Householder QR and gesdd
+// never do (LAPACK's norms are scale-safe), so such operands are brought to
+// unit order by a power of two first (exact; Q and the rank cut are
+// scale-invariant).  Returns e with X * 2^-e of unit order, or 0 when X is
+// within 2^+-400 already (fp32 data: Grams are fp64, always 0).
+template <typename T>
+int unit_exponent(Ctx& c, const T* X, int64_t rows, int cols, int64_t ld) {
+  if (sizeof(T) != 8 || rows * cols == 0) return 0;
+  const MaxAbs pk = maxabs<T>(c, X, rows, cols, ld);
+  if (pk.nonfinite || !(pk.peak > 0.0)) return 0;
+  int e;
+  std::frexp(pk.peak, &e);
+  return (e > 400 || e < -400) ? e : 0;
+}
+
 constexpr int kCholMaxL = 320;  // cholinv_kernel shared-memory limit (~196 KB at 320)
 
 // Cholesky basis change of X (r x l): with s_j = 1/||x_j|| and the scaled Gram
@@ -87,15 +103,34 @@ CholInfo chol_basis(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double sh
 // (for fp32 data its fp32-rounded entries), for the exact overflow guard.
 template <typename T>
 void normalize_sketch(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, T* Xout,
-                      int64_t ldo, double* Tout = nullptr) {
+                      int64_t ldo, double* Tout = nullptr, bool scale_check = false) {
   DBuf<double> Tm(c, (size_t)l * l);
+  // fp64 X near the exponent limits (its Gram would overflow / underflow):
+  // factor 2^-e X and fold 2^-e into the basis change, X (2^-e T) = (2^-e X) T
+  const int e = scale_check ? unit_exponent<T>(c, X, r, l, ldx) : 0;
+  DBuf<T> Xs;
+  const T* Xf = X;
+  int64_t ldf = ldx;
+  if (e != 0) {
+    Xs.alloc(c, (size_t)r * l);
+    scale_copy_kernel<T><<<grid_for(r * l), 256, 0, c.stream>>>(X, r, l, ldx, Xs.p, r,
+                                                                std::ldexp(1.0, -e));
+    BRSVD_CHECK_LAUNCH();
+    Xf = Xs.p;
+    ldf = r;
+  }
   if (l <= kCholMaxL) {
-    chol_basis<T>(c, X, r, l, ldx, 16.0 * l * 2.220446049250313e-16, Tm.p, false);
+    chol_basis<T>(c, Xf, r, l, ldf, 16.0 * l * 2.220446049250313e-16, Tm.p, false);
   } else {
     DBuf<double> E(c, (size_t)l * l), lam(c, l), s(c, l);
-    gram_eig<T>(c, X, r, l, ldx, E.p, lam.p, s.p, kJacobiTolNormalize);
+    gram_eig<T>(c, Xf, r, l, ldf, E.p, lam.p, s.p, kJacobiTolNormalize);
     build_basis_kernel<<<1, 1024, 0, c.stream>>>(E.p, lam.p, s.p, l, orth_tau(r, l), 0,
                                                  Tm.p, nullptr);
+    BRSVD_CHECK_LAUNCH();
+  }
+  if (e != 0) {
+    scale_copy_kernel<double><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(
+        Tm.p, l, l, l, Tm.p, l, std::ldexp(1.0, -e));
     BRSVD_CHECK_LAUNCH();
   }
   apply_basis<T>(c, X, r, l, ldx, Tm.p, l, l, Xout, ldo);
@@ -345,21 +380,6 @@ inline int orth_full_f32(Ctx& c, const float* X, int64_t r, int l, int64_t ldx, 
   return std::min(ci.rank_ref, k1);
 }
 
-// fp64 data near the ends of the exponent range: Cholesky QR and the Jacobi
-// sweeps square magnitudes, which the reference's Householder QR and gesdd
-// never do (LAPACK's norms are scale-safe), so such operands are brought to
-// unit order by a power of two first (exact; Q and the rank cut are
-// scale-invariant).  Returns e with X * 2^-e of unit order, or 0 when X is
-// within 2^+-400 already (fp32 data: Grams are fp64, always 0).
-template <typename T>
-int unit_exponent(Ctx& c, const T* X, int64_t rows, int cols, int64_t ld) {
-  if (sizeof(T) != 8 || rows * cols == 0) return 0;
-  const MaxAbs pk = maxabs<T>(c, X, rows, cols, ld);
-  if (pk.nonfinite || !(pk.peak > 0.0)) return 0;
-  int e;
-  std::frexp(pk.peak, &e);
-  return (e > 400 || e < -400) ? e : 0;
-}
 
 template <typename T>
 int orth_full(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, T* Q, uint64_t seed,

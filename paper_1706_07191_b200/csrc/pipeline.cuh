@@ -276,6 +276,10 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
     // ordinary magnitude, else recompute A^T Y scaled (A is resident now)
     if (e < -40 || e > 40) z_ready = false;
   }
+  // fp64 inputs of extreme magnitude: A^T Y would square it in the Gram of the
+  // basis change, so that Gram is formed at unit scale (normalize_sketch)
+  const bool f64_extreme =
+      sizeof(T) == 8 && (p0.peak > 0x1p150 || (p0.peak > 0.0 && p0.peak < 0x1p-150));
   // the applied basis changes, for the exact overflow guard (Cholesky route)
   const bool track = !paper && q > 0 && l <= kCholMaxL;
   DBuf<double> Ts;
@@ -286,7 +290,8 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
     if (!fused)
       big_tn<T>(c, A, m, n, lda, row_major, Y.p, m, l, Z.p, n, acol.p, zscale);
     zfac.push_back(fused ? 1.0 : zscale);
-    normalize_sketch<T>(c, Z.p, n, l, n, Zn.p, n, track ? Ts.p + (size_t)it * l * l : nullptr);
+    normalize_sketch<T>(c, Z.p, n, l, n, Zn.p, n, track ? Ts.p + (size_t)it * l * l : nullptr,
+                        f64_extreme);
     big_nn<T>(c, A, m, n, lda, row_major, Zn.p, n, l, Y.p, m, arow.p);
   }
   info.words_read += (int64_t)(2 * q + 1) * m * n;

@@ -198,7 +198,7 @@ __global__ void colsign_kernel(const T* __restrict__ U, int64_t rows,
 template <typename T>
 __global__ void colmax_kernel(const T* __restrict__ U, int64_t rows, int64_t ldu,
                               int64_t row_offset, double* __restrict__ vals,
-                              int64_t* __restrict__ idx) {
+                              int64_t* __restrict__ idx, double* __restrict__ entry = nullptr) {
   const int j = blockIdx.x;
   double best = -1.0;
   int64_t bidx = 0;
@@ -223,6 +223,16 @@ __global__ void colmax_kernel(const T* __restrict__ U, int64_t rows, int64_t ldu
       if (sb[w] > best || (sb[w] == best && si[w] < bidx)) { best = sb[w]; bidx = si[w]; }
     vals[j] = best;
     idx[j] = row_offset + bidx;
+    if (entry) entry[j] = rows > 0 ? (double)U[bidx + j * ldu] : 0.0;
+  }
+}
+
+// In-place int64 -> double of a small index vector (exact below 2^53).
+__global__ void idx_to_double_kernel(int64_t* idx, int64_t l) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = (double)idx[i];
+    reinterpret_cast<double*>(idx)[i] = d;
   }
 }
 
@@ -287,6 +297,18 @@ __global__ void scale_copy_kernel(const T* __restrict__ src, int64_t rows, int64
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = idx % rows, j = idx / rows;
     dst[i + j * ldd] = (T)((double)src[i + j * lds] * s);
+  }
+}
+
+// dst = (TD)(src * s), s a power of two, any leading dimensions.
+template <typename TS, typename TD>
+__global__ void scale_cast_kernel(const TS* __restrict__ src, int64_t rows, int64_t cols,
+                                  int64_t lds, TD* __restrict__ dst, int64_t ldd, double s) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % rows, j = idx / rows;
+    dst[i + j * ldd] = (TD)((double)src[i + j * lds] * s);
   }
 }
 

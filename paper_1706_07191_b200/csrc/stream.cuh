@@ -31,11 +31,16 @@ struct PanelStreamer {
   std::vector<DBuf<T>*> bufs;
   int64_t panels_streamed = 0;
 
+  // rows_of_cm: row panels of a column-major A (a rank's row shard of a
+  // column-major matrix): each panel lands column-major with ld = panel
+  bool rows_of_cm = false;
+
   PanelStreamer(Ctx& c_, const T* host_, int64_t m_, int64_t n_, int64_t lda_, bool rm,
-                int64_t panel_, int nb_)
-      : c(c_), host(host_), m(m_), n(n_), lda(lda_), row_major(rm), panel(panel_), nb(nb_) {
+                int64_t panel_, int nb_, bool rows_of_cm_ = false)
+      : c(c_), host(host_), m(m_), n(n_), lda(lda_), row_major(rm), panel(panel_), nb(nb_),
+        rows_of_cm(rows_of_cm_ && !rm) {
     BRSVD_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
-    const int64_t inner = row_major ? n : m;
+    const int64_t inner = rows_of_cm ? n : (row_major ? n : m);
     for (int b = 0; b < nb; ++b) {
       cudaEvent_t e1, e2;
       BRSVD_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
@@ -55,7 +60,7 @@ struct PanelStreamer {
     for (auto b : bufs) delete b;
     if (copy) cudaStreamDestroy(copy);
   }
-  int64_t extent() const { return row_major ? m : n; }
+  int64_t extent() const { return (row_major || rows_of_cm) ? m : n; }
   int64_t count() const { return ceil_div(extent(), panel); }
 
   // f(device panel pointer, ld, p0, p1) runs on the compute stream.
@@ -67,12 +72,20 @@ struct PanelStreamer {
       const int b = (int)(i % nb);
       const int64_t p0 = i * panel, p1 = std::min(extent(), p0 + panel);
       BRSVD_CUDA(cudaStreamWaitEvent(copy, consumed[b], 0));
-      BRSVD_CUDA(cudaMemcpy2DAsync(bufs[b]->p, inner * sizeof(T), host + p0 * lda,
-                                   lda * sizeof(T), inner * sizeof(T), p1 - p0,
-                                   cudaMemcpyHostToDevice, copy));
+      int64_t ld = inner;
+      if (rows_of_cm) {   // rows p0..p1 of every column: n strided runs
+        ld = panel;
+        BRSVD_CUDA(cudaMemcpy2DAsync(bufs[b]->p, panel * sizeof(T), host + p0,
+                                     lda * sizeof(T), (p1 - p0) * sizeof(T), n,
+                                     cudaMemcpyHostToDevice, copy));
+      } else {
+        BRSVD_CUDA(cudaMemcpy2DAsync(bufs[b]->p, inner * sizeof(T), host + p0 * lda,
+                                     lda * sizeof(T), inner * sizeof(T), p1 - p0,
+                                     cudaMemcpyHostToDevice, copy));
+      }
       BRSVD_CUDA(cudaEventRecord(copied[b], copy));
       BRSVD_CUDA(cudaStreamWaitEvent(c.stream, copied[b], 0));
-      f(bufs[b]->p, inner, p0, p1);
+      f(bufs[b]->p, ld, p0, p1);
       BRSVD_CUDA(cudaEventRecord(consumed[b], c.stream));
       ++panels_streamed;
     }
@@ -144,7 +157,10 @@ RsvdInfo rsvd_stream(Ctx& c, const T* Ah, int64_t m, int64_t n, int64_t lda, boo
           return info;
         }
       }
-      if (more) normalize_sketch<T>(c, Z.p, n, l, n, Zn.p, n);
+      if (more)
+        normalize_sketch<T>(c, Z.p, n, l, n, Zn.p, n, nullptr,
+                            sizeof(T) == 8 && (peak0 > 0x1p150 ||
+                                               (peak0 > 0.0 && peak0 < 0x1p-150)));
     }
   } else {
     // column panels: Y = sum_J A_J Omega_J, then Y' = sum_J A_J (A_J^T Yn)
@@ -153,7 +169,10 @@ RsvdInfo rsvd_stream(Ctx& c, const T* Ah, int64_t m, int64_t n, int64_t lda, boo
     for (int it = 0; it <= iters; ++it) {
       T* acc = it == 0 ? Y.p : Ynew.p;
       BRSVD_CUDA(cudaMemsetAsync(acc, 0, sizeof(T) * m * l, c.stream));
-      if (it > 0) normalize_sketch<T>(c, Y.p, m, l, m, Yn.p, m);
+      if (it > 0)
+        normalize_sketch<T>(c, Y.p, m, l, m, Yn.p, m, nullptr,
+                            sizeof(T) == 8 && (peak0 > 0x1p150 ||
+                                               (peak0 > 0.0 && peak0 < 0x1p-150)));
       // A_J^T Yn at a power-of-two scale fixed by the first block (fp32
       // inputs far from unit magnitude would under/overflow A_J A_J^T Yn;
       // the sum is renormalised in the next iteration)
@@ -240,6 +259,118 @@ RsvdInfo rsvd_stream(Ctx& c, const T* Ah, int64_t m, int64_t n, int64_t lda, boo
                         : (peak0 > 0.0 ? std::log10(peak0) : -400.0);
   info.overflow = !std::isfinite(s0) || info.log10_peak > lim;
   return info;
+}
+
+// ---------------------------------------------------------------------------
+// One streamed pass over a host-resident row shard A (m x n; row-major, or
+// column-major streamed as row panels) -- the per-rank unit of the sharded
+// out-of-core decomposition (BASELINE config 4; rsvd_naive_ooc's passes,
+// rsvd.py:218-284, with the rows of A split over ranks as store.py:165-175
+// splits its columns).  For each row panel A_i, on the compute stream while
+// the next panel is in flight on the copy stream:
+//   X != NULL:  Y_i = A_i X                       (sample rows, into Y)
+//   Z != NULL:  Z  += A_i^T Y_i   (fp64 accumulator; Y_i as just formed, or
+//                                  as given when X == NULL: B^T = A^T Q)
+// fp32 data: each A_i^T Y_i is the fp16-split tcgen05 product left in its
+// power-of-two row/column scales and unscaled into the fp64 sum, so Z holds
+// inputs of any fp32 magnitude without over- or underflow and no host-side
+// scale has to be known before the pass.
+__global__ void accum_unscaled_kernel(const float* __restrict__ P, int64_t rows, int cols,
+                                      int64_t ldp, const float* __restrict__ scales,
+                                      double* __restrict__ Z, int64_t ldz) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % rows, j = idx / rows;
+    double v = (double)P[i + j * ldp];
+    if (scales) v *= (double)scales[i] * (double)scales[rows + j];
+    Z[i + j * ldz] += v;
+  }
+}
+
+template <typename T>
+__global__ void accum_f64_kernel(const T* __restrict__ P, int64_t rows, int cols, int64_t ldp,
+                                 double* __restrict__ Z, int64_t ldz) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % rows, j = idx / rows;
+    Z[i + j * ldz] += (double)P[i + j * ldp];
+  }
+}
+
+struct PassInfo {
+  int64_t panels = 0;
+  double ms = 0.0;     // pass time on the compute stream
+};
+
+template <typename T>
+PassInfo stream_rows_pass(Ctx& c, const T* Ah, int64_t m, int64_t n, int64_t lda,
+                          bool row_major, const T* X, int64_t ldx, int l, T* Y, int64_t ldy,
+                          double* Z, int64_t ldz, int64_t panel, int nbuf) {
+  PassInfo pi;
+  if (m < 1 || n < 1) return pi;
+  panel = std::max<int64_t>(1, std::min(panel, m));
+  StageEvents ev;
+  PanelStreamer<T> ps(c, Ah, m, n, lda, row_major, panel, nbuf, /*rows_of_cm=*/!row_major);
+  ev.rec(0, c.stream);
+  DBuf<T> tmp;
+  DBuf<float> scales;
+  if (Z != nullptr) {
+    BRSVD_CUDA(cudaMemset2DAsync(Z, (size_t)ldz * sizeof(double), 0, (size_t)n * sizeof(double),
+                                 (size_t)l, c.stream));
+    tmp.alloc(c, (size_t)n * l);
+    if (sizeof(T) == 4) scales.alloc(c, (size_t)n + l);
+  }
+  ps.pass([&](const T* Ap, int64_t ld, int64_t r0, int64_t r1) {
+    const int64_t rows = r1 - r0;
+    if (X != nullptr) big_nn<T>(c, Ap, rows, n, ld, row_major, X, ldx, l, Y + r0, ldy);
+    if (Z == nullptr) return;
+    if constexpr (sizeof(T) == 4) {
+      if (tc_gemm_supported<float>(c, Ap, ld, rows, n, l) && tc::h16_enabled()) {
+        tc_gemm_launch<float>(c, Ap, rows, n, ld, row_major, /*trans=*/true, Y + r0, ldy, l,
+                              tmp.p, n, 0, nullptr, nullptr, scales.p);
+        accum_unscaled_kernel<<<grid_for(n * l), 256, 0, c.stream>>>(tmp.p, n, l, n,
+                                                                     scales.p, Z, ldz);
+        BRSVD_CHECK_LAUNCH();
+        return;
+      }
+    }
+    big_tn<T>(c, Ap, rows, n, ld, row_major, Y + r0, ldy, l, tmp.p, n);
+    accum_f64_kernel<T><<<grid_for(n * l), 256, 0, c.stream>>>(tmp.p, n, l, n, Z, ldz);
+    BRSVD_CHECK_LAUNCH();
+  });
+  ev.rec(1, c.stream);
+  pi.panels = ps.count();
+  pi.ms = ev.ms(0, 1);
+  return pi;
+}
+
+// Z (n x l, fp64) -> a conditioned basis of its span in the data's precision
+// (the power iteration's basis change, normalize_sketch): fp32 data first
+// takes Z to unit order by a power of two (exact) so any magnitude the fp64
+// sum holds fits fp32; fp64 data is unit-scaled inside normalize_sketch.
+template <typename T>
+void normalize_from_f64(Ctx& c, const double* Z, int64_t n, int l, int64_t ldz, T* Zout,
+                        int64_t ldo) {
+  if constexpr (sizeof(T) == 8) {
+    normalize_sketch<double>(c, Z, n, l, ldz, Zout, ldo, nullptr, /*scale_check=*/true);
+  } else {
+    const MaxAbs pk = maxabs<double>(c, Z, n, l, ldz);
+    if (pk.nonfinite)
+      throw Error(kErrOverflow, "sample matrix is not finite; the overflow guard fires");
+    double s = 1.0;
+    if (pk.peak > 0.0) {
+      int e;
+      std::frexp(pk.peak, &e);
+      s = std::ldexp(1.0, -e);
+    }
+    DBuf<float> Zs(c, (size_t)n * l);
+    scale_cast_kernel<double, float><<<grid_for(n * l), 256, 0, c.stream>>>(Z, n, l, ldz, Zs.p,
+                                                                            n, s);
+    BRSVD_CHECK_LAUNCH();
+    normalize_sketch<float>(c, Zs.p, n, l, n, reinterpret_cast<float*>(Zout), ldo);
+  }
 }
 
 }  // namespace brsvd

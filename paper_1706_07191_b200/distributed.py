@@ -11,6 +11,11 @@ The global power iteration of ``rsvd_incore`` (rsvd.py:126-141) /
   * B^T = sum_g A_g^T Q_g          (n x l)   all-reduce, once
   * column argmax of U             (l)       all-gather, for the signs
 
+The shard is either resident in HBM (a torch CUDA tensor) or host-resident
+(``HostShard``: BASELINE config 4, each rank streams its own row panels over
+its own PCIe link through the panel streamer, one pass per power step --
+``brsvd_stream_rows_pass`` forms Y_i = A_i X and accumulates A_i^T Y_i from
+the same panel load, so the decomposition costs q + 2 passes over A).
 Everything else is local (the A-streaming products) or replicated and
 bit-identical on every rank (the l x l factorisations, the small SVD), so U
 stays row-sharded and sigma, Vt are replicated.  The stage operations come
@@ -74,12 +79,56 @@ class TorchComm:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return float(t.item())
 
+    def allgather_array(self, arr):
+        """All-gather of a small float64 array (one tensor collective)."""
+        if self.world == 1:
+            return [np.asarray(arr)]
+        import torch
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        t = torch.as_tensor(np.ascontiguousarray(arr, dtype=np.float64), device=dev)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [o.cpu().numpy() for o in out]
+
     def allgather_obj(self, obj):
         if self.world == 1:
             return [obj]
         out = [None] * self.world
         self.dist.all_gather_object(out, obj, group=self.group)
         return out
+
+
+# ---------------------------------------------------------------------------
+class HostShard:
+    """This rank's row shard A[r0:r1, :] held in host memory (pinned for
+    overlapped DMA, e.g. a numpy view of ``torch.empty(..., pin_memory=True)``),
+    streamed to the GPU in row panels of ``panel`` rows through ``nbuf``
+    device buffers once per pass (store.py:165-175 reads a column block per
+    pass the same way; here the unit is a row panel of the rank's shard).
+    C-ordered or Fortran-ordered arrays are accepted."""
+
+    def __init__(self, a, panel=None, nbuf=3):
+        a = np.asarray(a)
+        if a.ndim != 2:
+            from .kernels import ShapeError
+            raise ShapeError(f"expected a 2-D shard, got shape {a.shape}")
+        if a.dtype not in (np.float32, np.float64):
+            a = a.astype(np.float64)
+        if not (a.flags.c_contiguous or a.flags.f_contiguous):
+            a = np.ascontiguousarray(a)
+        self.a = a
+        self.shape = a.shape
+        self.dtype = a.dtype
+        if panel is None:   # ~512 MiB panels
+            panel = max(1, (512 << 20) // max(1, a.shape[1] * a.itemsize))
+        self.panel = int(panel)
+        self.nbuf = int(nbuf)
+        self.passes = 0
+        self.pass_ms = []
+
+    @property
+    def nbytes(self):
+        return self.a.nbytes
 
 
 # ---------------------------------------------------------------------------
@@ -233,8 +282,48 @@ class GpuOps:
                                          ctypes.c_void_p(idx.ctypes.data)))
         return vals, idx
 
-    def entry(self, U, i, j):
-        return float(U[i, j].item())
+    def colmax_entries(self, U, row_offset):
+        """(3, l) float64: per column max |u|, its global row, the signed u
+        there (brsvd_colmax_entries: one kernel, one D2H copy)."""
+        self._sync_stream()
+        l = U.shape[1]
+        out = np.empty(3 * l, dtype=np.float64)
+        _lib.check(self.lib.brsvd_colmax_entries(self.ctx.handle, _vp(U), U.shape[0], l, _ld(U),
+                                                 _code(U), int(row_offset),
+                                                 ctypes.c_void_p(out.ctypes.data)))
+        return out.reshape(3, l)
+
+    def stream_pass(self, shard, X, Y=None, want_z=False):
+        """One pass of the host-resident shard through the panel streamer
+        (brsvd_stream_rows_pass): Y = A X when X is given (else Y is an
+        input), and the fp64 Z = A^T Y when want_z.  Returns (Y, Z)."""
+        self._sync_stream()
+        a = shard.a
+        m, n = a.shape
+        layout = _lib.ROW_MAJOR if a.flags.c_contiguous else _lib.COL_MAJOR
+        lda = n if layout == _lib.ROW_MAJOR else m
+        tdt = self.torch.float64 if a.dtype == np.float64 else self.torch.float32
+        l = X.shape[1] if X is not None else Y.shape[1]
+        if Y is None:
+            Y = _cm_empty(m, l, tdt, self.device)
+        Z = _cm_empty(n, l, self.torch.float64, self.device) if want_z else None
+        ms = ctypes.c_double()
+        _lib.check(self.lib.brsvd_stream_rows_pass(
+            self.ctx.handle, ctypes.c_void_p(a.ctypes.data), m, n, lda, _lib.dtype_code(a.dtype),
+            layout, _vp(X) if X is not None else None, _ld(X) if X is not None else 1, l,
+            _vp(Y), _ld(Y), _vp(Z) if Z is not None else None, _ld(Z) if Z is not None else 1,
+            shard.panel, shard.nbuf, ctypes.byref(ms)))
+        shard.passes += 1
+        shard.pass_ms.append(ms.value)
+        return Y, Z
+
+    def normalize_f64(self, Z, dtype):
+        """Basis change of an fp64 Z (brsvd_normalize_f64) in the data's dtype."""
+        self._sync_stream()
+        out = _cm_empty(Z.shape[0], Z.shape[1], dtype, self.device)
+        _lib.check(self.lib.brsvd_normalize_f64(self.ctx.handle, _vp(Z), Z.shape[0], Z.shape[1],
+                                                _ld(Z), _code(out), _vp(out), _ld(out)))
+        return out
 
     def scale_cols(self, X, scale):
         self._sync_stream()
@@ -299,57 +388,86 @@ def _orth_sharded(Y, ops, comm, eps_data, row_offset, m_total, seed):
     return Q, min(rank_ref, kept)
 
 
+def _sign_flips(cands, l):
+    """_fix_signs (rsvd.py:105-115) over the global rows: per column, the
+    first row (lowest global index) of the largest |u| decides; cands are the
+    ranks' (3, l) [max |u|, global row, signed u] arrays."""
+    signs = np.ones(l)
+    for j in range(l):
+        best = None
+        for c in cands:
+            v, i, e = float(c[0, j]), float(c[1, j]), float(c[2, j])
+            if v != v:
+                v = np.inf
+            if best is None or v > best[0] or (v == best[0] and i < best[1]):
+                best = (v, i, e)
+        signs[j] = -1.0 if best[2] < 0 else 1.0
+    return signs
+
+
 def rsvd_sharded(A_local, cfg, row_offset, m_total, comm=None, ops=None, omega=None):
     """Randomized SVD of the row-sharded matrix whose rows
     [row_offset, row_offset + A_local.shape[0]) this rank holds.
 
+    ``A_local`` is resident (torch CUDA tensor; numpy with the test ops) or a
+    ``HostShard`` streamed from host memory (q + 2 passes over PCIe).
     Returns (factors, info): factors.U holds this rank's rows of U;
     sigma and Vt are replicated.  Same semantics (global power iteration) and
-    validation as rsvd_incore (rsvd.py:126-141).
+    validation as rsvd_incore (rsvd.py:126-141) / rsvd_naive_ooc
+    (rsvd.py:218-284).
     """
     comm = comm or TorchComm()
     ops = ops or GpuOps()
     row_offset, m_total = int(row_offset), int(m_total)
+    streamed = isinstance(A_local, HostShard)
     m_loc, n = A_local.shape
     cfg.validate(m_total, n)
     k, p, q = cfg.target_rank, cfg.oversampling, cfg.power_exponent
     l = k + p
-    dtype = ops.dtype_of(A_local)
-    npdt = np.dtype(np.float64) if str(dtype).endswith("float64") else np.dtype(np.float32)
+    if streamed:
+        npdt = np.dtype(A_local.dtype)
+        dtype = (ops.torch.float64 if npdt == np.float64 else ops.torch.float32) \
+            if hasattr(ops, "torch") else npdt
+    else:
+        dtype = ops.dtype_of(A_local)
+        npdt = np.dtype(np.float64) if str(dtype).endswith("float64") else np.dtype(np.float32)
     eps_data = _EPS[npdt]
     seed = int(cfg.master_seed)
     X = ops.asarray(omega, dtype) if omega is not None else ops.gaussian(n, l, seed, 0, 0, dtype)
-    amax = ops.absmax(A_local) if hasattr(ops, "absmax") else None
-    Y = ops.product(A_local, X, False, amax)
-    vals, _ = ops.colmax(Y, row_offset)
+    if streamed:
+        def sample(Xs, want_z):
+            return ops.stream_pass(A_local, Xs, None, want_z)
+
+        def basis(Z):
+            return ops.normalize_f64(Z, dtype)
+    else:
+        amax = ops.absmax(A_local) if hasattr(ops, "absmax") else None
+
+        def sample(Xs, want_z):
+            Ys = ops.product(A_local, Xs, False, amax)
+            return Ys, (ops.product(A_local, Ys, True, amax) if want_z else None)
+
+        basis = ops.normalize
+    Y, Zp = sample(X, q > 0)
+    vals = ops.colmax_entries(Y, row_offset)[0]
     bad = not np.all(np.isfinite(vals)) or np.any(vals < 0)
     peak0 = comm.allreduce_max(float(np.max(vals)) if vals.size else 0.0)
     bad = comm.allreduce_max(1.0 if bad else 0.0) > 0
     if bad:
         raise FloatingPointError("sample matrix is not finite; the overflow guard fires")
-    for _ in range(q):
-        Z = comm.allreduce_sum(ops.product(A_local, Y, True, amax))
-        Y = ops.product(A_local, ops.normalize(Z), False, amax)
+    for it in range(q):
+        Z = comm.allreduce_sum(Zp)
+        Y, Zp = sample(basis(Z), it < q - 1)
     Q, rank_y = _orth_sharded(Y, ops, comm, eps_data, row_offset, m_total, seed ^ 0x7153)
     Qd = ops.cast(Q, dtype)
-    Bt = comm.allreduce_sum(ops.product(A_local, Qd, True, amax))
+    if streamed:
+        _, Bt64 = ops.stream_pass(A_local, None, Qd, True)
+        Bt = ops.cast(comm.allreduce_sum(Bt64), dtype)
+    else:
+        Bt = comm.allreduce_sum(ops.product(A_local, Qd, True, amax))
     W, sigma, Vt, rank_b = ops.small_svd(Bt)
     U = ops.apply(Q, W, dtype)
-    # _fix_signs (rsvd.py:105-115) over the global rows
-    vals, idx = ops.colmax(U, row_offset)
-    entries = []
-    for j in range(l):
-        i_loc = int(idx[j]) - row_offset
-        entries.append((float(vals[j]), int(idx[j]), ops.entry(U, i_loc, j)))
-    gathered = comm.allgather_obj(entries)
-    signs = np.ones(l)
-    for j in range(l):
-        best = None
-        for ent in gathered:
-            v, i, e = ent[j]
-            if best is None or v > best[0] or (v == best[0] and i < best[1]):
-                best = (v, i, e)
-        signs[j] = -1.0 if best[2] < 0 else 1.0
+    signs = _sign_flips(comm.allgather_array(ops.colmax_entries(U, row_offset)), l)
     ops.scale_cols(U, signs)
     ops.scale_cols(Vt.t() if hasattr(Vt, "t") and not isinstance(Vt, np.ndarray) else Vt.T,
                    signs)
@@ -361,4 +479,7 @@ def rsvd_sharded(A_local, cfg, row_offset, m_total, comm=None, ops=None, omega=N
     if log_peak > lim:
         raise FloatingPointError("sample matrix magnitude exceeds the overflow guard")
     info = {"rank_y": rank_y, "rank_b": rank_b, "max_abs_y0": peak0, "log10_peak": log_peak}
+    if streamed:
+        info.update(passes=A_local.passes, pass_ms=list(A_local.pass_ms),
+                    h2d_bytes=A_local.passes * A_local.nbytes)
     return SvdFactors(U=U, sigma=sigma, Vt=Vt, target_rank=k, effective_l=l), info

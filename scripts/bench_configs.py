@@ -8,6 +8,10 @@ headline, which is bench.py / config 2).  One JSON line per config.
       pinned host memory streamed over PCIe (the full 1e6 rows = 400 GB exceed
       this box's 196 GB of host RAM; the default is the 1/10 row sample the
       survey's CPU plan uses, 40 GB).  Roofline: measured pinned H2D.
+  c4  the c3 matrix row-sharded over torchrun ranks, one host-resident pinned
+      shard per GPU streamed over its own link (distributed.HostShard), NCCL
+      all-reduce of Z / Grams / B^T; roofline: concurrent pinned H2D.
+      torchrun --nproc-per-node N scripts/bench_configs.py --configs c4
   c5  IALM-RPCA fp64 76800 x 20000 (12.3 GB, in HBM), low-rank background +
       moving sparse foreground, k=p=10, q=1, tol 1e-7 (ialm_rpca).
 """
@@ -113,6 +117,111 @@ def bench_c3(rows, steps):
                          "svd": run.stats.seconds_svd}}
 
 
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if not dist.is_initialized():
+            dist.init_process_group("nccl", device_id=torch.device(
+                f"cuda:{local % max(1, torch.cuda.device_count())}"))
+    return world, rank, local
+
+
+def _max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def concurrent_h2d_gbs(world):
+    """Aggregate pinned H2D with every rank copying 1 GiB at once (the C4
+    roofline denominator: host memory and the PCIe links all busy)."""
+    import torch
+    n = 1 << 28
+    h = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    d = torch.empty(n, dtype=torch.float32, device="cuda")
+    d.copy_(h)
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(3):
+        _barrier(world)
+        s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+        s.record()
+        d.copy_(h, non_blocking=True)
+        e.record()
+        torch.cuda.synchronize()
+        best = min(best, _max_over_ranks(s.elapsed_time(e) / 1e3, world))
+    return world * n * 4 / best / 1e9
+
+
+def bench_c4(rows_total, steps):
+    """Config 4 structure: the (rows_total x 1e5) fp32 rank-100 + noise matrix
+    row-sharded over the ranks, each shard host-resident in pinned memory and
+    streamed over its own PCIe link (distributed.HostShard), Z / Gram / B^T
+    all-reduced over NCCL.  Strong scaling over the fixed matrix."""
+    import torch
+    from paper_1706_07191_b200 import SketchConfig
+    from paper_1706_07191_b200.distributed import GpuOps, HostShard, TorchComm, rsvd_sharded
+    world, rank, local = _dist()
+    n, rk = 100000, 100
+    bounds = np.linspace(0, rows_total, world + 1).astype(np.int64)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    host = torch.empty((r1 - r0, n), dtype=torch.float32, pin_memory=True)
+    gR = torch.Generator(device="cuda").manual_seed(5)          # shared right factor
+    R = torch.randn(rk, n, generator=gR, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    chunk = 8192
+    for c0 in range(0, r1 - r0, chunk):
+        c1 = min(r1 - r0, c0 + chunk)
+        blk = torch.randn(c1 - c0, rk, generator=g, device="cuda") @ R
+        blk.add_(torch.randn(c1 - c0, n, generator=g, device="cuda"), alpha=1e-3)
+        host[c0:c1].copy_(blk)
+    del R, blk
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    shard = HostShard(host.numpy(), panel=8192, nbuf=3)
+    cfg = SketchConfig(100, 20, 1)
+    comm, ops = TorchComm(), GpuOps()
+    rsvd_sharded(shard, cfg, r0, rows_total, comm=comm, ops=ops)   # warm-up
+    ts = []
+    for _ in range(steps):
+        shard.passes, shard.pass_ms = 0, []
+        _barrier(world)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+        s.record()
+        f, info = rsvd_sharded(shard, cfg, r0, rows_total, comm=comm, ops=ops)
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(_max_over_ranks(s.elapsed_time(e) / 1e3, world))
+    t = float(np.median(ts))
+    passes = info["passes"]
+    gbs = passes * rows_total * n * 4 / t / 1e9
+    peak = concurrent_h2d_gbs(world)
+    return {"config": "c4_rowshard_stream", "gpus": world, "rows": rows_total, "n": n,
+            "dtype": "f32", "k": 100, "p": 20, "q": 1, "host_bytes": rows_total * n * 4,
+            "passes": passes, "seconds": t, "a_stream_gbs": gbs, "scaling": "strong",
+            "roofline": {"bound": "pcie_h2d", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                         "frac": gbs / peak,
+                         "peak_basis": f"measured concurrent pinned H2D, {world} GPU(s)"},
+            "sigma_top3": [float(x) for x in f.sigma[:3].cpu()], "rank": rank}
+
+
 def video_matrix(m, n, seed=0):
     """Low-rank nonnegative background (rank 3) + moving blocks."""
     import torch
@@ -173,6 +282,10 @@ def main():
             out = bench_c3(args.c3_rows, args.steps)
         elif c == "c5":
             out = bench_c5(args.steps)
+        elif c == "c4":
+            out = bench_c4(args.c3_rows, args.steps)
+            if out.pop("rank") != 0:
+                continue
         else:
             continue
         print(json.dumps(out), flush=True)

@@ -88,6 +88,42 @@ class NumpyOps:
     def entry(self, U, i, j):
         return float(U[i, j])
 
+    def colmax_entries(self, U, row_offset):
+        """brsvd_colmax_entries: [max |u| | global row | signed u] per column
+        (NaN counts as +inf, like the kernel)."""
+        a = np.abs(U).astype(F64)
+        a[np.isnan(a)] = np.inf
+        idx = np.argmax(a, axis=0)
+        cols = np.arange(U.shape[1])
+        return np.stack([a[idx, cols], (idx + row_offset).astype(F64),
+                         U[idx, cols].astype(F64)])
+
+    def stream_pass(self, shard, X, Y=None, want_z=False):
+        """brsvd_stream_rows_pass: row panels of the host shard; Y_i = A_i X,
+        Z += A_i^T Y_i summed in fp64."""
+        a = shard.a
+        m, n = a.shape
+        if X is not None:
+            Y = np.empty((m, X.shape[1]), dtype=a.dtype, order="F")
+        Z = np.zeros((n, Y.shape[1]), dtype=F64, order="F") if want_z else None
+        for r0 in range(0, m, shard.panel):
+            r1 = min(m, r0 + shard.panel)
+            if X is not None:
+                Y[r0:r1] = a[r0:r1] @ X
+            if want_z:
+                Z += (a[r0:r1].T @ Y[r0:r1]).astype(F64)
+        shard.passes += 1
+        shard.pass_ms.append(0.0)
+        return Y, Z
+
+    def normalize_f64(self, Z, dtype):
+        """brsvd_normalize_f64: fp32 data first at a power-of-two unit scale."""
+        if np.dtype(dtype) == np.float32:
+            peak = float(np.max(np.abs(Z))) if Z.size else 0.0
+            e = np.frexp(peak)[1] if peak > 0 else 0
+            Z = np.asfortranarray((Z * 2.0 ** -int(e)).astype(np.float32))
+        return self.normalize(np.asfortranarray(Z, dtype=dtype))
+
     def scale_cols(self, X, scale):
         X *= np.asarray(scale, dtype=X.dtype)[None, :]
         return X

@@ -19,7 +19,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, case, out_dir):
+def _worker(rank, world, port, case, out_dir, streamed=False):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -33,8 +33,14 @@ def _worker(rank, world, port, case, out_dir):
     m = A.shape[0]
     bounds = np.linspace(0, m, world + 1).astype(int)
     r0, r1 = bounds[rank], bounds[rank + 1]
-    f, info = rsvd_sharded(A[r0:r1].copy(), SketchConfig(**cfg_args), r0, m,
+    shard = A[r0:r1].copy()
+    if streamed:   # host-resident shard streamed in row panels (config 4)
+        from paper_1706_07191_b200.distributed import HostShard
+        shard = HostShard(shard if case != "f32" else np.asfortranarray(shard), panel=37)
+    f, info = rsvd_sharded(shard, SketchConfig(**cfg_args), r0, m,
                            comm=TorchComm(), ops=NumpyOps())
+    if streamed:
+        assert info["passes"] == cfg_args["power_exponent"] + 2
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), U=f.U, sigma=f.sigma, Vt=f.Vt, r0=r0,
              rank_y=info["rank_y"], rank_b=info["rank_b"])
     dist.barrier()
@@ -55,20 +61,23 @@ def _case(name):
     raise KeyError(name)
 
 
-def _run(case, world, tmp_path):
+def _run(case, world, tmp_path, streamed=False):
     import torch.multiprocessing as mp
     port = _free_port()
-    mp.start_processes(_worker, args=(world, port, case, str(tmp_path)), nprocs=world,
-                       join=True, start_method="spawn")
+    mp.start_processes(_worker, args=(world, port, case, str(tmp_path), streamed),
+                       nprocs=world, join=True, start_method="spawn")
     parts = [np.load(tmp_path / f"r{r}.npz") for r in range(world)]
     U = np.vstack([p["U"] for p in parts])
     return U, parts
 
 
+@pytest.mark.parametrize("streamed", [False, True])
 @pytest.mark.parametrize("case", ["noisy", "f32"])
-def test_sharded_matches_single_process_oracle(case, tmp_path):
+def test_sharded_matches_single_process_oracle(case, streamed, tmp_path):
+    """In-memory shards and host-resident shards streamed in row panels
+    (q + 2 passes, fp64 Z accumulation) against the single-process oracle."""
     from oracle import ref_cpu
-    U, parts = _run(case, 2, tmp_path)
+    U, parts = _run(case, 2, tmp_path, streamed)
     A, cfg = _case(case)
     k, p, q, seed = (cfg["target_rank"], cfg["oversampling"], cfg["power_exponent"],
                      cfg["master_seed"])

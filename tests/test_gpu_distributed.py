@@ -17,7 +17,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, dtype_name, out_dir):
+def _worker(rank, world, port, dtype_name, out_dir, streamed=False):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -36,22 +36,38 @@ def _worker(rank, world, port, dtype_name, out_dir):
     omega = ref_cpu.normal_sketch(800, 30, 0, dtype=dtype)
     bounds = [0, 1500, 3000]
     r0, r1 = bounds[rank], bounds[rank + 1]
-    A_loc = torch.as_tensor(A[r0:r1], device="cuda")
+    if streamed:
+        # host-resident shard in pinned memory, streamed in 301-row panels
+        # (the f32 case as a column-major shard: strided row panels)
+        from paper_1706_07191_b200.distributed import HostShard
+        pin = torch.empty(A[r0:r1].shape[::-1] if dtype_name == "f32" else A[r0:r1].shape,
+                          dtype=torch.float64 if dtype == np.float64 else torch.float32,
+                          pin_memory=True).numpy()
+        host = pin.T if dtype_name == "f32" else pin
+        host[...] = A[r0:r1]
+        A_loc = HostShard(host, panel=301, nbuf=3)
+    else:
+        A_loc = torch.as_tensor(A[r0:r1], device="cuda")
     f, info = rsvd_sharded(A_loc, SketchConfig(20, 10, 2), r0, 3000, comm=TorchComm(),
                            ops=GpuOps(0), omega=omega)
+    if streamed:
+        assert info["passes"] == 4 and info["h2d_bytes"] == 4 * A[r0:r1].nbytes
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), U=f.U.cpu().numpy(),
              sigma=f.sigma.cpu().numpy(), Vt=f.Vt.cpu().numpy())
     dist.barrier()
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("streamed", [False, True])
 @pytest.mark.parametrize("dtype_name", ["f64", "f32"])
-def test_two_shards_match_single_gpu(dtype_name, tmp_path):
+def test_two_shards_match_single_gpu(dtype_name, streamed, tmp_path):
+    """Resident shards and host-resident shards streamed through the panel
+    streamer (config 4's path) against the single-GPU decomposition."""
     import torch.multiprocessing as mp
     from oracle import ref_cpu
     from paper_1706_07191_b200 import SketchConfig, rsvd_incore
-    mp.start_processes(_worker, args=(2, _free_port(), dtype_name, str(tmp_path)), nprocs=2,
-                       join=True, start_method="spawn")
+    mp.start_processes(_worker, args=(2, _free_port(), dtype_name, str(tmp_path), streamed),
+                       nprocs=2, join=True, start_method="spawn")
     parts = [np.load(tmp_path / f"r{r}.npz") for r in range(2)]
     U = np.vstack([p["U"] for p in parts])
     dtype = np.float64 if dtype_name == "f64" else np.float32
