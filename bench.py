@@ -56,6 +56,10 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the other BASELINE configs (c1, c3 sample, c5)")
+    ap.add_argument("--configs", default="c1,c3,c5")
+    ap.add_argument("--c3-rows", type=int, default=25000)
     return ap.parse_args()
 
 
@@ -288,6 +292,36 @@ def run_reference(args, world, rank, local):
     print(json.dumps(line), flush=True)
 
 
+def other_configs(args, local):
+    """The other BASELINE configurations, each timed on the device with its
+    own clock record (scripts/bench_configs.py): c1 (in-core fp64, device
+    A), c3 (out-of-core fp32, a row sample of the 1e6 x 1e5 matrix in pinned
+    host memory streamed over PCIe; roofline = measured pinned H2D), c5
+    (IALM-RPCA fp64 76800 x 20000 in HBM)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "bench_configs", os.path.join(ROOT, "scripts", "bench_configs.py"))
+    bc = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bc)
+    out = {}
+    for c in args.configs.split(","):
+        c = c.strip()
+        fn = {"c1": lambda: bc.bench_c1(10), "c3": lambda: bc.bench_c3(args.c3_rows, 2),
+              "c5": lambda: bc.bench_c5(1)}.get(c)
+        if fn is None:
+            continue
+        try:
+            with ClockSampler(local) as clk:
+                r = fn()
+            r["clocks"] = clk.summary()
+        except Exception as e:   # a config that cannot run here is reported, not fatal
+            r = {"config": c, "error": f"{type(e).__name__}: {e}"}
+        out[c] = r
+        import torch
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, world, rank, local):
     import torch
     from paper_1706_07191_b200 import SketchConfig, _lib
@@ -426,6 +460,15 @@ def run_ours(args, world, rank, local):
         torch.cuda.empty_cache()
         cpu = cpu_baseline(a_cpu)
 
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        try:
+            del A
+        except NameError:
+            pass
+        torch.cuda.empty_cache()
+        configs = other_configs(args, local)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
@@ -445,6 +488,7 @@ def run_ours(args, world, rank, local):
                 "sketch": st.seconds_sketch, "orthonormalize": st.seconds_orthonormalize,
                 "form_core": st.seconds_form_core, "svd": st.seconds_svd},
             "sigma_top3": [float(x) for x in sigma_top.cpu()],
+            "other_configs": configs,
         }
         print(json.dumps(line), flush=True)
 

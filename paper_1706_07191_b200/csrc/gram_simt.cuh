@@ -149,6 +149,128 @@ __global__ void __launch_bounds__(Cfg<BT, NCG>::NT,
   }
 }
 
+// ---------------------------------------------------------------------------
+// FP64 tensor-core (DMMA, mma.sync m8n8k4 f64) variant of the same tiled,
+// split-K Gram: BT x BT output tiles, one 32 x 32 warp tile each (4 x 4 DMMA
+// blocks, 32 fp64 accumulators per thread); X, Y slabs staged i-major
+// (k contiguous, padded) so the loader's coalesced k-runs store without
+// bank conflicts and each fragment load is two wavefronts.  Products of
+// fp32 data are exact in fp64; fp64 accumulation as the SIMT kernel (the
+// summation order differs, the partials are summed in the same fixed order).
+constexpr int DBK = 16;   // k slab of the DMMA kernel
+template <int BT> struct DCfg {
+  static constexpr int LDK = DBK + 4;                       // padded k run (doubles)
+  static constexpr int WT = BT / 32;                        // warp tiles per side
+  static constexpr int NT = WT * WT * 32;
+  static constexpr int PER = (BT * DBK + NT - 1) / NT;
+  static constexpr size_t SMEM = (size_t)2 * 2 * BT * LDK * sizeof(double);
+};
+
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, "
+               "{%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <typename TX, typename TY, int BT>
+__global__ void __launch_bounds__(DCfg<BT>::NT,
+                                  (DCfg<BT>::NT <= 288 && sizeof(TX) == 4) ? 2 : 1)
+    gram_dmma_kernel(int64_t r, int a, int b, const TX* __restrict__ X, int64_t ldx,
+                     const TY* __restrict__ Y, int64_t ldy, int sym, int ntj, int64_t kchunk,
+                     double* __restrict__ part) {
+  using C = DCfg<BT>;
+  constexpr int LDK = C::LDK, NT = C::NT, PER = C::PER, WT = C::WT;
+  extern __shared__ __align__(16) double gsm[];
+  double(*As)[BT][LDK] = reinterpret_cast<double(*)[BT][LDK]>(gsm);
+  double(*Bs)[BT][LDK] = reinterpret_cast<double(*)[BT][LDK]>(gsm + 2 * BT * LDK);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int wi = wid / WT, wj = wid % WT;
+  int ti, tj;
+  const int t = blockIdx.x;
+  if (sym) {
+    ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+    while (ti * (ti + 1) / 2 > t) --ti;
+    tj = t - ti * (ti + 1) / 2;
+  } else {
+    ti = t / ntj;
+    tj = t % ntj;
+  }
+  const int i0 = ti * BT, j0 = tj * BT;
+  const int64_t kb = (int64_t)blockIdx.y * kchunk;
+  const int64_t ke = min(r, kb + kchunk);
+  TX ra[PER];
+  TY rb[PER];
+  auto load = [&](int64_t k0) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = tid + q * NT;
+      const int lc = e / DBK, lk = e % DBK;
+      const int64_t k = k0 + lk;
+      const bool ok = e < BT * DBK && k < ke;
+      ra[q] = (ok && i0 + lc < a) ? X[k + (int64_t)(i0 + lc) * ldx] : TX(0);
+      rb[q] = (ok && j0 + lc < b) ? Y[k + (int64_t)(j0 + lc) * ldy] : TY(0);
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = tid + q * NT;
+      if (e < BT * DBK) {
+        As[buf][e / DBK][e % DBK] = (double)ra[q];
+        Bs[buf][e / DBK][e % DBK] = (double)rb[q];
+      }
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
+  const int fr = lane >> 2, fk = lane & 3;   // fragment row / k of this lane
+  int buf = 0;
+  if (kb < ke) {
+    load(kb);
+    store(0);
+  }
+  __syncthreads();
+  for (int64_t k0 = kb; k0 < ke; k0 += DBK) {
+    const bool more = k0 + DBK < ke;
+    if (more) load(k0 + DBK);
+#pragma unroll
+    for (int kk = 0; kk < DBK; kk += 4) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) av[u] = As[buf][wi * 32 + u * 8 + fr][kk + fk];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) bv[v] = Bs[buf][wj * 32 + v * 8 + fr][kk + fk];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) dmma_8x8x4(acc[u][v][0], acc[u][v][1], av[u], bv[v]);
+    }
+    if (more) {
+      store(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  double* P = part + (int64_t)blockIdx.y * a * b;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int i = i0 + wi * 32 + u * 8 + fr;
+    if (i >= a) continue;
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = j0 + wj * 32 + v * 8 + 2 * fk + e;
+        if (j < b) P[i + (int64_t)j * a] = acc[u][v][e];
+      }
+  }
+}
+
 // C = sum over splits (fixed order); sym: mirror the lower-triangle tiles.
 __global__ void gram_reduce_kernel(const double* __restrict__ part, int a, int b, int splits,
                                    int sym, int BT, double* __restrict__ C, int64_t ldc) {

@@ -168,14 +168,53 @@ void gram_fp64_bt(Ctx& c, int64_t a, int64_t b, int64_t r, const TX* X, int64_t 
   BRSVD_CHECK_LAUNCH();
 }
 
+// DMMA (fp64 tensor core) Gram: same tiles, split-K and fixed-order partial
+// sum as gram_fp64_bt.
+template <typename TX, typename TY, int BT>
+void gram_dmma_bt(Ctx& c, int64_t a, int64_t b, int64_t r, const TX* X, int64_t ldx,
+                  const TY* Y, int64_t ldy, double* C, int64_t ldc, bool sym) {
+  using namespace gram;
+  using Cf = DCfg<BT>;
+  const int nti = (int)ceil_div(a, BT), ntj = (int)ceil_div(b, BT);
+  const int tiles = sym ? nti * (nti + 1) / 2 : nti * ntj;
+  const int per_sm = (Cf::NT <= 288 && sizeof(TX) == 4) ? 2 : 1;
+  int64_t splits = std::max<int64_t>(1, ceil_div((int64_t)per_sm * c.num_sms, tiles));
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, r / (8 * DBK)));
+  int64_t kchunk = ceil_div(ceil_div(r, splits), DBK) * DBK;
+  splits = ceil_div(r, kchunk);
+  DBuf<double> part(c, (size_t)(splits * a * b));
+  BRSVD_CUDA(cudaFuncSetAttribute(gram_dmma_kernel<TX, TY, BT>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)Cf::SMEM));
+  gram_dmma_kernel<TX, TY, BT><<<dim3(tiles, (unsigned)splits), Cf::NT, Cf::SMEM,
+                                 c.stream>>>(r, (int)a, (int)b, X, ldx, Y, ldy, sym ? 1 : 0,
+                                             ntj, kchunk, part.p);
+  BRSVD_CHECK_LAUNCH();
+  gram_reduce_kernel<<<grid_for(a * b), 256, 0, c.stream>>>(part.p, (int)a, (int)b,
+                                                            (int)splits, sym ? 1 : 0, BT, C,
+                                                            ldc);
+  BRSVD_CHECK_LAUNCH();
+}
+
+inline bool gram_simt_forced() {
+  const char* e = std::getenv("BRSVD_GRAM_SIMT");
+  return e && e[0] == '1';
+}
+
 // Tall-skinny fp64 Gram C (a x b) = X^T Y (gram_simt.cuh), deterministic
-// split-K; symmetric when X is Y.  The tile size pads a, b least.
+// split-K; symmetric when X is Y.  The tile size pads a, b least.  DMMA
+// tensor-core tiles unless BRSVD_GRAM_SIMT=1.
 template <typename TX, typename TY>
 void gram_fp64(Ctx& c, int64_t a, int64_t b, int64_t r, const TX* X, int64_t ldx,
                const TY* Y, int64_t ldy, double* C, int64_t ldc) {
   const bool sym = (a == b) && ((const void*)X == (const void*)Y) && ldx == ldy;
   const int64_t w96 = ceil_div(a, 96) * ceil_div(b, 96) * 96 * 96;
   const int64_t w128 = ceil_div(a, 128) * ceil_div(b, 128) * 128 * 128;
+  if (!gram_simt_forced()) {
+    if (w96 < w128) gram_dmma_bt<TX, TY, 96>(c, a, b, r, X, ldx, Y, ldy, C, ldc, sym);
+    else gram_dmma_bt<TX, TY, 128>(c, a, b, r, X, ldx, Y, ldy, C, ldc, sym);
+    return;
+  }
   if (w96 < w128)
     gram_fp64_bt<TX, TY, 96, (sizeof(TX) == 4 && sizeof(TY) == 4) ? 3 : 2>(c, a, b, r, X, ldx,
                                                                            Y, ldy, C, ldc, sym);
