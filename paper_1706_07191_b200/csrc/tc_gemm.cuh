@@ -211,7 +211,7 @@ __device__ __forceinline__ uint32_t tf32_rna(float x) {
 
 // Tensor-core accumulation truncates (round-toward-zero) on every MMA add
 // into TMEM, a bias of ~0.4 ulp per add that grows linearly with K
-// (scripts/exp_tc_bias.py: -2.3e-6 at K=256, -1.7e-4 at K=16384).  The
+// (scripts/probe.py bias: -2.3e-6 at K=256, -1.7e-4 at K=16384).  The
 // accumulator is therefore double-buffered and flushed every kChunkKB
 // k-blocks (128 k values = 48 MMA adds, bias ~1e-6) into round-to-nearest
 // fp32 running sums held in the converter warps' registers.
