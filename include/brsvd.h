@@ -263,6 +263,23 @@ BRSVD_API int brsvd_ialm_blocked(brsvd_ctx* ctx, const void* M, int64_t m, int64
                                  double* residuals, double* mus, double* svd_seconds,
                                  double* iter_seconds);
 
+/* Host-streamed IALM (the reference's out-of-core branch, _ialm_rpca_ooc,
+ * rpca.py:216-304): M (host, column-major m x n, ld ldm -- e.g. a store's
+ * payload), the sparse part S and the dual workspace Y (host, m x n, ld ldm,
+ * caller-allocated; pinned memory overlaps the copies) never reside on the
+ * device; every pass streams their column blocks col_bounds[0..nblocks]
+ * (the memory budget's plan, which is also the inner SVD's block partition:
+ * brsvd_run's per-block power iteration, rpca.py:274) through `nslots`
+ * device slots, H2D and D2H on separate streams.  L (host, m x n) receives
+ * the low-rank part.  History arrays as brsvd_ialm. */
+BRSVD_API int brsvd_ialm_stream(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n,
+                                int64_t ldm, int dtype, int k, int p, int q, uint64_t seed,
+                                const void* omega, double lam, double mu0, double rho,
+                                double tol, int max_iterations, const int64_t* col_bounds,
+                                int nblocks, void* L, void* S, void* Y, int nslots,
+                                int32_t* iterations, int32_t* converged, double* residuals,
+                                double* mus, double* svd_seconds, double* iter_seconds);
+
 /* ---- stage entry points for the row-sharded driver ---------------------
  * (paper_1706_07191_b200/distributed.py).  Device pointers only; the small
  * matrices are fp64 column-major.  Each replaces one step of the reference

@@ -29,7 +29,7 @@ EXPORTED = (
     "brsvd_scale_cols", "brsvd_rsvd_stream", "brsvd_residual", "brsvd_rsvd_blocked",
     "brsvd_rsvd_stream_blocked", "brsvd_ialm_blocked", "brsvd_sketch_product_scaled",
     "brsvd_absmax", "brsvd_range_finder", "brsvd_colmax_entries", "brsvd_stream_rows_pass",
-    "brsvd_normalize_f64",
+    "brsvd_normalize_f64", "brsvd_ialm_stream",
 )
 
 
@@ -130,6 +130,10 @@ def _declare(lib):
     lib.brsvd_stream_rows_pass.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, vp, i64, i64,
                                            vp, i64, vp, i64, i64, c_int, ctypes.POINTER(dbl)]
     lib.brsvd_normalize_f64.argtypes = [vp, vp, i64, i64, i64, c_int, vp, i64]
+    lib.brsvd_ialm_stream.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, c_int, u64,
+                                      vp, dbl, dbl, dbl, dbl, c_int, vp, c_int, vp, vp, vp,
+                                      c_int, ctypes.POINTER(i32), ctypes.POINTER(i32), vp, vp,
+                                      vp, vp]
     lib.brsvd_profile_begin.argtypes = [vp]
     lib.brsvd_profile_end.argtypes = [vp, ctypes.POINTER(BrsvdProfile)]
     for name in EXPORTED:

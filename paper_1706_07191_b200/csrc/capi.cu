@@ -8,6 +8,7 @@
 
 #include "pipeline.cuh"
 #include "rpca.cuh"
+#include "rpca_stream.cuh"
 #include "stream.cuh"
 #include "residual.cuh"
 
@@ -643,6 +644,49 @@ int brsvd_ialm_blocked(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n, int6
                              col_bounds, nblocks);
     lo.flush();
     so.flush();
+    BRSVD_CUDA(cudaStreamSynchronize(c.stream));
+    if (iterations) *iterations = r.iterations;
+    if (converged) *converged = r.converged ? 1 : 0;
+    return (int)kOk;
+  });
+}
+
+int brsvd_ialm_stream(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n, int64_t ldm,
+                      int dtype, int k, int p, int q, uint64_t seed, const void* omega,
+                      double lam, double mu0, double rho, double tol, int max_iterations,
+                      const int64_t* col_bounds, int nblocks, void* L, void* S, void* Y,
+                      int nslots, int32_t* iterations, int32_t* converged, double* residuals,
+                      double* mus, double* svd_seconds, double* iter_seconds) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && M != nullptr && L && S && Y, kErrArg, "NULL argument");
+    BRSVD_REQUIRE(residuals && mus && svd_seconds && iter_seconds, kErrArg,
+                  "history arrays are required");
+    BRSVD_REQUIRE(nblocks >= 1 && col_bounds != nullptr && col_bounds[0] == 0 &&
+                      col_bounds[nblocks] == n,
+                  kErrShape, "column blocks must tile [0, n)");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    const size_t es = esize(dtype);
+    BRSVD_REQUIRE(m >= 1 && n >= 1 && ldm >= m, kErrShape, "bad shape");
+    BRSVD_REQUIRE(k >= 1 && p >= 0 && k + p <= std::min(m, n), kErrConfig,
+                  "k + p exceeds min(m, n)");
+    BRSVD_REQUIRE(q >= 0, kErrConfig, "power exponent must be non-negative");
+    BRSVD_REQUIRE(rho > 1.0 && tol > 0.0 && max_iterations >= 1, kErrArg,
+                  "rho must exceed 1, tol and max_iterations must be positive");
+    BRSVD_REQUIRE(nslots >= 1, kErrArg, "nslots must be positive");
+    std::vector<int64_t> bounds(col_bounds, col_bounds + nblocks + 1);
+    InView ov(c, omega, n, k + p, n, es, omega ? BRSVD_HOST : BRSVD_DEVICE);
+    IalmOut r;
+    if (dtype == BRSVD_F64)
+      r = ialm_stream<double>(c, (const double*)M, m, n, ldm, k, p, q, seed,
+                              (const double*)ov.dptr, lam, mu0, rho, tol, max_iterations,
+                              bounds, (double*)L, (double*)S, (double*)Y, nslots, residuals,
+                              mus, svd_seconds, iter_seconds);
+    else
+      r = ialm_stream<float>(c, (const float*)M, m, n, ldm, k, p, q, seed,
+                             (const float*)ov.dptr, lam, mu0, rho, tol, max_iterations, bounds,
+                             (float*)L, (float*)S, (float*)Y, nslots, residuals, mus,
+                             svd_seconds, iter_seconds);
     BRSVD_CUDA(cudaStreamSynchronize(c.stream));
     if (iterations) *iterations = r.iterations;
     if (converged) *converged = r.converged ? 1 : 0;

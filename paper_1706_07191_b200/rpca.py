@@ -120,19 +120,87 @@ _IALM_RESIDENT_COPIES = 6
 
 
 def _require_device_room(payload_bytes):
-    """The IALM iterates stay in HBM (no host-streamed IALM is built): a store
-    whose iterates cannot be held on the device raises BudgetError up front
-    (store.py:42-47 semantics) instead of failing inside the loop."""
+    """In-memory inputs keep the IALM iterates in HBM: one whose iterates
+    cannot be held on the device raises BudgetError up front (store.py:42-47
+    semantics) instead of failing inside the loop (stores take the streamed
+    path instead, _ialm_stream)."""
     import torch
     free, _ = torch.cuda.mem_get_info(_lib.context().device)
     need = _IALM_RESIDENT_COPIES * int(payload_bytes)
     if need > free:
         raise BudgetError(
             f"IALM iterates of a {payload_bytes} B matrix need ~{need} B of device memory, "
-            f"{free} B free (host-streamed IALM is not implemented)", need)
+            f"{free} B free (pass a MatrixStore with a memory budget to stream it)", need)
 
 
-def ialm_rpca(m_input, cfg, omega=None):
+def _pinned_cm(m, n, dtype):
+    """Column-major (m x n) host array in page-locked memory when possible."""
+    try:
+        import torch
+        tdt = torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
+        return torch.empty((n, m), dtype=tdt, pin_memory=True).numpy().T
+    except (RuntimeError, ImportError):
+        return np.empty((m, n), dtype=dtype, order="F")
+
+
+def _ialm_stream(store, cfg, blocks, omega=None, nslots=2):
+    """The reference's out-of-core branch (_ialm_rpca_ooc, rpca.py:216-304)
+    with M, S and Y host-resident and streamed block by block
+    (brsvd_ialm_stream); returns L and S as stores like the reference."""
+    from .rsvd import _store_payload
+    m, n = store.m, store.n
+    dt = store.dtype
+    payload = _store_payload(store)          # read-only memory map, m x n, Fortran order
+    M = _pinned_cm(m, n, dt)
+    w0, b0 = store.stats.words_read, store.stats.block_reads
+    for j0, j1 in blocks:                    # one read of the store into pinned memory
+        M[:, j0:j1] = payload[:, j0:j1]
+    store.stats.words_read, store.stats.block_reads = w0 + m * n, b0 + len(blocks)
+    S = _pinned_cm(m, n, dt)
+    Y = _pinned_cm(m, n, dt)
+    L = _pinned_cm(m, n, dt)
+    maxit = int(cfg.max_iterations)
+    res, mus, svd_s, it_s = (np.zeros(maxit) for _ in range(4))
+    iters, conv = ctypes.c_int32(), ctypes.c_int32()
+    l = int(cfg.target_rank) + int(cfg.oversampling)
+    om, optr = None, None
+    if omega is not None:
+        if tuple(np.shape(omega)) != (n, l):
+            raise ValueError(f"omega has shape {np.shape(omega)}, expected ({n}, {l})")
+        om = np.asfortranarray(np.asarray(omega), dtype=dt)
+        optr = ctypes.c_void_p(om.ctypes.data)
+    edges = [int(blocks[0][0])] + [int(j1) for _, j1 in blocks]
+    bounds = (ctypes.c_int64 * len(edges))(*edges)
+    nan = float("nan")
+    dptr = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    _lib.check(_require("brsvd_ialm_stream")(
+        _lib.context().handle, dptr(M), m, n, m, _lib.dtype_code(dt),
+        int(cfg.target_rank), int(cfg.oversampling), int(cfg.power_exponent),
+        ctypes.c_uint64(int(cfg.master_seed) & (2 ** 64 - 1)), optr,
+        ctypes.c_double(nan if cfg.lam is None else float(cfg.lam)),
+        ctypes.c_double(nan if cfg.mu0 is None else float(cfg.mu0)),
+        ctypes.c_double(float(cfg.rho)), ctypes.c_double(float(cfg.tol)), maxit,
+        bounds, len(edges) - 1, dptr(L), dptr(S), dptr(Y), int(nslots),
+        ctypes.byref(iters), ctypes.byref(conv), dptr(res), dptr(mus), dptr(svd_s),
+        dptr(it_s)))
+    k = iters.value
+    history = [{"i": i + 1, "mu": float(mus[i]), "residual": float(res[i]),
+                "svd_seconds": float(svd_s[i]), "iter_seconds": float(it_s[i])}
+               for i in range(k)]
+    workdir = tempfile.mkdtemp(prefix="rpca_")
+    Ls = MatrixStore.from_array(os.path.join(workdir, "lowrank.oocm"), L)
+    Ss = MatrixStore.from_array(os.path.join(workdir, "sparse.oocm"), S)
+    return RpcaResult(L=Ls, S=Ss, iterations=k, residual_history=[float(r) for r in res[:k]],
+                      converged=bool(conv.value), history=history)
+
+
+def _device_room(payload_bytes):
+    import torch
+    free, _ = torch.cuda.mem_get_info(_lib.context().device)
+    return _IALM_RESIDENT_COPIES * int(payload_bytes) <= free
+
+
+def ialm_rpca(m_input, cfg, omega=None, stream=None):
     """Inexact-ALM robust PCA with a randomized inner SVD (rpca.py:153-213).
 
     Non-convergence at max_iterations returns ``converged=False``.  numpy (or
@@ -141,7 +209,10 @@ def ialm_rpca(m_input, cfg, omega=None):
     (store payload above ``memory_budget_bytes``, rpca.py:160-163) the split
     is returned as MatrixStore objects as it does.  ``omega`` optionally
     injects the n x (k+p) sketch used by every inner SVD (parity runs pass the
-    reference's ``gaussian_matrix(n, k+p, seed, 0, dtype)``).
+    reference's ``gaussian_matrix(n, k+p, seed, 0, dtype)``).  ``stream``
+    (out-of-core branch only): True streams M, S, Y from host memory block by
+    block every pass (brsvd_ialm_stream); None does so when the iterates do not
+    fit in device memory, else they are held in HBM.
     """
     cfg.validate()
     as_stores = False
@@ -157,6 +228,12 @@ def ialm_rpca(m_input, cfg, omega=None):
             plan = plan_blocks(m_input.n, m_input.m, l_, m_input.element_size,
                                memory_budget_bytes=budget)
             blocks = list(plan)
+            # iterates that fit in HBM stay there (one read of the store);
+            # beyond that (or stream=True) M, S, Y are streamed per pass
+            if stream is None:
+                stream = not _device_room(m_input.payload_bytes)
+            if stream:
+                return _ialm_stream(m_input, cfg, blocks, omega)
         _require_device_room(m_input.payload_bytes)
         m_input = m_input.read_full()
     device = is_torch(m_input)
