@@ -38,6 +38,21 @@ __global__ void lat_div(double* out, double a, int iters, long long* cyc) {
   long long t1 = clock64();
   if (threadIdx.x == 0) { *cyc = t1 - t0; out[0] = x; }
 }
+// DMMA (mma.sync m8n8k4 f64) throughput: 8 independent accumulators per warp
+__global__ void tput_dmma(double* out, double a, double b, int iters) {
+  double c[8][2];
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = a + threadIdx.x + i;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[j][0]), "+d"(c[j][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+// DFMA throughput with W warps per SM (occupancy sweep)
 int main() {
   double* d; long long* c; float* f;
   cudaMalloc(&d, 1 << 24); cudaMalloc(&c, 64); cudaMalloc(&f, 1 << 24);
@@ -61,6 +76,20 @@ int main() {
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
     printf("FFMA throughput: %.1f TFLOP/s\n", 2.0 * 8 * 4000 * 148.0 * 4 * 512 / (ms * 1e-3) / 1e12);
+    for (int thr : {64, 128, 256, 512}) {
+      cudaEventRecord(e0);
+      tput_dmma<<<148, thr>>>(d, 1.0, 0.999, 4000);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+      printf("DMMA throughput (%d warps/SM): %.1f TFLOP/s\n", thr / 32,
+             2.0 * 256 * 8 * 4000 * 148.0 * (thr / 32) / (ms * 1e-3) / 1e12);
+      cudaEventRecord(e0);
+      tput_dfma<<<148, thr>>>(d, 1.0, 0.999, 4000);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+      printf("DFMA throughput (%d warps/SM): %.1f TFLOP/s\n", thr / 32,
+             2.0 * 8 * 4000 * 148.0 * thr / (ms * 1e-3) / 1e12);
+    }
   }
   return 0;
 }
