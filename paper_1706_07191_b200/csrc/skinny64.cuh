@@ -234,9 +234,217 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// DMMA variant (fp64 tensor core, mma.sync m8n8k4): same 128-row x 32-k A
+// tiles through the same 4-stage cp.async ring, but each of the 8 warps owns
+// 16 rows of op(A) (two m8 blocks) and every column block (LB8 / 8 n8 blocks)
+// over the whole k range of the tile, so there is no k-group reduction; the
+// fp64 tensor pipe issues one instruction per 256 FMAs (the SIMT kernel needs
+// eight), which is what keeps it fed at 8 warps per SM (scripts/micro:
+// 36.6 TF/s DMMA vs 33 TF/s DFMA at 8 warps).  Shared-memory pitches are
+// padded so each fragment load is two wavefronts: KC rows 36 doubles, MC
+// k-rows 132, the B slice LB8 + 4.
+template <bool KC, int LB8>
+struct DLayout {
+  // 128 rows x 32 k tiles (32 KB of A): KC rows are 256-byte DRAM runs, MC
+  // k-rows 1 KB runs.  (64 x 64 KC tiles -- 512-byte runs -- measured no
+  // faster at config 5, and 12 % slower for the transposed column-major case.)
+  static constexpr bool WIDE = false;
+  static constexpr int ROWS = WIDE ? 64 : 128;
+  static constexpr int KT = WIDE ? 64 : 32;
+  static constexpr int MB = ROWS / 64;               // m8 blocks per warp
+  static constexpr int NB = LB8 / 8;                 // n8 blocks
+  static constexpr int LBP = LB8 + 4;                // B slice pitch (doubles)
+  static constexpr int APITCH = KC ? KT + 4 : ROWS + 4;   // row (KC) / k-row (MC) pitch
+  static constexpr int a_elems = KC ? ROWS * APITCH : KT * APITCH;
+  static constexpr int b_elems = KT * LBP;
+  static constexpr int stage_elems = a_elems + b_elems;
+  static constexpr size_t smem = sizeof(double) * (size_t)stage_elems * kStages;
+  static_assert(smem <= 227 * 1024, "shared-memory ring exceeds the opt-in limit");
+};
+
+// Bt (K x LBP, row-major, zero beyond l) <- B (K x l, column-major)
+template <int LBP>
+__global__ void pack_bp_kernel(const double* __restrict__ B, int64_t ldb, int64_t K, int l,
+                               double* __restrict__ Bt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < K * LBP;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % LBP);
+    const int64_t k = e / LBP;
+    Bt[e] = c < l ? B[k + (int64_t)c * ldb] : 0.0;
+  }
+}
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, "
+               "{%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <bool KC, int LB8>
+__global__ void __launch_bounds__(kThreads)
+    skinny_dmma_kernel(const double* __restrict__ A, int64_t M, int64_t K, int64_t lda,
+                       const double* __restrict__ Bt, int l, int64_t kchunk,
+                       double* __restrict__ C, int64_t ldc, double* __restrict__ part) {
+  using L = DLayout<KC, LB8>;
+  constexpr int NB = L::NB, MB = L::MB, LBP = L::LBP, AP = L::APITCH;
+  constexpr int ROWS = L::ROWS, KT = L::KT;
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t i0 = (int64_t)blockIdx.x * ROWS;
+  const int64_t kb = (int64_t)blockIdx.y * kchunk;
+  const int64_t ke = min(K, kb + kchunk);
+  const int nt = (int)((ke - kb + KT - 1) / KT);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
+
+  // A-tile copy plan (16-byte pieces): every thread moves APT pieces of one
+  // column of pieces, addresses a per-thread base plus a constant stride
+  constexpr int APT = ROWS * KT / 2 / kThreads;
+  constexpr int PPR = KC ? KT / 2 : ROWS / 2;    // pieces per tile row (KC) / k row (MC)
+  constexpr int LPJ = kThreads / PPR;            // tile rows (KC) / k rows (MC) per j
+  const int pc = tid % PPR, pl = tid / PPR;
+  const double* abase;
+  int64_t astride;
+  uint32_t adst0, rowmask = 0;
+  int mc_bytes = 0;
+  if (KC) {
+    abase = A + (i0 + pl) * lda + 2 * pc;
+    astride = (int64_t)LPJ * lda;
+    adst0 = (uint32_t)(pl * AP + 2 * pc) * 8u;
+#pragma unroll
+    for (int j = 0; j < APT; ++j)
+      if (i0 + pl + LPJ * j < M) rowmask |= 1u << j;
+  } else {
+    const int64_t row = i0 + 2 * pc;
+    mc_bytes = row < M ? (row + 1 < M ? 16 : 8) : 0;
+    abase = A + row + (int64_t)pl * lda;
+    astride = (int64_t)LPJ * lda;
+    adst0 = (uint32_t)(pl * AP + 2 * pc) * 8u;
+  }
+  auto issue = [&](int t) {
+    const int slot = t % kStages;
+    const int64_t k0 = kb + (int64_t)t * KT;
+    const uint32_t sa = sbase + (uint32_t)(slot * L::stage_elems) * 8u;
+    if (KC) {
+      const int64_t kp = k0 + 2 * pc;
+      const int kbytes = kp < ke ? (kp + 1 < ke ? 16 : 8) : 0;
+      const double* src = abase + k0;
+#pragma unroll
+      for (int j = 0; j < APT; ++j) {
+        const int bytes = ((rowmask >> j) & 1u) ? kbytes : 0;
+        cp_async16(sa + adst0 + (uint32_t)(j * LPJ * AP) * 8u, bytes ? src + j * astride : A,
+                   bytes);
+      }
+    } else {
+      const double* src = abase + k0 * lda;
+#pragma unroll
+      for (int j = 0; j < APT; ++j) {
+        const int bytes = (k0 + pl + LPJ * j < ke) ? mc_bytes : 0;
+        cp_async16(sa + adst0 + (uint32_t)(j * LPJ * AP) * 8u, bytes ? src + j * astride : A,
+                   bytes);
+      }
+    }
+    const uint32_t sb = sa + (uint32_t)L::a_elems * 8u;
+    for (int p = tid; p < KT * LBP / 2; p += kThreads) {
+      const int64_t k = k0 + p / (LBP / 2);
+      const int bytes = k < ke ? 16 : 0;
+      cp_async16(sb + (uint32_t)(2 * p) * 8u, bytes ? Bt + k0 * LBP + 2 * p : Bt, bytes);
+    }
+  };
+
+  double acc[MB][NB][2];
+#pragma unroll
+  for (int u = 0; u < MB; ++u)
+#pragma unroll
+    for (int v = 0; v < NB; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < nt) issue(s);
+    cp_async_commit();
+  }
+  const int fr = lane >> 2, fk = lane & 3;
+  const int rbase = warp * (8 * MB) + fr;
+  for (int t = 0; t < nt; ++t) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    if (t + kStages - 1 < nt) issue(t + kStages - 1);
+    cp_async_commit();
+    const double* st = sm + (t % kStages) * L::stage_elems;
+    const double* bs = st + L::a_elems;
+#pragma unroll 4
+    for (int k4 = 0; k4 < KT; k4 += 4) {
+      const int kk = k4 + fk;
+      double a[MB], b[NB];
+#pragma unroll
+      for (int u = 0; u < MB; ++u)
+        a[u] = KC ? st[(rbase + 8 * u) * AP + kk] : st[kk * AP + rbase + 8 * u];
+#pragma unroll
+      for (int v = 0; v < NB; ++v) b[v] = bs[kk * LBP + 8 * v + fr];
+#pragma unroll
+      for (int u = 0; u < MB; ++u)
+#pragma unroll
+        for (int v = 0; v < NB; ++v) dmma884(acc[u][v][0], acc[u][v][1], a[u], b[v]);
+    }
+  }
+  cp_async_wait<0>();
+  double* out = part ? part + (int64_t)blockIdx.y * M * l : C;
+  const int64_t ld = part ? M : ldc;
+#pragma unroll
+  for (int u = 0; u < MB; ++u) {
+    const int64_t i = i0 + warp * (8 * MB) + 8 * u + fr;
+    if (i >= M) continue;
+#pragma unroll
+    for (int v = 0; v < NB; ++v)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int cc = 8 * v + 2 * fk + e;
+        if (cc < l) out[i + (int64_t)cc * ld] = acc[u][v][e];
+      }
+  }
+}
+
+template <bool KC, int LB8>
+void launch_dmma(Ctx& c, const double* A, int64_t M, int64_t K, int64_t lda, const double* B,
+                 int64_t ldb, int l, double* C, int64_t ldc) {
+  using L = DLayout<KC, LB8>;
+  DBuf<double> Bt(c, (size_t)(K * L::LBP));
+  pack_bp_kernel<L::LBP><<<grid_for(K * L::LBP), 256, 0, c.stream>>>(B, ldb, K, l, Bt.p);
+  BRSVD_CHECK_LAUNCH();
+  const int64_t blocks = ceil_div(M, (int64_t)L::ROWS);
+  int64_t splits = std::max<int64_t>(1, ceil_div(16 * (int64_t)c.num_sms, blocks));
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, K / 256));
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, K / (8 * (int64_t)l)));
+  int64_t kchunk = ceil_div(ceil_div(K, splits), (int64_t)L::KT) * L::KT;
+  splits = std::max<int64_t>(1, ceil_div(K, kchunk));
+  DBuf<double> part;
+  if (splits > 1) part.alloc(c, (size_t)(splits * M * l));
+  const size_t smem = L::smem;
+  BRSVD_CUDA(cudaFuncSetAttribute(skinny_dmma_kernel<KC, LB8>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  skinny_dmma_kernel<KC, LB8><<<dim3((unsigned)blocks, (unsigned)splits), kThreads, smem,
+                                c.stream>>>(A, M, K, lda, Bt.p, l, kchunk, C, ldc, part.p);
+  BRSVD_CHECK_LAUNCH();
+  if (splits > 1) {
+    splitk_reduce_kernel<double, double><<<grid_for(M * l), 256, 0, c.stream>>>(
+        M, l, (int)splits, part.p, C, 1, ldc, 1.0, 0.0, nullptr, 0, 0);
+    BRSVD_CHECK_LAUNCH();
+  }
+}
+
+inline bool skinny_simt_forced() {
+  const char* e = std::getenv("BRSVD_SKINNY_SIMT");
+  return e && e[0] == '1';
+}
+
 template <bool KC, int LB>
 void launch(Ctx& c, const double* A, int64_t M, int64_t K, int64_t lda, const double* B,
             int64_t ldb, int l, double* C, int64_t ldc) {
+  if (LB >= 8 && !skinny_simt_forced()) {   // l > 4: the DMMA kernel
+    constexpr int LB8 = LB < 8 ? 8 : ((LB + 7) / 8) * 8;
+    launch_dmma<KC, LB8>(c, A, M, K, lda, B, ldb, l, C, ldc);
+    return;
+  }
   DBuf<double> Bt(c, (size_t)(K * LB));
   pack_b_kernel<LB><<<grid_for(K * LB), 256, 0, c.stream>>>(B, ldb, K, l, Bt.p);
   BRSVD_CHECK_LAUNCH();

@@ -92,6 +92,101 @@ struct PanelStreamer {
   }
 };
 
+// Z (fp64, ldz) += op(A) X, op(A) = A^T (trans) or A: the product's magnitude
+// is carried into the fp64 sum -- for fp32 data the fp16-split product is
+// left in its power-of-two row / column scales (tc_gemm_launch scales_out)
+// and unscaled in fp64 by the accumulation, so no fp32 over- or underflow
+// can occur in the partial product and no host-known scale is needed.
+__global__ void accum_unscaled_kernel(const float* __restrict__ P, int64_t rows, int cols,
+                                      int64_t ldp, const float* __restrict__ scales,
+                                      double* __restrict__ Z, int64_t ldz) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % rows, j = idx / rows;
+    double v = (double)P[i + j * ldp];
+    if (scales) v *= (double)scales[i] * (double)scales[rows + j];
+    Z[i + j * ldz] += v;
+  }
+}
+
+template <typename T>
+__global__ void accum_f64_kernel(const T* __restrict__ P, int64_t rows, int cols, int64_t ldp,
+                                 double* __restrict__ Z, int64_t ldz) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % rows, j = idx / rows;
+    Z[i + j * ldz] += (double)P[i + j * ldp];
+  }
+}
+
+template <typename T>
+void product_accum(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool row_major,
+                   bool trans, const T* X, int64_t ldx, int l, T* tmp, float* scales,
+                   double* Z, int64_t ldz) {
+  const int64_t rows = trans ? n : m;
+  if constexpr (sizeof(T) == 4) {
+    if (scales != nullptr && tc_gemm_supported<float>(c, A, lda, m, n, l) &&
+        tc::h16_enabled()) {
+      tc_gemm_launch<float>(c, A, m, n, lda, row_major, trans, X, ldx, l, tmp, rows, 0,
+                            nullptr, nullptr, scales);
+      accum_unscaled_kernel<<<grid_for(rows * l), 256, 0, c.stream>>>(tmp, rows, l, rows,
+                                                                      scales, Z, ldz);
+      BRSVD_CHECK_LAUNCH();
+      return;
+    }
+  }
+  if (trans) big_tn<T>(c, A, m, n, lda, row_major, X, ldx, l, tmp, rows);
+  else big_nn<T>(c, A, m, n, lda, row_major, X, ldx, l, tmp, rows);
+  accum_f64_kernel<T><<<grid_for(rows * l), 256, 0, c.stream>>>(tmp, rows, l, rows, Z, ldz);
+  BRSVD_CHECK_LAUNCH();
+}
+
+// Z (n x l, fp64) -> a conditioned basis of its span in the data's precision
+// (the power iteration's basis change, normalize_sketch): fp32 data first
+// takes Z to unit order by a power of two (exact) so any magnitude the fp64
+// sum holds fits fp32; fp64 data is unit-scaled inside normalize_sketch.
+template <typename T>
+void normalize_from_f64(Ctx& c, const double* Z, int64_t n, int l, int64_t ldz, T* Zout,
+                        int64_t ldo) {
+  if constexpr (sizeof(T) == 8) {
+    normalize_sketch<double>(c, Z, n, l, ldz, Zout, ldo, nullptr, /*scale_check=*/true);
+  } else {
+    const MaxAbs pk = maxabs<double>(c, Z, n, l, ldz);
+    if (pk.nonfinite)
+      throw Error(kErrOverflow, "sample matrix is not finite; the overflow guard fires");
+    double s = 1.0;
+    if (pk.peak > 0.0) {
+      int e;
+      std::frexp(pk.peak, &e);
+      s = std::ldexp(1.0, -e);
+    }
+    DBuf<float> Zs(c, (size_t)n * l);
+    scale_cast_kernel<double, float><<<grid_for(n * l), 256, 0, c.stream>>>(Z, n, l, ldz, Zs.p,
+                                                                            n, s);
+    BRSVD_CHECK_LAUNCH();
+    normalize_sketch<float>(c, Zs.p, n, l, n, reinterpret_cast<float*>(Zout), ldo);
+  }
+}
+
+// Y (T, m x l) = 2^-e Y64 with 2^e the order of max |Y64| (exact); returns the
+// unscaled peak (max |Y64|, +inf when not finite).
+template <typename T>
+double unit_cast(Ctx& c, const double* Y64, int64_t m, int l, T* Y, int64_t ldy) {
+  const MaxAbs pk = maxabs<double>(c, Y64, m, l, m);
+  if (pk.nonfinite) return INFINITY;
+  double s = 1.0;
+  if (pk.peak > 0.0) {
+    int e;
+    std::frexp(pk.peak, &e);
+    s = std::ldexp(1.0, -e);
+  }
+  scale_cast_kernel<double, T><<<grid_for(m * l), 256, 0, c.stream>>>(Y64, m, l, m, Y, ldy, s);
+  BRSVD_CHECK_LAUNCH();
+  return pk.peak;
+}
+
 // block_power (column panels only): the paper's two-pass scheme -- each panel
 // J runs its whole power iteration (A_J A_J^T)^q A_J Omega_J while resident,
 // the block samples are summed (block_range_finder, rsvd.py:150-185), then the
@@ -120,32 +215,25 @@ RsvdInfo rsvd_stream(Ctx& c, const T* Ah, int64_t m, int64_t n, int64_t lda, boo
   DBuf<T> tmpY(c, row_major ? (size_t)1 : (size_t)m * l);
   int passes = 0;
   double peak0 = 0.0;
+  // A^T Y (row panels) and A_J (A_J^T Yn) (column panels) are summed in fp64
+  // with the partial products' magnitudes carried exactly (product_accum), so
+  // inputs of any magnitude stream without under- or overflow and no scale
+  // has to be fixed from a first panel; the sums are brought back to unit
+  // order before the basis change.
+  DBuf<double> acc64(c, (size_t)std::max(m, n) * l);
+  DBuf<float> scales(c, (size_t)(std::max(m, n) + l));
+  DBuf<T> tmpP(c, (size_t)std::max(m, n) * l);
   if (row_major) {
     // pass 0: Y_i = A_i Omega (+ first power step Z = sum A_i^T Y_i)
     for (int it = 0; it <= q; ++it) {
       const T* Xin = it == 0 ? X : Zn.p;
       const bool more = it < q;
-      if (more) BRSVD_CUDA(cudaMemsetAsync(Z.p, 0, sizeof(T) * n * l, c.stream));
-      // A^T Y is accumulated at a power-of-two scale fixed by the first
-      // panel's max |Y_i| (fp32 inputs far from unit magnitude would
-      // otherwise underflow / overflow in Z; Z is renormalised right after)
-      double zscale = 1.0;
-      bool zscale_set = false;
+      if (more) BRSVD_CUDA(cudaMemsetAsync(acc64.p, 0, sizeof(double) * n * l, c.stream));
       ps.pass([&](const T* Ap, int64_t ld, int64_t r0, int64_t r1) {
         big_nn<T>(c, Ap, r1 - r0, n, ld, true, Xin, n, l, Y.p + r0, m);
-        if (more) {
-          if (sizeof(T) == 4 && !zscale_set) {
-            const MaxAbs pk = maxabs<T>(c, Y.p + r0, r1 - r0, l, m);
-            if (pk.peak > 0.0 && std::isfinite(pk.peak)) {
-              int e;
-              std::frexp(pk.peak, &e);
-              zscale = std::ldexp(1.0, -e);
-            }
-            zscale_set = true;
-          }
-          big_tn<T>(c, Ap, r1 - r0, n, ld, true, Y.p + r0, m, l, tmpZ.p, n, nullptr, zscale);
-          axpy<T>(c, tmpZ.p, n, l, n, Z.p, n);
-        }
+        if (more)
+          product_accum<T>(c, Ap, r1 - r0, n, ld, true, /*trans=*/true, Y.p + r0, m, l,
+                           tmpP.p, scales.p, acc64.p, n);
       });
       ++passes;
       if (it == 0) {
@@ -157,59 +245,38 @@ RsvdInfo rsvd_stream(Ctx& c, const T* Ah, int64_t m, int64_t n, int64_t lda, boo
           return info;
         }
       }
-      if (more)
-        normalize_sketch<T>(c, Z.p, n, l, n, Zn.p, n, nullptr,
-                            sizeof(T) == 8 && (peak0 > 0x1p150 ||
-                                               (peak0 > 0.0 && peak0 < 0x1p-150)));
+      if (more) normalize_from_f64<T>(c, acc64.p, n, l, n, Zn.p, n);
     }
   } else {
     // column panels: Y = sum_J A_J Omega_J, then Y' = sum_J A_J (A_J^T Yn)
-    DBuf<T> Yn(c, (size_t)m * l), Ynew(c, (size_t)m * l);
+    DBuf<T> Yn(c, (size_t)m * l);
     const int iters = block_power ? 0 : q;
     for (int it = 0; it <= iters; ++it) {
-      T* acc = it == 0 ? Y.p : Ynew.p;
-      BRSVD_CUDA(cudaMemsetAsync(acc, 0, sizeof(T) * m * l, c.stream));
-      if (it > 0)
-        normalize_sketch<T>(c, Y.p, m, l, m, Yn.p, m, nullptr,
-                            sizeof(T) == 8 && (peak0 > 0x1p150 ||
-                                               (peak0 > 0.0 && peak0 < 0x1p-150)));
-      // A_J^T Yn at a power-of-two scale fixed by the first block (fp32
-      // inputs far from unit magnitude would under/overflow A_J A_J^T Yn;
-      // the sum is renormalised in the next iteration)
-      double zscale = 1.0;
-      bool zscale_set = false;
+      BRSVD_CUDA(cudaMemsetAsync(acc64.p, 0, sizeof(double) * m * l, c.stream));
+      if (it > 0) normalize_sketch<T>(c, Y.p, m, l, m, Yn.p, m);
       ps.pass([&](const T* Ap, int64_t ld, int64_t j0, int64_t j1) {
         const int64_t w = j1 - j0;
-        if (it > 0 && sizeof(T) == 4 && !zscale_set) {
-          big_tn<T>(c, Ap, m, w, ld, false, Yn.p, m, l, tmpZ.p, pmax);
-          const MaxAbs pk = maxabs<T>(c, tmpZ.p, w, l, pmax);
-          if (pk.peak > 0.0 && std::isfinite(pk.peak)) {
-            int e;
-            std::frexp(pk.peak, &e);
-            zscale = std::ldexp(1.0, -e);
-          }
-          zscale_set = true;
-        }
         if (it == 0) {
           big_nn<T>(c, Ap, m, w, ld, false, X + j0, n, l, tmpY.p, m);
           for (int pw = 0; block_power && pw < q; ++pw) {
             big_tn<T>(c, Ap, m, w, ld, false, tmpY.p, m, l, tmpZ.p, pmax);
             big_nn<T>(c, Ap, m, w, ld, false, tmpZ.p, pmax, l, tmpY.p, m);
           }
+          accum_f64_kernel<T><<<grid_for(m * l), 256, 0, c.stream>>>(tmpY.p, m, l, m,
+                                                                     acc64.p, m);
+          BRSVD_CHECK_LAUNCH();
         } else {
-          big_tn<T>(c, Ap, m, w, ld, false, Yn.p, m, l, tmpZ.p, pmax, nullptr, zscale);
-          big_nn<T>(c, Ap, m, w, ld, false, tmpZ.p, pmax, l, tmpY.p, m);
+          big_tn<T>(c, Ap, m, w, ld, false, Yn.p, m, l, tmpZ.p, pmax);   // Yn unit columns
+          product_accum<T>(c, Ap, m, w, ld, false, /*trans=*/false, tmpZ.p, pmax, l, tmpP.p,
+                           scales.p, acc64.p, m);
         }
-        axpy<T>(c, tmpY.p, m, l, m, acc, m);
       });
       ++passes;
-      if (it > 0)
-        BRSVD_CUDA(cudaMemcpyAsync(Y.p, Ynew.p, sizeof(T) * m * l, cudaMemcpyDeviceToDevice,
-                                   c.stream));
+      const double pk = unit_cast<T>(c, acc64.p, m, l, Y.p, m);
       if (it == 0) {
-        const MaxAbs p0 = maxabs<T>(c, Y.p, m, l, m);
-        peak0 = p0.peak;
-        if (p0.nonfinite) {
+        peak0 = pk;
+        // the reference's sample lives in the data's precision (rsvd.py:84-91)
+        if (!(pk <= (double)finfo_max<T>())) {
           info.overflow = true;
           info.log10_peak = INFINITY;
           return info;
@@ -275,30 +342,6 @@ RsvdInfo rsvd_stream(Ctx& c, const T* Ah, int64_t m, int64_t n, int64_t lda, boo
 // power-of-two row/column scales and unscaled into the fp64 sum, so Z holds
 // inputs of any fp32 magnitude without over- or underflow and no host-side
 // scale has to be known before the pass.
-__global__ void accum_unscaled_kernel(const float* __restrict__ P, int64_t rows, int cols,
-                                      int64_t ldp, const float* __restrict__ scales,
-                                      double* __restrict__ Z, int64_t ldz) {
-  const int64_t total = rows * cols;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = idx % rows, j = idx / rows;
-    double v = (double)P[i + j * ldp];
-    if (scales) v *= (double)scales[i] * (double)scales[rows + j];
-    Z[i + j * ldz] += v;
-  }
-}
-
-template <typename T>
-__global__ void accum_f64_kernel(const T* __restrict__ P, int64_t rows, int cols, int64_t ldp,
-                                 double* __restrict__ Z, int64_t ldz) {
-  const int64_t total = rows * cols;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = idx % rows, j = idx / rows;
-    Z[i + j * ldz] += (double)P[i + j * ldp];
-  }
-}
-
 struct PassInfo {
   int64_t panels = 0;
   double ms = 0.0;     // pass time on the compute stream
@@ -325,52 +368,14 @@ PassInfo stream_rows_pass(Ctx& c, const T* Ah, int64_t m, int64_t n, int64_t lda
   ps.pass([&](const T* Ap, int64_t ld, int64_t r0, int64_t r1) {
     const int64_t rows = r1 - r0;
     if (X != nullptr) big_nn<T>(c, Ap, rows, n, ld, row_major, X, ldx, l, Y + r0, ldy);
-    if (Z == nullptr) return;
-    if constexpr (sizeof(T) == 4) {
-      if (tc_gemm_supported<float>(c, Ap, ld, rows, n, l) && tc::h16_enabled()) {
-        tc_gemm_launch<float>(c, Ap, rows, n, ld, row_major, /*trans=*/true, Y + r0, ldy, l,
-                              tmp.p, n, 0, nullptr, nullptr, scales.p);
-        accum_unscaled_kernel<<<grid_for(n * l), 256, 0, c.stream>>>(tmp.p, n, l, n,
-                                                                     scales.p, Z, ldz);
-        BRSVD_CHECK_LAUNCH();
-        return;
-      }
-    }
-    big_tn<T>(c, Ap, rows, n, ld, row_major, Y + r0, ldy, l, tmp.p, n);
-    accum_f64_kernel<T><<<grid_for(n * l), 256, 0, c.stream>>>(tmp.p, n, l, n, Z, ldz);
-    BRSVD_CHECK_LAUNCH();
+    if (Z != nullptr)
+      product_accum<T>(c, Ap, rows, n, ld, row_major, /*trans=*/true, Y + r0, ldy, l, tmp.p,
+                       scales.p, Z, ldz);
   });
   ev.rec(1, c.stream);
   pi.panels = ps.count();
   pi.ms = ev.ms(0, 1);
   return pi;
-}
-
-// Z (n x l, fp64) -> a conditioned basis of its span in the data's precision
-// (the power iteration's basis change, normalize_sketch): fp32 data first
-// takes Z to unit order by a power of two (exact) so any magnitude the fp64
-// sum holds fits fp32; fp64 data is unit-scaled inside normalize_sketch.
-template <typename T>
-void normalize_from_f64(Ctx& c, const double* Z, int64_t n, int l, int64_t ldz, T* Zout,
-                        int64_t ldo) {
-  if constexpr (sizeof(T) == 8) {
-    normalize_sketch<double>(c, Z, n, l, ldz, Zout, ldo, nullptr, /*scale_check=*/true);
-  } else {
-    const MaxAbs pk = maxabs<double>(c, Z, n, l, ldz);
-    if (pk.nonfinite)
-      throw Error(kErrOverflow, "sample matrix is not finite; the overflow guard fires");
-    double s = 1.0;
-    if (pk.peak > 0.0) {
-      int e;
-      std::frexp(pk.peak, &e);
-      s = std::ldexp(1.0, -e);
-    }
-    DBuf<float> Zs(c, (size_t)n * l);
-    scale_cast_kernel<double, float><<<grid_for(n * l), 256, 0, c.stream>>>(Z, n, l, ldz, Zs.p,
-                                                                            n, s);
-    BRSVD_CHECK_LAUNCH();
-    normalize_sketch<float>(c, Zs.p, n, l, n, reinterpret_cast<float*>(Zout), ldo);
-  }
 }
 
 }  // namespace brsvd
