@@ -43,6 +43,7 @@
 #include <utility>
 
 #include "tc_gemm.cuh"
+#include "tc_pair.cuh"
 
 namespace brsvd {
 namespace tcs {
@@ -828,6 +829,10 @@ inline void tc_product(Ctx& c, const float* A, int64_t m, int64_t n, int64_t lda
   if (tcs_gemm_launch(c, A, m, n, lda, row_major, trans, X, ldx, l, C, ldc, opa_max,
                       out_scale))
     return;
+  if (tcp::enabled() && tc::h16_enabled() && tcp::tcp_fits(l)) {
+    tcp_gemm_launch(c, A, m, n, lda, row_major, trans, X, ldx, l, C, ldc, opa_max, out_scale);
+    return;
+  }
   tc_gemm_launch<float>(c, A, m, n, lda, row_major, trans, X, ldx, l, C, ldc, 0, nullptr,
                         opa_max, nullptr, out_scale);
 }
