@@ -11,6 +11,7 @@ one subcommand per probe; run under gpurun, results on stdout).
     python scripts/probe.py sharded    # row-sharded driver at world size 1 vs single GPU
     python scripts/probe.py tcs [FLAGS...]  # product-kernel variants (BRSVD_TCS_FLAGS)
     python scripts/probe.py bias       # bias of tensor-core fp32 accumulation
+    python scripts/probe.py lsweep     # config-2 product time against l
 """
 
 import json
@@ -255,6 +256,19 @@ def tcs(argv):
         subprocess.run([sys.executable, __file__, "tcs", "child"], env=e)
 
 
+def lsweep(_):
+    """Config-2 product time against the sketch width l (MMA N per CTA chunk):
+    separates the per-MMA fixed cost from the N-proportional one."""
+    import torch
+    import bench
+    from paper_1706_07191_b200.rsvd import sketch_product
+    A = bench.make_matrix(torch.device("cuda:0"))
+    for l in (16, 32, 64, 96, 128, 160, 192, 256, 288, 320):
+        X = torch.randn(l, 32768, device="cuda").t()
+        ms = _time(lambda: sketch_product(A, X, False))
+        print(f"l={l:4d}: {ms:.3f} ms  {2 * 32768 ** 2 * l / ms / 1e9:.1f} TF/s")
+
+
 def bias(_):
     import torch
     from paper_1706_07191_b200.rsvd import sketch_product
@@ -269,7 +283,7 @@ def bias(_):
 
 
 if __name__ == "__main__":
-    cmds = {f.__name__: f for f in (box, h2d, products, e2e, c1, c5, scale, sharded, tcs, bias)}
+    cmds = {f.__name__: f for f in (box, h2d, products, e2e, c1, c5, scale, sharded, tcs, bias, lsweep)}
     if len(sys.argv) < 2 or sys.argv[1] not in cmds:
         print(__doc__)
         sys.exit(2)
