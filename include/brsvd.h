@@ -233,6 +233,14 @@ BRSVD_API int brsvd_spectral_norm(brsvd_ctx* ctx, const void* M, int64_t m, int6
                                   uint64_t seed, double tol, int max_iterations,
                                   double* out, int32_t* iterations);
 
+/* brsvd_spectral_norm from an injected start vector (host, n doubles; the
+ * reference's gaussian_matrix(n, 1, seed, stream_index=7) for parity, NULL:
+ * this library's stream-7 sketch column). */
+BRSVD_API int brsvd_spectral_norm_start(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n,
+                                        int64_t ldm, int dtype, int layout, int where,
+                                        uint64_t seed, const double* start, double tol,
+                                        int max_iterations, double* out, int32_t* iterations);
+
 /* Inexact-ALM robust PCA with the randomized SVD inside
  * (ialm_rpca / _ialm_rpca_incore, rpca.py:153-213).  lam / mu0 = NaN select
  * the defaults 1/sqrt(max(m, n)) and 1.25/||M||_2.  L and S (m x n, same

@@ -29,7 +29,7 @@ EXPORTED = (
     "brsvd_scale_cols", "brsvd_rsvd_stream", "brsvd_residual", "brsvd_rsvd_blocked",
     "brsvd_rsvd_stream_blocked", "brsvd_ialm_blocked", "brsvd_sketch_product_scaled",
     "brsvd_absmax", "brsvd_range_finder", "brsvd_colmax_entries", "brsvd_stream_rows_pass",
-    "brsvd_normalize_f64", "brsvd_ialm_stream",
+    "brsvd_normalize_f64", "brsvd_ialm_stream", "brsvd_spectral_norm_start",
 )
 
 
@@ -98,6 +98,9 @@ def _declare(lib):
     lib.brsvd_spectral_norm.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, u64,
                                         dbl, c_int, ctypes.POINTER(dbl),
                                         ctypes.POINTER(i32)]
+    lib.brsvd_spectral_norm_start.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, u64,
+                                              vp, dbl, c_int, ctypes.POINTER(dbl),
+                                              ctypes.POINTER(i32)]
     lib.brsvd_ialm.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, c_int, c_int,
                                c_int, u64, vp, dbl, dbl, dbl, dbl, c_int, vp, vp, c_int,
                                ctypes.POINTER(i32), ctypes.POINTER(i32), vp, vp, vp, vp]

@@ -564,6 +564,14 @@ int brsvd_gaussian(brsvd_ctx* ctx, void* out, int64_t rows, int64_t cols, int64_
 int brsvd_spectral_norm(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n, int64_t ldm,
                         int dtype, int layout, int where, uint64_t seed, double tol,
                         int max_iterations, double* out, int32_t* iterations) {
+  return brsvd_spectral_norm_start(ctx, M, m, n, ldm, dtype, layout, where, seed, nullptr, tol,
+                                   max_iterations, out, iterations);
+}
+
+int brsvd_spectral_norm_start(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n,
+                              int64_t ldm, int dtype, int layout, int where, uint64_t seed,
+                              const double* start, double tol, int max_iterations,
+                              double* out, int32_t* iterations) {
   return guarded([&] {
     BRSVD_REQUIRE(ctx != nullptr && out != nullptr, kErrArg, "NULL argument");
     Ctx& c = ctx->c;
@@ -578,10 +586,10 @@ int brsvd_spectral_norm(brsvd_ctx* ctx, const void* M, int64_t m, int64_t n, int
     double v;
     if (dtype == BRSVD_F64)
       v = spectral_norm<double>(c, (const double*)mv.dptr, m, n, sm, sn, seed, tol,
-                                max_iterations, &it);
+                                max_iterations, &it, start);
     else
       v = spectral_norm<float>(c, (const float*)mv.dptr, m, n, sm, sn, seed, tol,
-                               max_iterations, &it);
+                               max_iterations, &it, start);
     BRSVD_CUDA(cudaStreamSynchronize(c.stream));
     *out = v;
     if (iterations) *iterations = it;

@@ -117,10 +117,16 @@ void matvec(Ctx& c, const T* X, int64_t O, int64_t Kd, int64_t so, int64_t sk,
 // M (m x n): element (i, j) at M[i*sm + j*sn].  Returns 0 for a zero matrix.
 template <typename T>
 double spectral_norm(Ctx& c, const T* Mx, int64_t m, int64_t n, int64_t sm, int64_t sn,
-                     uint64_t seed, double tol, int max_it, int* iters_out) {
+                     uint64_t seed, double tol, int max_it, int* iters_out,
+                     const double* start = nullptr) {
   DBuf<double> v(c, n), u(c, m), nrm(c, 1);
-  gaussian_kernel<double><<<grid_for(n), 256, 0, c.stream>>>(v.p, n, 1, n, seed, 7, 0);
-  BRSVD_CHECK_LAUNCH();
+  if (start != nullptr) {   // injected start vector (host, n doubles)
+    BRSVD_CUDA(cudaMemcpyAsync(v.p, start, sizeof(double) * n, cudaMemcpyHostToDevice,
+                               c.stream));
+  } else {
+    gaussian_kernel<double><<<grid_for(n), 256, 0, c.stream>>>(v.p, n, 1, n, seed, 7, 0);
+    BRSVD_CHECK_LAUNCH();
+  }
   vec_norm2_kernel<<<1, 1024, 0, c.stream>>>(v.p, n, nrm.p);
   BRSVD_CHECK_LAUNCH();
   vec_scale_kernel<<<grid_for(n), 256, 0, c.stream>>>(v.p, n, nrm.p, 1);

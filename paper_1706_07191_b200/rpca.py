@@ -89,25 +89,36 @@ def _require(name):
     return getattr(lib, name)
 
 
-def spectral_norm_estimate(source, seed=0, tol=1e-10, max_iterations=100):
+def spectral_norm_estimate(source, seed=0, tol=1e-10, max_iterations=100, start=None):
     """Largest singular value by power iteration on M^T M (rpca.py:72-100).
 
-    Runs on the GPU; a zero matrix returns 0 with a warning.
+    Runs on the GPU; a zero matrix returns 0 with a warning.  ``start``
+    (n values) injects the start vector -- the reference's
+    ``gaussian_matrix(n, 1, seed, stream_index=7)[:, 0]`` for parity -- in place
+    of this library's stream-7 sketch column (it is normalised here, as the
+    reference does).
     """
     import warnings
     if isinstance(source, MatrixStore):
         source = source.read_full()
     mat = DeviceMatrix(source) if is_torch(source) else HostMatrix(source, "M")
     m, n = mat.shape
-    fn = _require("brsvd_spectral_norm")
+    fn = _require("brsvd_spectral_norm_start")
     ctx = _lib.context(getattr(mat, "device", None))
+    st = None
+    if start is not None:
+        st = np.ascontiguousarray(np.asarray(start, dtype=np.float64).reshape(-1))
+        if st.shape[0] != n:
+            from .kernels import ShapeError
+            raise ShapeError(f"start has {st.shape[0]} entries, expected {n}")
     if is_torch(source):
         ctx.set_stream(torch_stream_ptr(mat.t))
     out = ctypes.c_double()
     iters = ctypes.c_int32()
     _lib.check(fn(ctx.handle, mat.ptr, m, n, mat.ld, mat.code, mat.layout,
                   _lib.DEVICE if is_torch(source) else _lib.HOST,
-                  ctypes.c_uint64(int(seed) & (2 ** 64 - 1)), ctypes.c_double(tol),
+                  ctypes.c_uint64(int(seed) & (2 ** 64 - 1)),
+                  None if st is None else ctypes.c_void_p(st.ctypes.data), ctypes.c_double(tol),
                   int(max_iterations), ctypes.byref(out), ctypes.byref(iters)))
     if out.value == 0.0:
         warnings.warn("spectral_norm_estimate: zero matrix")

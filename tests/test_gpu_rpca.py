@@ -112,6 +112,25 @@ def test_spectral_norm_known_answers():
         assert spectral_norm_estimate(np.zeros((4, 4))) == 0.0
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_spectral_norm_matches_oracle_with_reference_start(dtype):
+    """spectral_norm_estimate (rpca.py:72-100) from the reference's own start
+    vector (gaussian_matrix(n, 1, seed, stream_index=7)) follows the
+    reference's power iteration: a random (slow-converging) matrix agrees with
+    the oracle to its stopping tolerance, not just to the 1 % of two different
+    starts."""
+    from oracle import ref_cpu
+    from paper_1706_07191_b200 import spectral_norm_estimate
+    rng = np.random.default_rng(31)
+    a = rng.standard_normal((400, 300)).astype(dtype)
+    v0 = ref_cpu.normal_sketch(300, 1, 5, 7, dtype=dtype)[:, 0]
+    ref = ref_cpu.power_norm(a, seed=5)
+    got = spectral_norm_estimate(a, seed=5, start=v0)
+    assert abs(got - ref) <= (1e-9 if dtype == np.float64 else 1e-5) * ref
+    got_c = spectral_norm_estimate(np.asfortranarray(a), seed=5, start=v0)
+    assert abs(got_c - got) <= 1e-12 * ref
+
+
 def test_store_paths(tmp_path):
     from paper_1706_07191_b200 import MatrixStore, RpcaConfig, ialm_rpca
     L0, S0, _ = planted(m=80, n=200, seed=12)
