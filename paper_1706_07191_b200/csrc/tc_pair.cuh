@@ -220,6 +220,9 @@ __global__ void __launch_bounds__(kThreadsP, 1)
         mbar_wait(&freeb[kp % kStages], (kp / kStages) & 1);
       }
       const uint32_t sa = smem_base + (uint32_t)s * stage_bytes;
+      // both 16-k quarters of this warp's k half: 16 adjacent TMEM columns of
+      // hi and of lo, one 16-column store each
+      uint32_t hi[16], lo[16];
 #pragma unroll
       for (int sub = 0; sub < 2; ++sub) {
         const int qtr = 2 * half + sub;     // k values 16 qtr .. + 15
@@ -242,17 +245,16 @@ __global__ void __launch_bounds__(kThreadsP, 1)
 #pragma unroll
           for (int k = 0; k < 16; ++k) v[k] = lds32(box + (16 * qtr + k) * 128);
         }
-        uint32_t hi[8], lo[8];
 #pragma unroll
         for (int i2 = 0; i2 < 8; ++i2) {
           const float x0 = v[2 * i2] * rscale, x1 = v[2 * i2 + 1] * rscale;
-          hi[i2] = pack_h2(x0, x1);
-          const float2 hf = unpack_h2(hi[i2]);
-          lo[i2] = pack_h2(x0 - hf.x, x1 - hf.y);
+          hi[8 * sub + i2] = pack_h2(x0, x1);
+          const float2 hf = unpack_h2(hi[8 * sub + i2]);
+          lo[8 * sub + i2] = pack_h2(x0 - hf.x, x1 - hf.y);
         }
-        tmem_st8(tmem + lane_base + kASlotP + slot * 64 + 8 * qtr, hi);
-        tmem_st8(tmem + lane_base + kASlotP + slot * 64 + 32 + 8 * qtr, lo);
       }
+      tmem_st16(tmem + lane_base + kASlotP + slot * 64 + 16 * half, hi);
+      tmem_st16(tmem + lane_base + kASlotP + slot * 64 + 32 + 16 * half, lo);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_before_sync();
       __syncwarp();
