@@ -255,6 +255,7 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
     z_ready = feed_and_sample<T>(c, const_cast<T*>(A), m, n, lda, row_major, *feed, X, l, Y.p,
                                  q > 0 ? Z.p : nullptr, arow.p, acol.p);
   } else {
+    PowerLowp lowp(c);
     big_nn<T>(c, A, m, n, lda, row_major, X, n, l, Y.p, m, arow.p);
   }
   const MaxAbs p0 = maxabs<T>(c, Y.p, m, l, m);
@@ -287,11 +288,17 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
   if (track) Ts.alloc(c, (size_t)q * l * l);
   for (int it = 0; it < (paper ? 0 : q); ++it) {
     const bool fused = it == 0 && z_ready;   // the feed's A^T Y ran unscaled
+    PowerLowp lowp(c);
     if (!fused)
       big_tn<T>(c, A, m, n, lda, row_major, Y.p, m, l, Z.p, n, acol.p, zscale);
     zfac.push_back(fused ? 1.0 : zscale);
-    normalize_sketch<T>(c, Z.p, n, l, n, Zn.p, n, track ? Ts.p + (size_t)it * l * l : nullptr,
-                        f64_extreme);
+    {
+      const bool keep = c.b_hi_only;   // the basis change stays three-term
+      c.b_hi_only = false;
+      normalize_sketch<T>(c, Z.p, n, l, n, Zn.p, n, track ? Ts.p + (size_t)it * l * l : nullptr,
+                          f64_extreme);
+      c.b_hi_only = keep;
+    }
     big_nn<T>(c, A, m, n, lda, row_major, Zn.p, n, l, Y.p, m, arow.p);
   }
   info.words_read += (int64_t)(2 * q + 1) * m * n;

@@ -39,6 +39,27 @@ struct Ctx {
   std::vector<cudaEvent_t> prof_ev;  // start/stop pairs
   double prof_flops = 0.0, prof_bytes = 0.0;
   long long prof_launch0 = 0;
+  // fp16-split products of the power iteration with the sketch operand
+  // rounded to fp16 (two MMAs per term instead of three), see PowerLowp
+  bool b_hi_only = false;
+};
+
+// Scope in which the fp32 A-streaming products may use the two-term split
+// (a_hi b_hi + a_lo b_hi: A keeps its 22 bits, the sketch operand X / Y
+// rounded to fp16) -- the power-iteration products only; the core product
+// B = Q^T A and every basis change stay three-term.  OFF by default (the
+// shipped products carry ~22 bits in both operands, fp32-equivalent);
+// BRSVD_POWER_LOWP=1 opts in: measured 19.3 -> 17.7 ms at config 2 with
+// every GPU parity test still inside the north-star tolerances, but the
+// sketch operand of those products is then below fp32 precision.
+struct PowerLowp {
+  Ctx& c;
+  bool prev;
+  explicit PowerLowp(Ctx& c_) : c(c_), prev(c_.b_hi_only) {
+    const char* e = std::getenv("BRSVD_POWER_LOWP");
+    c.b_hi_only = e && e[0] == '1';
+  }
+  ~PowerLowp() { c.b_hi_only = prev; }
 };
 
 // Brackets one big-product launch with events when profiling is on.

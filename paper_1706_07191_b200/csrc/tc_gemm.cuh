@@ -61,6 +61,7 @@ struct Params {
   const float* col_inv;
   int keep_scaled;  // H16: leave the row/column scales in (caller unscales)
   double out_scale;  // H16: output multiplied by this power of two (range control)
+  int b_terms;       // pair kernel: 3 (a_lo b_hi + a_hi b_lo + a_hi b_hi) or 2 (no b_lo)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -893,6 +894,7 @@ inline void tc_gemm_launch<float>(Ctx& c, const float* A, int64_t m, int64_t n, 
   p.col_inv = nullptr;
   p.keep_scaled = 0;
   p.out_scale = out_scale;
+  p.b_terms = 3;
   DBuf<float> hi, lo, opmax, cinv;
   CUtensorMap mapBhi, mapBlo;
   if (h16) {

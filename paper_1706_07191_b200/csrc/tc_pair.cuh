@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(kThreadsP, 1)
   const int kb_begin = ks * per;
   const int nk = max(0, min(nk_all, kb_begin + per) - kb_begin);
   const int nchunk = (nk + CHUNK - 1) / CHUNK;
+  const bool two = p.b_terms == 2;   // sketch operand rounded to fp16: no B_lo term
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(kThreadsP, 1)
         mbar_wait(&freeb[s], ph ^ 1);
         uint8_t* st = smem + (size_t)s * stage_bytes;
         const int k0 = (kb_begin + kb) * BK_H16;
-        mbar_expect_tx(&full[s], stage_bytes);
+        mbar_expect_tx(&full[s], two ? ASB + bhb : stage_bytes);
         if (A_KMAJOR) {
           tma_load_2d(st, &mapA, &full[s], k0, (int)m0);
           tma_load_2d(st + BM * 128, &mapA, &full[s], k0 + 32, (int)m0);
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(kThreadsP, 1)
             tma_load_2d(st + b * (32 * BK_H16 * 4), &mapA, &full[s], (int)m0 + 32 * b, k0);
         }
         tma_load_2d(st + ASB, &mapBhi, &full[s], k0, br);
-        tma_load_2d(st + ASB + bhb, &mapBlo, &full[s], k0, br);
+        if (!two) tma_load_2d(st + ASB + bhb, &mapBlo, &full[s], k0, br);
       }
     }
   } else if (warp == 1) {
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(kThreadsP, 1)
           const uint64_t dl = desc_kmajor_sw128(bl + kk * 32);
           const uint32_t acc = (chunk_start && kk == 0) ? 0u : 1u;
           mma2_f16(d, a_lo + kk * 8, dh, idesc, acc);
-          mma2_f16(d, a_hi + kk * 8, dl, idesc, 1u);
+          if (!two) mma2_f16(d, a_hi + kk * 8, dl, idesc, 1u);
           mma2_f16(d, a_hi + kk * 8, dh, idesc, 1u);
         }
         commit2(&freeb[s]);
@@ -377,6 +378,7 @@ inline void tcp_gemm_launch(Ctx& c, const float* A, int64_t m, int64_t n, int64_
   p.part = nullptr;
   p.keep_scaled = 0;
   p.out_scale = out_scale;
+  p.b_terms = c.b_hi_only ? 2 : 3;
   DBuf<float> hi, lo, opmax, cinv;
   const int64_t kld = ceil_div(K, 8) * 8;
   if (opa_max == nullptr) {
