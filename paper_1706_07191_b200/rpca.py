@@ -154,22 +154,55 @@ def _pinned_cm(m, n, dtype):
         return np.empty((m, n), dtype=dtype, order="F")
 
 
-def _ialm_stream(store, cfg, blocks, omega=None, nslots=2):
+def _host_room(nbytes):
+    """True when nbytes fit comfortably in the host's available memory."""
+    try:
+        import psutil
+        return nbytes <= 0.7 * psutil.virtual_memory().available
+    except ImportError:
+        return False
+
+
+def _ialm_stream(store, cfg, blocks, omega=None, nslots=2, pinned=None):
     """The reference's out-of-core branch (_ialm_rpca_ooc, rpca.py:216-304)
-    with M, S and Y host-resident and streamed block by block
-    (brsvd_ialm_stream); returns L and S as stores like the reference."""
+    with M, S and Y streamed block by block every pass (brsvd_ialm_stream);
+    returns L and S as stores like the reference.
+
+    pinned=None: when M, S, Y, L fit in host memory they live in page-locked
+    buffers (overlapped DMA); otherwise -- a store beyond host RAM, the case
+    the reference's branch exists for -- M is streamed straight from the
+    store's memory map and S, Y, L are file-backed maps in a temporary
+    directory, like the reference's temporary stores (rpca.py:240-243)."""
     from .rsvd import _store_payload
+    from .store import HEADER_SIZE
     m, n = store.m, store.n
     dt = store.dtype
     payload = _store_payload(store)          # read-only memory map, m x n, Fortran order
-    M = _pinned_cm(m, n, dt)
+    if pinned is None:
+        pinned = _host_room(4 * store.payload_bytes)
+    workdir = tempfile.mkdtemp(prefix="rpca_")
     w0, b0 = store.stats.words_read, store.stats.block_reads
-    for j0, j1 in blocks:                    # one read of the store into pinned memory
-        M[:, j0:j1] = payload[:, j0:j1]
+    if pinned:
+        M = _pinned_cm(m, n, dt)
+        for j0, j1 in blocks:                # one read of the store into pinned memory
+            M[:, j0:j1] = payload[:, j0:j1]
+        S, Y, L = (_pinned_cm(m, n, dt) for _ in range(3))
+        Ls = Ss = None
+    else:
+        M = payload
+        Ls = MatrixStore.create(os.path.join(workdir, "lowrank.oocm"), m, n, dt)
+        Ss = MatrixStore.create(os.path.join(workdir, "sparse.oocm"), m, n, dt)
+        Ls.close()
+        Ss.close()
+
+        maps = [np.memmap(os.path.join(workdir, "lowrank.oocm"), dtype=dt, mode="r+",
+                          offset=HEADER_SIZE, shape=(n, m)),
+                np.memmap(os.path.join(workdir, "sparse.oocm"), dtype=dt, mode="r+",
+                          offset=HEADER_SIZE, shape=(n, m)),
+                np.memmap(os.path.join(workdir, "dual.bin"), dtype=dt, mode="w+",
+                          shape=(n, m))]
+        L, S, Y = (mm.T for mm in maps)       # m x n, Fortran order
     store.stats.words_read, store.stats.block_reads = w0 + m * n, b0 + len(blocks)
-    S = _pinned_cm(m, n, dt)
-    Y = _pinned_cm(m, n, dt)
-    L = _pinned_cm(m, n, dt)
     maxit = int(cfg.max_iterations)
     res, mus, svd_s, it_s = (np.zeros(maxit) for _ in range(4))
     iters, conv = ctypes.c_int32(), ctypes.c_int32()
@@ -198,9 +231,16 @@ def _ialm_stream(store, cfg, blocks, omega=None, nslots=2):
     history = [{"i": i + 1, "mu": float(mus[i]), "residual": float(res[i]),
                 "svd_seconds": float(svd_s[i]), "iter_seconds": float(it_s[i])}
                for i in range(k)]
-    workdir = tempfile.mkdtemp(prefix="rpca_")
-    Ls = MatrixStore.from_array(os.path.join(workdir, "lowrank.oocm"), L)
-    Ss = MatrixStore.from_array(os.path.join(workdir, "sparse.oocm"), S)
+    if pinned:
+        Ls = MatrixStore.from_array(os.path.join(workdir, "lowrank.oocm"), L)
+        Ss = MatrixStore.from_array(os.path.join(workdir, "sparse.oocm"), S)
+    else:
+        for mm in maps:
+            mm.flush()
+        del L, S, Y, maps
+        os.remove(os.path.join(workdir, "dual.bin"))
+        Ls = MatrixStore(os.path.join(workdir, "lowrank.oocm"))
+        Ss = MatrixStore(os.path.join(workdir, "sparse.oocm"))
     return RpcaResult(L=Ls, S=Ss, iterations=k, residual_history=[float(r) for r in res[:k]],
                       converged=bool(conv.value), history=history)
 
@@ -211,7 +251,7 @@ def _device_room(payload_bytes):
     return _IALM_RESIDENT_COPIES * int(payload_bytes) <= free
 
 
-def ialm_rpca(m_input, cfg, omega=None, stream=None):
+def ialm_rpca(m_input, cfg, omega=None, stream=None, pinned=None):
     """Inexact-ALM robust PCA with a randomized inner SVD (rpca.py:153-213).
 
     Non-convergence at max_iterations returns ``converged=False``.  numpy (or
@@ -244,7 +284,7 @@ def ialm_rpca(m_input, cfg, omega=None, stream=None):
             if stream is None:
                 stream = not _device_room(m_input.payload_bytes)
             if stream:
-                return _ialm_stream(m_input, cfg, blocks, omega)
+                return _ialm_stream(m_input, cfg, blocks, omega, pinned=pinned)
         _require_device_room(m_input.payload_bytes)
         m_input = m_input.read_full()
     device = is_torch(m_input)

@@ -181,6 +181,21 @@ def test_out_of_core_branch_matches_reference(tmp_path, stream):
     assert rel <= 1e-6, rel
 
 
+def test_streamed_ooc_file_backed_matches_pinned(tmp_path):
+    """A store beyond host RAM streams M from its memory map and keeps S, Y,
+    L in file-backed maps (pinned=False); same iteration as the pinned path."""
+    from paper_1706_07191_b200 import MatrixStore, RpcaConfig, ialm_rpca
+    L0, S0, _ = planted(m=500, n=180, seed=14)
+    st = MatrixStore.from_array(tmp_path / "m.oocm", L0 + S0)
+    cfg = RpcaConfig(target_rank=8, tol=1e-7, memory_budget_bytes=(L0.nbytes // 3))
+    a = ialm_rpca(st, cfg, stream=True, pinned=True)
+    b = ialm_rpca(st, cfg, stream=True, pinned=False)
+    assert a.iterations == b.iterations and b.converged
+    np.testing.assert_allclose(b.residual_history, a.residual_history, rtol=1e-12)
+    np.testing.assert_array_equal(b.L.read_full(), a.L.read_full())
+    np.testing.assert_array_equal(b.S.read_full(), a.S.read_full())
+
+
 def test_streamed_ooc_matches_resident_blocked(tmp_path):
     """The host-streamed IALM and the HBM-resident blocked IALM run the same
     iteration (same plan, same inner SVD semantics): identical iteration
