@@ -339,8 +339,17 @@ def run_ours(args, world, rank, local):
     if sharded:
         # config 4: A row-sharded over the ranks (weak scaling: each rank keeps
         # its 32768-row panel), NCCL all-reduce of Z / Grams / B^T.
-        from paper_1706_07191_b200.distributed import GpuOps, TorchComm, rsvd_sharded
-        comm, ops = TorchComm(), GpuOps(local)
+        from paper_1706_07191_b200.distributed import (GpuOps, NcclComm, TorchComm,
+                                                        rsvd_sharded)
+        ops = GpuOps(local)
+        comm = TorchComm()
+        if comm.backend == "nccl" and os.environ.get("BRSVD_BENCH_COMM", "library") == "library":
+            # the library's own communicator: collectives on its stream
+            try:
+                comm = NcclComm(ops)
+            except RuntimeError as e:   # collectives are plumbing: keep torch's then
+                print(f"bench: library NCCL communicator unavailable ({e}); "
+                      "using torch.distributed", file=sys.stderr)
 
         def one_step(a):
             f, _ = rsvd_sharded(a, cfg, rank * M, world * M, comm=comm, ops=ops)
@@ -478,6 +487,7 @@ def run_ours(args, world, rank, local):
             "config": {"workload": "config2", "m": M, "n": N_COLS, "k": K, "p": P, "q": Q,
                        "rank": RANK, "noise": NOISE, "passes": PASSES,
                        "parallelism": f"rowshard{world}" if world > 1 else "single",
+                       "collectives": (type(comm).__name__ if sharded else None),
                        "l2": "A (4.3 GB) exceeds L2; no flush needed"},
             "roofline": roofline,
             "cpu_baseline": cpu,

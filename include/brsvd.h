@@ -100,6 +100,20 @@ BRSVD_API int brsvd_ctx_create(int device, void* stream, brsvd_ctx** out);
 BRSVD_API int brsvd_ctx_set_stream(brsvd_ctx* ctx, void* stream);
 BRSVD_API int brsvd_ctx_destroy(brsvd_ctx* ctx);
 
+/* NCCL communicator of a context, for the row-sharded decomposition
+ * (BASELINE config 4): rank 0 draws a unique id
+ * (brsvd_nccl_unique_id, 128 bytes), every rank attaches with it; the
+ * collectives below then run on the context's stream, in order with its
+ * kernels.  libnccl.so.2 is opened at run time (BRSVD_NCCL_LIB overrides);
+ * failures return BRSVD_ERR_NCCL.  dtype: 1 f64, 2 f32, 3 int64; op: 0 sum,
+ * 2 max.  Buffers are device memory. */
+BRSVD_API int brsvd_nccl_unique_id(char* unique_id_128);
+BRSVD_API int brsvd_ctx_attach_nccl(brsvd_ctx* ctx, const char* unique_id_128, int nranks,
+                                    int rank);
+BRSVD_API int brsvd_allreduce(brsvd_ctx* ctx, void* buf, int64_t count, int dtype, int op);
+BRSVD_API int brsvd_allgather(brsvd_ctx* ctx, const void* send, void* recv, int64_t count,
+                              int dtype);
+
 BRSVD_API int brsvd_profile_begin(brsvd_ctx* ctx);
 BRSVD_API int brsvd_profile_end(brsvd_ctx* ctx, brsvd_profile* out);
 

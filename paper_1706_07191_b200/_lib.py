@@ -30,6 +30,7 @@ EXPORTED = (
     "brsvd_rsvd_stream_blocked", "brsvd_ialm_blocked", "brsvd_sketch_product_scaled",
     "brsvd_absmax", "brsvd_range_finder", "brsvd_colmax_entries", "brsvd_stream_rows_pass",
     "brsvd_normalize_f64", "brsvd_ialm_stream", "brsvd_spectral_norm_start",
+    "brsvd_nccl_unique_id", "brsvd_ctx_attach_nccl", "brsvd_allreduce", "brsvd_allgather",
 )
 
 
@@ -101,6 +102,10 @@ def _declare(lib):
     lib.brsvd_spectral_norm_start.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, u64,
                                               vp, dbl, c_int, ctypes.POINTER(dbl),
                                               ctypes.POINTER(i32)]
+    lib.brsvd_nccl_unique_id.argtypes = [ctypes.c_char_p]
+    lib.brsvd_ctx_attach_nccl.argtypes = [vp, ctypes.c_char_p, c_int, c_int]
+    lib.brsvd_allreduce.argtypes = [vp, vp, i64, c_int, c_int]
+    lib.brsvd_allgather.argtypes = [vp, vp, vp, i64, c_int]
     lib.brsvd_ialm.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, c_int, c_int,
                                c_int, u64, vp, dbl, dbl, dbl, dbl, c_int, vp, vp, c_int,
                                ctypes.POINTER(i32), ctypes.POINTER(i32), vp, vp, vp, vp]
@@ -237,7 +242,9 @@ def check(rc):
             except ValueError:
                 need = None
         raise BudgetError(msg, need)
-    if rc in (ERR_CUDA, ERR_NCCL):
+    if rc == ERR_NCCL:
+        raise RuntimeError(f"NCCL error: {msg}")
+    if rc == ERR_CUDA:
         raise RuntimeError(f"CUDA error: {msg}")
     raise ValueError(msg)
 

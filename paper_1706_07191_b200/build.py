@@ -38,7 +38,7 @@ def up_to_date():
 def build(force=False, verbose=False):
     if not force and up_to_date():
         return OUT
-    cmd = [NVCC, *ARCH, *FLAGS, "-o", OUT + ".tmp", os.path.join(CSRC, "capi.cu")]
+    cmd = [NVCC, *ARCH, *FLAGS, "-o", OUT + ".tmp", os.path.join(CSRC, "capi.cu"), "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

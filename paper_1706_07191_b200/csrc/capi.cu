@@ -11,6 +11,7 @@
 #include "rpca_stream.cuh"
 #include "stream.cuh"
 #include "residual.cuh"
+#include "nccl_rt.cuh"
 
 using namespace brsvd;
 
@@ -20,6 +21,8 @@ thread_local long long g_brsvd_launches = 0;
 
 struct brsvd_ctx {
   Ctx c;
+  nccl::ncclComm_t comm = nullptr;   // brsvd_ctx_attach_nccl (sharded path)
+  int nranks = 1, rank = 0;
 };
 
 namespace {
@@ -179,9 +182,65 @@ int brsvd_ctx_destroy(brsvd_ctx* ctx) {
   return guarded([&] {
     if (!ctx) return (int)kOk;
     cudaStreamSynchronize(ctx->c.stream);
+    if (ctx->comm) nccl::api().CommDestroy(ctx->comm);
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
     if (ctx->c.h_pinned) cudaFreeHost(ctx->c.h_pinned);
     delete ctx;
+    return (int)kOk;
+  });
+}
+
+int brsvd_nccl_unique_id(char* out) {
+  return guarded([&] {
+    BRSVD_REQUIRE(out != nullptr, kErrArg, "out is NULL");
+    nccl::ncclUniqueId id;
+    nccl::check(nccl::api().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out, id.internal, nccl::kUniqueIdBytes);
+    return (int)kOk;
+  });
+}
+
+int brsvd_ctx_attach_nccl(brsvd_ctx* ctx, const char* unique_id, int nranks, int rank) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && unique_id != nullptr, kErrArg, "NULL argument");
+    BRSVD_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, kErrArg, "bad rank / nranks");
+    BRSVD_CUDA(cudaSetDevice(ctx->c.device));
+    if (ctx->comm) {
+      nccl::api().CommDestroy(ctx->comm);
+      ctx->comm = nullptr;
+    }
+    nccl::ncclUniqueId id;
+    std::memcpy(id.internal, unique_id, nccl::kUniqueIdBytes);
+    nccl::check(nccl::api().CommInitRank(&ctx->comm, nranks, id, rank), "ncclCommInitRank");
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    return (int)kOk;
+  });
+}
+
+int brsvd_allreduce(brsvd_ctx* ctx, void* buf, int64_t count, int dtype, int op) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && ctx->comm != nullptr, kErrNccl,
+                  "no NCCL communicator attached (brsvd_ctx_attach_nccl)");
+    BRSVD_REQUIRE(op == 0 || op == 2, kErrArg, "op must be 0 (sum) or 2 (max)");
+    BRSVD_CUDA(cudaSetDevice(ctx->c.device));
+    if (count > 0)
+      nccl::check(nccl::api().AllReduce(buf, buf, (size_t)count, nccl::dtype_of(dtype), op,
+                                        ctx->comm, ctx->c.stream),
+                  "ncclAllReduce");
+    return (int)kOk;
+  });
+}
+
+int brsvd_allgather(brsvd_ctx* ctx, const void* send, void* recv, int64_t count, int dtype) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && ctx->comm != nullptr, kErrNccl,
+                  "no NCCL communicator attached (brsvd_ctx_attach_nccl)");
+    BRSVD_CUDA(cudaSetDevice(ctx->c.device));
+    if (count > 0)
+      nccl::check(nccl::api().AllGather(send, recv, (size_t)count, nccl::dtype_of(dtype),
+                                        ctx->comm, ctx->c.stream),
+                  "ncclAllGather");
     return (int)kOk;
   });
 }

@@ -98,6 +98,70 @@ class TorchComm:
         return out
 
 
+class NcclComm:
+    """Collectives on the library's own NCCL communicator
+    (brsvd_ctx_attach_nccl): they run on the context's stream, in order with
+    the kernels that produce and consume them, and fail as BRSVD_ERR_NCCL.
+    The 128-byte unique id travels once through torch.distributed (any
+    backend, plumbing only); world size 1 needs no process group.  Same
+    interface as TorchComm for rsvd_sharded."""
+
+    def __init__(self, ops, group=None):
+        import torch
+        import torch.distributed as dist
+        self.ops = ops
+        self.torch = torch
+        active = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if active else 1
+        self.rank = dist.get_rank(group) if active else 0
+        lib = _lib.load_library()
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _lib.check(lib.brsvd_nccl_unique_id(uid))
+        if self.world > 1:
+            box = [bytes(uid.raw) if self.rank == 0 else None]
+            dist.broadcast_object_list(box, src=0, group=group)
+            uid = ctypes.create_string_buffer(box[0], 128)
+        _lib.check(lib.brsvd_ctx_attach_nccl(ops.ctx.handle, uid, self.world, self.rank))
+        self.lib = lib
+
+    def _dense(self, x):
+        """A contiguous CUDA tensor sharing x's storage (column-major views
+        are transposed: element-wise reductions do not care)."""
+        t = x if x.is_contiguous() else x.t()
+        if not t.is_contiguous():
+            raise ValueError("collective operand must be dense")
+        return t
+
+    def allreduce_sum(self, x):
+        t = self._dense(x)
+        self.ops._sync_stream()
+        code = 1 if t.dtype == self.torch.float64 else 2
+        _lib.check(self.lib.brsvd_allreduce(self.ops.ctx.handle, ctypes.c_void_p(t.data_ptr()),
+                                            t.numel(), code, 0))
+        return x
+
+    def allreduce_max(self, value):
+        t = self.torch.tensor([float(value)], dtype=self.torch.float64,
+                              device=self.ops.device)
+        self.ops._sync_stream()
+        _lib.check(self.lib.brsvd_allreduce(self.ops.ctx.handle, ctypes.c_void_p(t.data_ptr()),
+                                            1, 1, 2))
+        return float(t.item())
+
+    def allgather_array(self, arr):
+        a = np.ascontiguousarray(arr, dtype=np.float64)
+        send = self.torch.as_tensor(a, device=self.ops.device)
+        recv = self.torch.empty((self.world,) + a.shape, dtype=self.torch.float64,
+                                device=self.ops.device)
+        self.ops._sync_stream()
+        _lib.check(self.lib.brsvd_allgather(self.ops.ctx.handle,
+                                            ctypes.c_void_p(send.data_ptr()),
+                                            ctypes.c_void_p(recv.data_ptr()), send.numel(), 1))
+        out = recv.cpu().numpy()
+        return [out[r] for r in range(self.world)]
+
+
 # ---------------------------------------------------------------------------
 class HostShard:
     """This rank's row shard A[r0:r1, :] held in host memory (pinned for

@@ -80,3 +80,30 @@ def test_two_shards_match_single_gpu(dtype_name, streamed, tmp_path):
     np.testing.assert_allclose(U[:, :20], f.U[:, :20], atol=1e-8 if fp64 else 1e-3)
     np.testing.assert_allclose(parts[0]["Vt"][:20], f.Vt[:20], atol=1e-8 if fp64 else 1e-3)
     np.testing.assert_array_equal(parts[0]["sigma"], parts[1]["sigma"])
+
+
+def test_library_nccl_communicator_world1():
+    """The sharded driver over the library's own NCCL communicator
+    (brsvd_ctx_attach_nccl / brsvd_allreduce / brsvd_allgather), one rank,
+    against the single-GPU decomposition; a collective without a communicator
+    fails as BRSVD_ERR_NCCL."""
+    import ctypes
+    import torch
+    from oracle import ref_cpu
+    from paper_1706_07191_b200 import SketchConfig, _lib, rsvd_incore
+    from paper_1706_07191_b200.distributed import GpuOps, NcclComm, rsvd_sharded
+    A = ref_cpu.lowrank_plus_noise(2000, 600, 20, 1e-3, seed=19, dtype=np.float64)
+    omega = ref_cpu.normal_sketch(600, 30, 0, dtype=np.float64)
+    fresh = ctypes.c_void_p()
+    lib = _lib.load_library()
+    assert lib.brsvd_ctx_create(0, None, ctypes.byref(fresh)) == _lib.OK
+    buf = torch.zeros(4, dtype=torch.float64, device="cuda")
+    assert lib.brsvd_allreduce(fresh, ctypes.c_void_p(buf.data_ptr()), 4, 1, 0) == _lib.ERR_NCCL
+    lib.brsvd_ctx_destroy(fresh)
+    ops = GpuOps(0)
+    comm = NcclComm(ops)
+    f, _ = rsvd_sharded(torch.as_tensor(A, device="cuda"), SketchConfig(20, 10, 2), 0, 2000,
+                        comm=comm, ops=ops, omega=omega)
+    ref = rsvd_incore(A, SketchConfig(20, 10, 2), omega=omega)
+    np.testing.assert_allclose(f.sigma.cpu().numpy()[:20], ref.sigma[:20], rtol=1e-10)
+    np.testing.assert_allclose(f.U.cpu().numpy()[:, :20], ref.U[:, :20], atol=1e-8)
