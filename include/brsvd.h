@@ -362,7 +362,26 @@ BRSVD_API int brsvd_stream_rows_pass(brsvd_ctx* ctx, const void* A, int64_t m, i
 /* brsvd_normalize of an fp64 Z (the all-reduced sum of brsvd_stream_rows_pass)
  * into a basis in `dtype` (fp32: taken to unit order by a power of two first). */
 BRSVD_API int brsvd_normalize_f64(brsvd_ctx* ctx, const double* Z, int64_t n, int64_t l,
-                                  int64_t ldz, int dtype, void* Zout, int64_t ldo);
+                                  int64_t ldz, int dtype, void* Zout, int64_t ldo, double* T,
+                                  double* scale);
+
+/* brsvd_normalize returning the applied transform: Zout = Z T (T: device
+ * l x l fp64, upper triangular on the Cholesky route; for fp32 data its
+ * fp32-rounded entries); brsvd_normalize_f64's T / scale (optional) give
+ * Zout = (scale Z) T.  The sharded driver keeps them for its exact overflow
+ * guard. */
+BRSVD_API int brsvd_normalize_t(brsvd_ctx* ctx, const void* Z, int64_t n, int64_t l,
+                                int64_t ldz, int dtype, void* Zout, int64_t ldo, double* T);
+
+/* Exact overflow guard of the global power iteration (rsvd.py:84-91): the
+ * peak of the reference's unnormalised sample (A A^T)^q A Omega, formed in
+ * fp64 from this rank's rows Yq (m x l, column-major, ld m) of the
+ * normalised sample and the q applied transforms Ts (device, q x l x l,
+ * each upper triangular) with their scales zfac (host, q): max |Yq (prod
+ * zfac_i T_i)^-1|. */
+BRSVD_API int brsvd_unnormalised_peak(brsvd_ctx* ctx, const void* Yq, int64_t m, int64_t l,
+                                      int dtype, int q, const double* Ts, const double* zfac,
+                                      double* peak);
 
 /* X[:, j] *= scale[j] (scale: host array of l doubles). */
 BRSVD_API int brsvd_scale_cols(brsvd_ctx* ctx, void* X, int64_t r, int64_t l, int64_t ldx,

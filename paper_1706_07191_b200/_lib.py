@@ -31,6 +31,7 @@ EXPORTED = (
     "brsvd_absmax", "brsvd_range_finder", "brsvd_colmax_entries", "brsvd_stream_rows_pass",
     "brsvd_normalize_f64", "brsvd_ialm_stream", "brsvd_spectral_norm_start",
     "brsvd_nccl_unique_id", "brsvd_ctx_attach_nccl", "brsvd_allreduce", "brsvd_allgather",
+    "brsvd_normalize_t", "brsvd_unnormalised_peak",
 )
 
 
@@ -137,7 +138,10 @@ def _declare(lib):
     lib.brsvd_colmax_entries.argtypes = [vp, vp, i64, i64, i64, c_int, i64, vp]
     lib.brsvd_stream_rows_pass.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, vp, i64, i64,
                                            vp, i64, vp, i64, i64, c_int, ctypes.POINTER(dbl)]
-    lib.brsvd_normalize_f64.argtypes = [vp, vp, i64, i64, i64, c_int, vp, i64]
+    lib.brsvd_normalize_f64.argtypes = [vp, vp, i64, i64, i64, c_int, vp, i64, vp, vp]
+    lib.brsvd_normalize_t.argtypes = [vp, vp, i64, i64, i64, c_int, vp, i64, vp]
+    lib.brsvd_unnormalised_peak.argtypes = [vp, vp, i64, i64, c_int, c_int, vp, vp,
+                                            ctypes.POINTER(dbl)]
     lib.brsvd_ialm_stream.argtypes = [vp, vp, i64, i64, i64, c_int, c_int, c_int, c_int, u64,
                                       vp, dbl, dbl, dbl, dbl, c_int, vp, c_int, vp, vp, vp,
                                       c_int, ctypes.POINTER(i32), ctypes.POINTER(i32), vp, vp,

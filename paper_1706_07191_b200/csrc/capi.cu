@@ -841,7 +841,8 @@ int brsvd_normalize(brsvd_ctx* ctx, const void* Z, int64_t n, int64_t l, int64_t
     BRSVD_CUDA(cudaSetDevice(c.device));
     esize(dtype);
     if (dtype == BRSVD_F64)
-      normalize_sketch<double>(c, (const double*)Z, n, (int)l, ldz, (double*)Zout, ldo);
+      normalize_sketch<double>(c, (const double*)Z, n, (int)l, ldz, (double*)Zout, ldo,
+                               nullptr, /*scale_check=*/true);
     else
       normalize_sketch<float>(c, (const float*)Z, n, (int)l, ldz, (float*)Zout, ldo);
     return (int)kOk;
@@ -927,16 +928,52 @@ int brsvd_stream_rows_pass(brsvd_ctx* ctx, const void* A, int64_t m, int64_t n, 
 }
 
 int brsvd_normalize_f64(brsvd_ctx* ctx, const double* Z, int64_t n, int64_t l, int64_t ldz,
-                        int dtype, void* Zout, int64_t ldo) {
+                        int dtype, void* Zout, int64_t ldo, double* T, double* scale) {
   return guarded([&] {
     BRSVD_REQUIRE(ctx != nullptr && Z != nullptr && Zout != nullptr, kErrArg, "NULL argument");
     Ctx& c = ctx->c;
     BRSVD_CUDA(cudaSetDevice(c.device));
     esize(dtype);
     if (dtype == BRSVD_F64)
-      normalize_from_f64<double>(c, Z, n, (int)l, ldz, (double*)Zout, ldo);
+      normalize_from_f64<double>(c, Z, n, (int)l, ldz, (double*)Zout, ldo, T, scale);
     else
-      normalize_from_f64<float>(c, Z, n, (int)l, ldz, (float*)Zout, ldo);
+      normalize_from_f64<float>(c, Z, n, (int)l, ldz, (float*)Zout, ldo, T, scale);
+    return (int)kOk;
+  });
+}
+
+int brsvd_normalize_t(brsvd_ctx* ctx, const void* Z, int64_t n, int64_t l, int64_t ldz,
+                      int dtype, void* Zout, int64_t ldo, double* T) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && Z != nullptr && Zout != nullptr, kErrArg, "NULL argument");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    esize(dtype);
+    if (dtype == BRSVD_F64)   // fp64 near the exponent limits: Gram at unit scale
+      normalize_sketch<double>(c, (const double*)Z, n, (int)l, ldz, (double*)Zout, ldo, T,
+                               /*scale_check=*/true);
+    else
+      normalize_sketch<float>(c, (const float*)Z, n, (int)l, ldz, (float*)Zout, ldo, T);
+    return (int)kOk;
+  });
+}
+
+int brsvd_unnormalised_peak(brsvd_ctx* ctx, const void* Yq, int64_t m, int64_t l, int dtype,
+                            int q, const double* Ts, const double* zfac, double* peak) {
+  return guarded([&] {
+    BRSVD_REQUIRE(ctx != nullptr && Yq != nullptr && Ts != nullptr && zfac && peak, kErrArg,
+                  "NULL argument");
+    BRSVD_REQUIRE(q >= 1 && l >= 1 && m >= 0, kErrArg, "bad shape");
+    Ctx& c = ctx->c;
+    BRSVD_CUDA(cudaSetDevice(c.device));
+    esize(dtype);
+    if (m == 0) {
+      *peak = 0.0;
+      return (int)kOk;
+    }
+    *peak = dtype == BRSVD_F64
+                ? unnormalised_peak<double>(c, (const double*)Yq, m, (int)l, q, Ts, zfac)
+                : unnormalised_peak<float>(c, (const float*)Yq, m, (int)l, q, Ts, zfac);
     return (int)kOk;
   });
 }

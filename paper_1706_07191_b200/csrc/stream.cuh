@@ -149,9 +149,12 @@ void product_accum(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda, bool r
 // sum holds fits fp32; fp64 data is unit-scaled inside normalize_sketch.
 template <typename T>
 void normalize_from_f64(Ctx& c, const double* Z, int64_t n, int l, int64_t ldz, T* Zout,
-                        int64_t ldo) {
+                        int64_t ldo, double* Tout = nullptr, double* scale_out = nullptr) {
+  // Tout / scale_out (optional): Zout = (scale_out Z) Tout, the transform the
+  // exact overflow guard of the sharded driver inverts
+  if (scale_out) *scale_out = 1.0;
   if constexpr (sizeof(T) == 8) {
-    normalize_sketch<double>(c, Z, n, l, ldz, Zout, ldo, nullptr, /*scale_check=*/true);
+    normalize_sketch<double>(c, Z, n, l, ldz, Zout, ldo, Tout, /*scale_check=*/true);
   } else {
     const MaxAbs pk = maxabs<double>(c, Z, n, l, ldz);
     if (pk.nonfinite)
@@ -166,7 +169,8 @@ void normalize_from_f64(Ctx& c, const double* Z, int64_t n, int l, int64_t ldz, 
     scale_cast_kernel<double, float><<<grid_for(n * l), 256, 0, c.stream>>>(Z, n, l, ldz, Zs.p,
                                                                             n, s);
     BRSVD_CHECK_LAUNCH();
-    normalize_sketch<float>(c, Zs.p, n, l, n, reinterpret_cast<float*>(Zout), ldo);
+    normalize_sketch<float>(c, Zs.p, n, l, n, reinterpret_cast<float*>(Zout), ldo, Tout);
+    if (scale_out) *scale_out = s;
   }
 }
 

@@ -381,13 +381,41 @@ class GpuOps:
         shard.pass_ms.append(ms.value)
         return Y, Z
 
-    def normalize_f64(self, Z, dtype):
-        """Basis change of an fp64 Z (brsvd_normalize_f64) in the data's dtype."""
+    def normalize_f64(self, Z, dtype, T=None):
+        """Basis change of an fp64 Z (brsvd_normalize_f64) in the data's dtype;
+        with T (device l x l fp64 buffer) also returns the power-of-two scale s
+        of Zout = (s Z) T."""
         self._sync_stream()
         out = _cm_empty(Z.shape[0], Z.shape[1], dtype, self.device)
+        sc = ctypes.c_double(1.0)
         _lib.check(self.lib.brsvd_normalize_f64(self.ctx.handle, _vp(Z), Z.shape[0], Z.shape[1],
-                                                _ld(Z), _code(out), _vp(out), _ld(out)))
+                                                _ld(Z), _code(out), _vp(out), _ld(out),
+                                                None if T is None else _vp(T),
+                                                ctypes.byref(sc)))
+        return out if T is None else (out, sc.value)
+
+    def normalize_t(self, Z, T):
+        """brsvd_normalize writing the applied transform into T (device l x l
+        fp64): Zout = Z T."""
+        self._sync_stream()
+        out = _cm_empty(Z.shape[0], Z.shape[1], Z.dtype, self.device)
+        _lib.check(self.lib.brsvd_normalize_t(self.ctx.handle, _vp(Z), Z.shape[0], Z.shape[1],
+                                              _ld(Z), _code(Z), _vp(out), _ld(out), _vp(T)))
         return out
+
+    def transform_buffers(self, q, l):
+        return self.torch.empty((q, l, l), dtype=self.torch.float64, device=self.device)
+
+    def unnormalised_peak(self, Y, Ts, zfac):
+        """max |Y (prod zfac_i T_i)^-1| over this rank's rows (brsvd_unnormalised_peak)."""
+        self._sync_stream()
+        z = np.ascontiguousarray(zfac, dtype=np.float64)
+        out = ctypes.c_double()
+        Yc = Y if _ld(Y) == Y.shape[0] else Y.t().contiguous().t()
+        _lib.check(self.lib.brsvd_unnormalised_peak(
+            self.ctx.handle, _vp(Yc), Y.shape[0], Y.shape[1], _code(Y), len(z), _vp(Ts),
+            ctypes.c_void_p(z.ctypes.data), ctypes.byref(out)))
+        return out.value
 
     def scale_cols(self, X, scale):
         self._sync_stream()
@@ -498,12 +526,21 @@ def rsvd_sharded(A_local, cfg, row_offset, m_total, comm=None, ops=None, omega=N
     eps_data = _EPS[npdt]
     seed = int(cfg.master_seed)
     X = ops.asarray(omega, dtype) if omega is not None else ops.gaussian(n, l, seed, 0, 0, dtype)
+    # the applied basis changes, for the exact overflow guard (Cholesky route,
+    # l <= 320 as pipeline.cuh): Zn_i = (zfac_i Z_i) T_i
+    track = q > 0 and l <= 320 and hasattr(ops, "unnormalised_peak")
+    Ts = ops.transform_buffers(q, l) if track else None
+    zfac = []
     if streamed:
         def sample(Xs, want_z):
             return ops.stream_pass(A_local, Xs, None, want_z)
 
-        def basis(Z):
-            return ops.normalize_f64(Z, dtype)
+        def basis(Z, it):
+            if not track:
+                return ops.normalize_f64(Z, dtype)
+            Zn, sc = ops.normalize_f64(Z, dtype, Ts[it])
+            zfac.append(sc)
+            return Zn
     else:
         amax = ops.absmax(A_local) if hasattr(ops, "absmax") else None
 
@@ -511,7 +548,11 @@ def rsvd_sharded(A_local, cfg, row_offset, m_total, comm=None, ops=None, omega=N
             Ys = ops.product(A_local, Xs, False, amax)
             return Ys, (ops.product(A_local, Ys, True, amax) if want_z else None)
 
-        basis = ops.normalize
+        def basis(Z, it):
+            if not track:
+                return ops.normalize(Z)
+            zfac.append(1.0)
+            return ops.normalize_t(Z, Ts[it])
     Y, Zp = sample(X, q > 0)
     vals = ops.colmax_entries(Y, row_offset)[0]
     bad = not np.all(np.isfinite(vals)) or np.any(vals < 0)
@@ -521,7 +562,7 @@ def rsvd_sharded(A_local, cfg, row_offset, m_total, comm=None, ops=None, omega=N
         raise FloatingPointError("sample matrix is not finite; the overflow guard fires")
     for it in range(q):
         Z = comm.allreduce_sum(Zp)
-        Y, Zp = sample(basis(Z), it < q - 1)
+        Y, Zp = sample(basis(Z, it), it < q - 1)
     Q, rank_y = _orth_sharded(Y, ops, comm, eps_data, row_offset, m_total, seed ^ 0x7153)
     Qd = ops.cast(Q, dtype)
     if streamed:
@@ -539,8 +580,22 @@ def rsvd_sharded(A_local, cfg, row_offset, m_total, comm=None, ops=None, omega=N
     lim = math.log10(0.01 * np.finfo(npdt).max)
     if not math.isfinite(s0):   # as pipeline.cuh: a non-finite sigma_1 is an overflow
         raise FloatingPointError("sample matrix is not finite; the overflow guard fires")
+    # _check_overflow (rsvd.py:84-91) on the reference's unnormalised sample:
+    # far below the threshold the bound max|A Omega| sqrt(m) s_1^(2q) settles
+    # it; near or above it the peak is formed exactly from this rank's rows
+    # and the kept transforms (one all-reduce max), as pipeline.cuh does
     log_peak = (math.log10(peak0) + 2 * q * math.log10(s0)) if peak0 > 0 and s0 > 0 else -400.0
-    if log_peak > lim:
+    if q == 0:
+        over = log_peak > lim
+    elif log_peak + 0.5 * math.log10(m_total) + 0.05 <= lim:
+        over = False
+    elif track:
+        pk = comm.allreduce_max(ops.unnormalised_peak(Y, Ts, zfac))
+        log_peak = math.log10(pk) if pk > 0 else -400.0
+        over = not (pk <= 0.01 * float(np.finfo(npdt).max))
+    else:
+        over = log_peak > lim
+    if over:
         raise FloatingPointError("sample matrix magnitude exceeds the overflow guard")
     info = {"rank_y": rank_y, "rank_b": rank_b, "max_abs_y0": peak0, "log10_peak": log_peak}
     if streamed:

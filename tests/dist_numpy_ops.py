@@ -68,9 +68,35 @@ class NumpyOps:
         return np.asfortranarray(r.astype(out_dtype))
 
     def normalize(self, Z):
+        return self.normalize_t(Z, None)
+
+    def normalize_t(self, Z, T_out):
+        """brsvd_normalize_t: Zout = Z T, T kept (fp32 data: T rounded to fp32
+        as the tensor-core basis change applies it)."""
         l = Z.shape[1]
-        T, _, _ = self.chol_basis(self.gram(Z), shift=16.0 * l * 2.220446049250313e-16)
+        # unit scale first (exact power of two, folded into T), as
+        # normalize_sketch does for fp64 operands near the exponent limits
+        peak = float(np.max(np.abs(Z))) if Z.size else 0.0
+        u = 2.0 ** -int(np.frexp(peak)[1]) if peak > 0 and np.isfinite(peak) else 1.0
+        T, _, _ = self.chol_basis(self.gram(Z * u), shift=16.0 * l * 2.220446049250313e-16)
+        T = T * u
+        if Z.dtype == np.float32:
+            T = T.astype(np.float32).astype(F64)
+        if T_out is not None:
+            T_out[...] = T
         return self.apply(Z, T, Z.dtype)
+
+    def transform_buffers(self, q, l):
+        return np.zeros((q, l, l))
+
+    def unnormalised_peak(self, Y, Ts, zfac):
+        """brsvd_unnormalised_peak: max |Y (prod zfac_i T_i)^-1| in fp64."""
+        P = np.eye(Y.shape[1])
+        scale = 1.0
+        for T, z in zip(Ts, zfac):
+            P = np.linalg.solve(np.asarray(T), P)
+            scale *= z
+        return float(np.max(np.abs(Y.astype(F64) @ P))) / scale if Y.size else 0.0
 
     def gaussian(self, rows, cols, seed, stream, row_offset, dtype):
         return ref_cpu.normal_sketch(int(rows), int(cols), seed % (2 ** 63), stream % (2 ** 63),
@@ -116,13 +142,17 @@ class NumpyOps:
         shard.pass_ms.append(0.0)
         return Y, Z
 
-    def normalize_f64(self, Z, dtype):
-        """brsvd_normalize_f64: fp32 data first at a power-of-two unit scale."""
+    def normalize_f64(self, Z, dtype, T=None):
+        """brsvd_normalize_f64: fp32 data first at a power-of-two unit scale;
+        with T also returns that scale (Zout = (s Z) T)."""
+        s = 1.0
         if np.dtype(dtype) == np.float32:
             peak = float(np.max(np.abs(Z))) if Z.size else 0.0
             e = np.frexp(peak)[1] if peak > 0 else 0
-            Z = np.asfortranarray((Z * 2.0 ** -int(e)).astype(np.float32))
-        return self.normalize(np.asfortranarray(Z, dtype=dtype))
+            s = 2.0 ** -int(e)
+            Z = np.asfortranarray((Z * s).astype(np.float32))
+        out = self.normalize_t(np.asfortranarray(Z, dtype=dtype), T)
+        return out if T is None else (out, s)
 
     def scale_cols(self, X, scale):
         X *= np.asarray(scale, dtype=X.dtype)[None, :]

@@ -101,3 +101,45 @@ def test_sharded_rank_deficient_completion(tmp_path):
     assert np.linalg.norm(Vt @ Vt.T - np.eye(l)) <= 100 * l * np.finfo(np.float64).eps
     s = parts[0]["sigma"]
     assert s[5] <= 1e-10 * s[0]
+
+
+def _guard_worker(rank, world, port, frac, q, out_dir):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+    from oracle import ref_cpu
+    from paper_1706_07191_b200 import SketchConfig
+    from paper_1706_07191_b200.distributed import TorchComm, rsvd_sharded
+    from tests.dist_numpy_ops import NumpyOps
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    a = ref_cpu.lowrank_plus_noise(300, 200, 5, 1e-2, seed=8)
+    omega = ref_cpu.normal_sketch(200, 10, 0, dtype=np.float64)
+    peak1 = float(np.max(np.abs(ref_cpu.power_sample(a, omega, q))))
+    c = (frac * 0.01 * float(np.finfo(np.float64).max) / peak1) ** (1.0 / (2 * q + 1))
+    ac = a * c
+    r0, r1 = (0, 140) if rank == 0 else (140, 300)
+    fired = False
+    try:
+        rsvd_sharded(ac[r0:r1].copy(), SketchConfig(5, 5, q), r0, 300, comm=TorchComm(),
+                     ops=NumpyOps(), omega=omega)
+    except FloatingPointError:
+        fired = True
+    np.save(os.path.join(out_dir, f"g{rank}.npy"), np.array([fired]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("q", [1, 2])
+@pytest.mark.parametrize("frac", [0.99, 1.01])
+def test_sharded_overflow_guard_is_exact(frac, q, tmp_path):
+    """_check_overflow (rsvd.py:84-91) in the row-sharded driver: inputs that
+    put the reference's unnormalised sample at 0.99x / 1.01x of 0.01 *
+    finfo.max fire exactly when the reference does, on every rank (the peak
+    is formed from each rank's rows and the kept basis changes, then
+    all-reduced)."""
+    import torch.multiprocessing as mp
+    mp.start_processes(_guard_worker, args=(2, _free_port(), frac, q, str(tmp_path)),
+                       nprocs=2, join=True, start_method="spawn")
+    fired = [bool(np.load(tmp_path / f"g{r}.npy")[0]) for r in range(2)]
+    assert fired == [frac > 1.0] * 2

@@ -107,3 +107,35 @@ def test_library_nccl_communicator_world1():
     ref = rsvd_incore(A, SketchConfig(20, 10, 2), omega=omega)
     np.testing.assert_allclose(f.sigma.cpu().numpy()[:20], ref.sigma[:20], rtol=1e-10)
     np.testing.assert_allclose(f.U.cpu().numpy()[:, :20], ref.U[:, :20], atol=1e-8)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("q", [1, 2])
+@pytest.mark.parametrize("frac", [0.99, 1.01])
+def test_sharded_overflow_guard_exact_on_gpu(dtype, q, frac):
+    """The sharded driver's exact _check_overflow (rsvd.py:84-91) through the
+    C ABI (brsvd_normalize_t / brsvd_unnormalised_peak): fires iff the
+    reference's unnormalised sample peaks above 0.01 * finfo.max."""
+    import torch
+    from oracle import ref_cpu
+    from paper_1706_07191_b200 import SketchConfig
+    from paper_1706_07191_b200.distributed import GpuOps, TorchComm, rsvd_sharded
+    a = ref_cpu.lowrank_plus_noise(300, 200, 5, 1e-2, seed=8)
+    omega = ref_cpu.normal_sketch(200, 10, 0, dtype=np.float64)
+    peak1 = float(np.max(np.abs(ref_cpu.power_sample(a, omega, q))))
+    lim = 0.01 * float(np.finfo(dtype).max)
+    c = (frac * lim / peak1) ** (1.0 / (2 * q + 1))
+    ac = (a * c).astype(dtype)
+    om = omega.astype(dtype)
+    with np.errstate(over="ignore", invalid="ignore"):
+        _, ref_fires = ref_cpu.overflow_peak(ref_cpu.power_sample(ac, om, q))
+    assert ref_fires == (frac > 1.0)
+    A = torch.as_tensor(ac, device="cuda")
+    if ref_fires:
+        with pytest.raises(FloatingPointError):
+            rsvd_sharded(A, SketchConfig(5, 5, q), 0, 300, comm=TorchComm(), ops=GpuOps(0),
+                         omega=om)
+    else:
+        f, _ = rsvd_sharded(A, SketchConfig(5, 5, q), 0, 300, comm=TorchComm(), ops=GpuOps(0),
+                            omega=om)
+        assert np.isfinite(f.sigma.cpu().numpy()).all()
