@@ -545,6 +545,36 @@ int brsvd_tsqr(brsvd_ctx* ctx, const void* Y, int64_t m, int64_t l, int64_t ldy,
         gemm_tn_cm<float, float, float>(c, l, l, m, Qw.p, m, (const float*)yv.dptr,
                                         yv.ld, (float*)ro.dptr, l);
     }
+    if (ro.dptr) {
+      // full-rank inputs: Q = Y T with T upper triangular (Cholesky QR in
+      // column order), so R = Q^T Y is upper triangular up to rounding --
+      // make it exactly so, as Householder QR returns it (kernels.py:139-164).
+      // Rank-deficient inputs (completed columns) keep the full Q^T Y.
+      DBuf<unsigned long long> tc(c, 2);
+      BRSVD_CUDA(cudaMemsetAsync(tc.p, 0, 2 * sizeof(unsigned long long), c.stream));
+      if (dtype == BRSVD_F64)
+        tri_check_kernel<double><<<grid_for(l * l), 256, 0, c.stream>>>((double*)ro.dptr,
+                                                                         (int)l, tc.p);
+      else
+        tri_check_kernel<float><<<grid_for(l * l), 256, 0, c.stream>>>((float*)ro.dptr,
+                                                                        (int)l, tc.p);
+      BRSVD_CHECK_LAUNCH();
+      unsigned long long hb[2];
+      readback(c, tc.p, hb, sizeof(hb));
+      double mx, low;
+      std::memcpy(&mx, &hb[0], 8);
+      std::memcpy(&low, &hb[1], 8);
+      const double eps = dtype == BRSVD_F64 ? 2.220446049250313e-16 : 1.1920928955078125e-07;
+      if (low <= 64.0 * l * eps * mx) {
+        if (dtype == BRSVD_F64)
+          zero_strict_lower_kernel<double><<<grid_for(l * l), 256, 0, c.stream>>>(
+              (double*)ro.dptr, (int)l);
+        else
+          zero_strict_lower_kernel<float><<<grid_for(l * l), 256, 0, c.stream>>>(
+              (float*)ro.dptr, (int)l);
+        BRSVD_CHECK_LAUNCH();
+      }
+    }
     qo.flush();
     ro.flush();
     BRSVD_CUDA(cudaStreamSynchronize(c.stream));

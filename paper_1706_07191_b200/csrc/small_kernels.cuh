@@ -227,6 +227,27 @@ __global__ void colmax_kernel(const T* __restrict__ U, int64_t rows, int64_t ldu
   }
 }
 
+// max |R| and max |strictly-lower R| of an l x l column-major matrix, as the
+// bit patterns of non-negative doubles (atomicMax on the unsigned image).
+template <typename T>
+__global__ void tri_check_kernel(const T* __restrict__ R, int l,
+                                 unsigned long long* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)l * l;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e % l), j = (int)(e / l);
+    const double v = fabs((double)R[e]);
+    const unsigned long long b = __double_as_longlong(v);
+    atomicMax(out, b);
+    if (i > j) atomicMax(out + 1, b);
+  }
+}
+template <typename T>
+__global__ void zero_strict_lower_kernel(T* __restrict__ R, int l) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)l * l;
+       e += (int64_t)gridDim.x * blockDim.x)
+    if ((int)(e % l) > (int)(e / l)) R[e] = T(0);
+}
+
 // In-place int64 -> double of a small index vector (exact below 2^53).
 __global__ void idx_to_double_kernel(int64_t* idx, int64_t l) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l;

@@ -188,6 +188,8 @@ def test_tsqr_against_golden():
     np.testing.assert_allclose(q @ r, y, atol=1e-12 * np.abs(y).max())
     proj = q @ q.T - g["q"] @ g["q"].T
     assert np.linalg.norm(proj) <= 1e-12
+    # full rank: R upper triangular, as the reference's Householder R
+    assert np.all(np.tril(r, -1) == 0.0)
     with pytest.warns(RankDeficiencyWarning) as rec:
         qd, _ = tsqr_factor(g["y_def"])
     assert rec[0].message.detected_rank == int(g["rank_def"])
