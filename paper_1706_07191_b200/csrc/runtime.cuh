@@ -170,7 +170,9 @@ void gram_fp64_bt(Ctx& c, int64_t a, int64_t b, int64_t r, const TX* X, int64_t 
   const int nti = (int)ceil_div(a, BT), ntj = (int)ceil_div(b, BT);
   const int tiles = sym ? nti * (nti + 1) / 2 : nti * ntj;
   const int per_sm = (Cfg<BT, NCG>::NT <= 288 && sizeof(TX) == 4) ? 2 : 1;
-  int64_t splits = std::max<int64_t>(1, ceil_div((int64_t)per_sm * c.num_sms, tiles));
+  // one full wave: tiles * splits <= resident CTAs (a ceil here left a
+  // second wave of a few CTAs that doubled the kernel time)
+  int64_t splits = std::max<int64_t>(1, ((int64_t)per_sm * c.num_sms) / tiles);
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, r / (4 * BK)));
   int64_t kchunk = ceil_div(ceil_div(r, splits), BK) * BK;
   splits = ceil_div(r, kchunk);
@@ -199,7 +201,9 @@ void gram_dmma_bt(Ctx& c, int64_t a, int64_t b, int64_t r, const TX* X, int64_t 
   const int nti = (int)ceil_div(a, BT), ntj = (int)ceil_div(b, BT);
   const int tiles = sym ? nti * (nti + 1) / 2 : nti * ntj;
   const int per_sm = (Cf::NT <= 288 && sizeof(TX) == 4) ? 2 : 1;
-  int64_t splits = std::max<int64_t>(1, ceil_div((int64_t)per_sm * c.num_sms, tiles));
+  // one full wave: tiles * splits <= resident CTAs (a ceil here left a
+  // second wave of a few CTAs that doubled the kernel time)
+  int64_t splits = std::max<int64_t>(1, ((int64_t)per_sm * c.num_sms) / tiles);
   splits = std::min<int64_t>(splits, std::max<int64_t>(1, r / (8 * DBK)));
   int64_t kchunk = ceil_div(ceil_div(r, splits), DBK) * DBK;
   splits = ceil_div(r, kchunk);
