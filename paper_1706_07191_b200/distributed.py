@@ -224,7 +224,6 @@ class GpuOps:
 
     def __init__(self, device=None):
         import torch
-        from ._arrays import torch_stream_ptr  # noqa: F401
         self.torch = torch
         self.device = torch.device("cuda", torch.cuda.current_device()
                                    if device is None else device)

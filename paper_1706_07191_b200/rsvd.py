@@ -25,7 +25,7 @@ import numpy as np
 from . import _lib
 from ._arrays import DeviceMatrix, HostMatrix, is_torch, torch_stream_ptr
 from .kernels import SvdFactors, warn_rank
-from .store import MatrixStore, PassStats, plan_blocks
+from .store import MatrixStore, plan_blocks
 
 __all__ = [
     "SketchConfig",

@@ -2,7 +2,6 @@
 test properties (tests/test_rpca.py of the reference)."""
 
 import os
-import warnings
 
 import numpy as np
 import pytest
