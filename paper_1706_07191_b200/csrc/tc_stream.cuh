@@ -44,6 +44,7 @@
 
 #include "tc_gemm.cuh"
 #include "tc_pair.cuh"
+#include "tc_pair_wide.cuh"
 
 namespace brsvd {
 namespace tcs {
@@ -829,6 +830,11 @@ inline void tc_product(Ctx& c, const float* A, int64_t m, int64_t n, int64_t lda
   if (tcs_gemm_launch(c, A, m, n, lda, row_major, trans, X, ldx, l, C, ldc, opa_max,
                       out_scale))
     return;
+  if (tcw::enabled() && tcp::enabled() && tc::h16_enabled() && tcw::fits(l) &&
+      !c.b_hi_only) {
+    tcw_gemm_launch(c, A, m, n, lda, row_major, trans, X, ldx, l, C, ldc, opa_max, out_scale);
+    return;
+  }
   if (tcp::enabled() && tc::h16_enabled() && tcp::tcp_fits(l)) {
     tcp_gemm_launch(c, A, m, n, lda, row_major, trans, X, ldx, l, C, ldc, opa_max, out_scale);
     return;
