@@ -273,9 +273,13 @@ __global__ void __launch_bounds__(kThreadsW, 1)
         if (col < p.n_out) {
           const float v = (float)((double)run[j] *
                                   ((double)rinv * (double)p.col_inv[col] * p.out_scale));
-          float* dst = p.C + row + (int64_t)col * p.ldc;
-          if (p.ksplit > 1) atomicAdd(dst, v);   // two partial sums: order-free
-          else *dst = v;
+          if (p.part != nullptr) {   // > 2 K-splits: partials, summed in a fixed order
+            p.part[(int64_t)ks * p.M * p.n_out + row + (int64_t)col * p.M] = v;
+          } else {
+            float* dst = p.C + row + (int64_t)col * p.ldc;
+            if (p.ksplit > 1) atomicAdd(dst, v);   // two partial sums: order-free
+            else *dst = v;
+          }
         }
       }
     }
@@ -288,6 +292,18 @@ __global__ void __launch_bounds__(kThreadsW, 1)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(kTmemCols)
                  : "memory");
+  }
+}
+
+// C = sum of the K-split partials in split order (deterministic), fp32
+__global__ void splitk_sum_f32_kernel(const float* __restrict__ part, int64_t M, int n,
+                                      int splits, float* __restrict__ C, int64_t ldc) {
+  const int64_t total = M * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    float v = 0.f;
+    for (int z = 0; z < splits; ++z) v += part[(int64_t)z * total + e];
+    C[(e % M) + (e / M) * ldc] = v;
   }
 }
 
@@ -351,15 +367,32 @@ inline void tcw_gemm_launch(Ctx& c, const float* A, int64_t m, int64_t n, int64_
                (uint32_t)(nc / 2), CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
   p.row_max = opa_max;
   p.col_inv = cinv.p;
+  // K splits so that the (tile x split) units fill their last wave of pairs
+  // well: the fraction of busy pair-slots over the waves, best of 1..4 splits
+  // (each split >= 4096 k).  Two partials combine by atomicAdd into a zeroed
+  // C (order-free); more go through a workspace summed in a fixed order.
   const int64_t tiles = ceil_div(M, 2 * BM);
-  const double waves = (double)tiles / (c.num_sms / 2);
-  p.ksplit = (K >= 8192 && waves > 1.0 && waves < 8.0 && waves - std::floor(waves) > 0.0 &&
-              waves - std::floor(waves) < 0.75)
-                 ? 2
-                 : 1;
-  if (p.ksplit > 1)
+  const int slots = std::max(1, c.num_sms / 2);
+  int best = 1;
+  double best_eff = 0.0;
+  for (int ks = 1; ks <= 4; ++ks) {
+    if (ks > 1 && K / ks < 4096) break;
+    const int64_t units = tiles * ks;
+    const double eff = (double)units / (double)(ceil_div(units, (int64_t)slots) * slots);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = ks;
+    }
+  }
+  p.ksplit = best;
+  DBuf<float> part;
+  if (p.ksplit > 2) {
+    part.alloc(c, (size_t)p.ksplit * M * l);
+    p.part = part.p;
+  } else if (p.ksplit == 2) {
     BRSVD_CUDA(cudaMemset2DAsync(C, (size_t)ldc * sizeof(float), 0, (size_t)M * sizeof(float),
                                  (size_t)l, c.stream));
+  }
   const size_t smem = tcw::smem_bytes(nc);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(2 * tiles * p.ksplit));
@@ -389,6 +422,11 @@ inline void tcw_gemm_launch(Ctx& c, const float* A, int64_t m, int64_t n, int64_
   }
 #undef BRSVD_TCW_LAUNCH
   ++g_brsvd_launches;
+  if (p.part != nullptr) {
+    tcw::splitk_sum_f32_kernel<<<grid_for(M * l), 256, 0, c.stream>>>(part.p, M, l, p.ksplit, C,
+                                                                  ldc);
+    BRSVD_CHECK_LAUNCH();
+  }
 }
 
 }  // namespace brsvd
