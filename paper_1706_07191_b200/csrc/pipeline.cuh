@@ -204,6 +204,72 @@ double unnormalised_peak(Ctx& c, const T* Yq, int64_t m, int l, int q, const dou
   return pk.nonfinite ? INFINITY : pk.peak / scale;
 }
 
+// fp16-split scales without an up-front pass over A.  The products need
+// per-line power-of-two scales of A (rows for Y = A X, columns for A^T Y); a
+// full absmax pass costs as much HBM traffic as a sixth of a product.  The
+// first product of each orientation instead runs on SAMPLED maxima
+// (amax_sampled: 1/16 of A) and, as its converters see every entry, writes
+// the exact maxima; a check kernel flags any line whose exact maximum the
+// sampled scale does not serve at full precision, and the same product is
+// launched again on the exact scales -- a launch that returns at once unless
+// flagged.  Later products use the exact maxima.  Only the single-chunk pair
+// kernel produces maxima (tcw_selected); otherwise the pass runs as before.
+struct LazyScales {
+  bool pend_r = false, pend_c = false;
+  DBuf<float> gr, gc;   // sampled maxima x 2^7
+  DBuf<int> flag;       // [2]: rows, columns
+};
+
+template <typename T>
+bool lazy_scales_ok(Ctx& c, int l) {
+  if (sizeof(T) != 4 || !tcw_selected(c, l)) return false;
+  const char* e = std::getenv("BRSVD_LAZY_SCALES");
+  return !(e && e[0] == '0');
+}
+
+template <typename T>
+void nn_product(Ctx& c, LazyScales& lz, const T* A, int64_t m, int64_t n, int64_t lda,
+                bool row_major, const T* X, int64_t ldx, int l, T* Y, int64_t ldy,
+                float* arow) {
+  if (lz.pend_r) {
+    lz.pend_r = false;
+    if (tcw_selected(c, l)) {
+      big_nn<T>(c, A, m, n, lda, row_major, X, ldx, l, Y, ldy, lz.gr.p,
+                reinterpret_cast<unsigned*>(arow));
+      tc::lazy_scale_check_kernel<<<grid_for(m), 256, 0, c.stream>>>(lz.gr.p, arow, m,
+                                                                      lz.flag.p);
+      BRSVD_CHECK_LAUNCH();
+      big_nn<T>(c, A, m, n, lda, row_major, X, ldx, l, Y, ldy, arow, nullptr, lz.flag.p);
+      return;
+    }
+    absmax_rows_cols(c, reinterpret_cast<const float*>(A), m, n, lda, row_major, arow,
+                     nullptr);
+  }
+  big_nn<T>(c, A, m, n, lda, row_major, X, ldx, l, Y, ldy, arow);
+}
+
+template <typename T>
+void tn_product(Ctx& c, LazyScales& lz, const T* A, int64_t m, int64_t n, int64_t lda,
+                bool row_major, const T* Yin, int64_t ldy, int l, T* Z, int64_t ldz,
+                float* acol, double out_scale = 1.0) {
+  if (lz.pend_c) {
+    lz.pend_c = false;
+    if (tcw_selected(c, l)) {
+      big_tn<T>(c, A, m, n, lda, row_major, Yin, ldy, l, Z, ldz, lz.gc.p, out_scale,
+                reinterpret_cast<unsigned*>(acol));
+      tc::lazy_scale_check_kernel<<<grid_for(n), 256, 0, c.stream>>>(lz.gc.p, acol, n,
+                                                                      lz.flag.p + 1);
+      BRSVD_CHECK_LAUNCH();
+      big_tn<T>(c, A, m, n, lda, row_major, Yin, ldy, l, Z, ldz, acol, out_scale, nullptr,
+                lz.flag.p + 1);
+      return;
+    }
+    absmax_rows_cols(c, reinterpret_cast<const float*>(A), m, n, lda, row_major, nullptr,
+                     acol);
+  }
+  big_tn<T>(c, A, m, n, lda, row_major, Yin, ldy, l, Z, ldz, acol, out_scale);
+}
+
 // range_only: stop after the orthonormal basis of the sample (block_range_finder,
 // rsvd.py:150-185); Q (m x l) is written to U.
 template <typename T>
@@ -228,10 +294,21 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
   DBuf<T> Y(c, (size_t)m * l), Z(c, (size_t)n * l), Zn(c, (size_t)n * l);
   // per-row / per-column maxima of |A| (one pass, reused by every product)
   DBuf<float> arow, acol;
+  LazyScales lz;
   if (want_amax<T>(c, A, lda, m, n, l)) {
     arow.alloc(c, (size_t)m);
     acol.alloc(c, (size_t)n);
-    if (feed == nullptr) {
+    if (feed == nullptr && !paper && lazy_scales_ok<T>(c, l)) {
+      lz.gr.alloc(c, (size_t)m);
+      lz.gc.alloc(c, (size_t)n);
+      lz.flag.alloc(c, 2);
+      BRSVD_CUDA(cudaMemsetAsync(lz.flag.p, 0, 2 * sizeof(int), c.stream));
+      BRSVD_CUDA(cudaMemsetAsync(arow.p, 0, sizeof(float) * m, c.stream));
+      BRSVD_CUDA(cudaMemsetAsync(acol.p, 0, sizeof(float) * n, c.stream));
+      amax_sampled(c, reinterpret_cast<const float*>(A), m, n, lda, row_major, lz.gr.p,
+                   lz.gc.p);
+      lz.pend_r = lz.pend_c = true;
+    } else if (feed == nullptr) {
       absmax_rows_cols(c, reinterpret_cast<const float*>(A), m, n, lda, row_major, arow.p,
                        acol.p);
     } else {  // the feed accumulates panel by panel
@@ -256,7 +333,7 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
                                  q > 0 ? Z.p : nullptr, arow.p, acol.p);
   } else {
     PowerLowp lowp(c);
-    big_nn<T>(c, A, m, n, lda, row_major, X, n, l, Y.p, m, arow.p);
+    nn_product<T>(c, lz, A, m, n, lda, row_major, X, n, l, Y.p, m, arow.p);
   }
   const MaxAbs p0 = maxabs<T>(c, Y.p, m, l, m);
   info.max_abs_y0 = p0.peak;
@@ -290,7 +367,7 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
     const bool fused = it == 0 && z_ready;   // the feed's A^T Y ran unscaled
     PowerLowp lowp(c);
     if (!fused)
-      big_tn<T>(c, A, m, n, lda, row_major, Y.p, m, l, Z.p, n, acol.p, zscale);
+      tn_product<T>(c, lz, A, m, n, lda, row_major, Y.p, m, l, Z.p, n, acol.p, zscale);
     zfac.push_back(fused ? 1.0 : zscale);
     {
       const bool keep = c.b_hi_only;   // the basis change stays three-term
@@ -299,7 +376,7 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
                           f64_extreme);
       c.b_hi_only = keep;
     }
-    big_nn<T>(c, A, m, n, lda, row_major, Zn.p, n, l, Y.p, m, arow.p);
+    nn_product<T>(c, lz, A, m, n, lda, row_major, Zn.p, n, l, Y.p, m, arow.p);
   }
   info.words_read += (int64_t)(2 * q + 1) * m * n;
   info.block_reads += 2 * q + 1;
@@ -339,7 +416,7 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
   const T* Qop = Qw.p;
   ev.rec(2, c.stream);
   DBuf<T> Bt(c, (size_t)n * l);
-  big_tn<T>(c, A, m, n, lda, row_major, Qop, m, l, Bt.p, n, acol.p);
+  tn_product<T>(c, lz, A, m, n, lda, row_major, Qop, m, l, Bt.p, n, acol.p);
   info.words_read += m * n;
   info.block_reads += 1;
   ev.rec(3, c.stream);

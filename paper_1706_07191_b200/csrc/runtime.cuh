@@ -66,7 +66,8 @@ struct PowerLowp {
 struct ProfScope {
   Ctx& c;
   bool on;
-  ProfScope(Ctx& c_, double flops, double bytes) : c(c_), on(c_.prof) {
+  ProfScope(Ctx& c_, double flops, double bytes, bool counted = true)
+      : c(c_), on(c_.prof && counted) {
     if (!on) return;
     cudaEvent_t e;
     BRSVD_CUDA(cudaEventCreate(&e));

@@ -62,6 +62,11 @@ struct Params {
   int keep_scaled;  // H16: leave the row/column scales in (caller unscales)
   double out_scale;  // H16: output multiplied by this power of two (range control)
   int b_terms;       // pair kernel: 3 (a_lo b_hi + a_hi b_lo + a_hi b_hi) or 2 (no b_lo)
+  // single-chunk pair kernel: max |opA(row, :)| of the rows it converts
+  // (float bits, atomicMax; the exact maxima behind a run on sampled scales),
+  // and a device flag that skips the whole launch while it reads 0
+  unsigned* amax_out = nullptr;
+  const int* run_flag = nullptr;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -572,7 +577,9 @@ __global__ void tc_split_kernel(const float* __restrict__ X, int64_t K, int n_sr
 __global__ void __launch_bounds__(512)
     tc_split16_col_kernel(const float* __restrict__ X, int64_t K, int n_src, int64_t ldx,
                           int64_t kld, uint16_t* __restrict__ hi, uint16_t* __restrict__ lo,
-                          float* __restrict__ col_inv, int qw = 0) {
+                          float* __restrict__ col_inv, int qw = 0,
+                          const int* __restrict__ run_flag = nullptr) {
+  if (run_flag != nullptr && *run_flag == 0) return;   // the product is skipped too
   __shared__ unsigned red[16];
   const int j = blockIdx.x;
   const float* col = X + (int64_t)j * ldx;
@@ -840,6 +847,85 @@ inline void absmax_rows_cols(Ctx& c, const float* A, int64_t m, int64_t n, int64
     const dim3 grid((unsigned)ceil_div(sr, 256), (unsigned)ceil_div(sc, 128));
     tc::absmax_rc_kernel<<<grid, 256, 0, c.stream>>>(A, sr, sc, lda, S_r, S_c);
   }
+  BRSVD_CHECK_LAUNCH();
+}
+
+namespace tc {
+// Sampled maxima along the outer index: per outer j, max |S| over chunks of
+// 128 contiguous entries every 4096 (1/32 of the line; one warp per line, a
+// chunk is one coalesced 512-byte load, all chunks of the line in flight).
+__global__ void amax_sample_outer_kernel(const float* __restrict__ S, int64_t sr, int64_t sc,
+                                         int64_t ld, float* __restrict__ out) {
+  constexpr int kChunks = 8;
+  const int lane = threadIdx.x & 31;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < sc;
+       j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const float* col = S + j * ld;
+    const bool vec = ((reinterpret_cast<uintptr_t>(col) & 15) == 0);
+    float mx = 0.f;
+    for (int64_t c00 = 0; c00 < sr; c00 += (int64_t)kChunks * 4096) {
+      float4 v[kChunks];
+#pragma unroll
+      for (int it = 0; it < kChunks; ++it) {
+        const int64_t c0 = c00 + (int64_t)it * 4096 + 4 * lane;
+        if (vec && c0 + 4 <= sr) {
+          v[it] = __ldcs(reinterpret_cast<const float4*>(col + c0));
+        } else {
+          v[it].x = c0 < sr ? col[c0] : 0.f;
+          v[it].y = c0 + 1 < sr ? col[c0 + 1] : 0.f;
+          v[it].z = c0 + 2 < sr ? col[c0 + 2] : 0.f;
+          v[it].w = c0 + 3 < sr ? col[c0 + 3] : 0.f;
+        }
+      }
+#pragma unroll
+      for (int it = 0; it < kChunks; ++it)
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[it].x), fabsf(v[it].y)),
+                             fmaxf(fabsf(v[it].z), fabsf(v[it].w))));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) out[j] = mx;
+  }
+}
+__global__ void scale_by_kernel(float* __restrict__ x, int64_t n, float f) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    x[i] *= f;
+}
+// flag = 1 if some row's exact maximum, under the scale its sampled maximum
+// gave, leaves [2^3, 65504): overflow of the fp16 high part, or fewer than
+// the split's 22 bits above the fp16 subnormal floor
+__global__ void lazy_scale_check_kernel(const float* __restrict__ guess,
+                                        const float* __restrict__ exact, int64_t n,
+                                        int* __restrict__ flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float x = exact[i];
+    if (!(x > 0.f) || !(x < INFINITY)) continue;
+    const float y = x * h16_scale(guess[i]);
+    if (!(y >= 8.f && y < 65504.f)) *flag = 1;
+  }
+}
+}  // namespace tc
+
+// Sampled row / column maxima of |A| (about 1/16 of A read), times 2^7: the
+// scales they give hold the true maxima in [2^3, 65504) unless a line's
+// largest entry is over 2^9 x its sampled one (lazy_scale_check_kernel).
+inline void amax_sampled(Ctx& c, const float* A, int64_t m, int64_t n, int64_t lda,
+                         bool row_major, float* g_rows, float* g_cols) {
+  const int64_t sr = row_major ? n : m, sc = row_major ? m : n;
+  // contiguous index: every 32nd line read whole
+  const int64_t sc32 = ceil_div(sc, 32);
+  if (row_major)
+    absmax_rows_cols(c, A, sc32, n, 32 * lda, true, nullptr, g_cols);
+  else
+    absmax_rows_cols(c, A, m, sc32, 32 * lda, false, g_rows, nullptr);
+  float* outer = row_major ? g_rows : g_cols;
+  tc::amax_sample_outer_kernel<<<(unsigned)std::min<int64_t>(ceil_div(sc, 8), 4096), 256, 0,
+                                 c.stream>>>(A, sr, sc, lda, outer);
+  BRSVD_CHECK_LAUNCH();
+  tc::scale_by_kernel<<<grid_for(m), 256, 0, c.stream>>>(g_rows, m, 128.f);
+  tc::scale_by_kernel<<<grid_for(n), 256, 0, c.stream>>>(g_cols, n, 128.f);
   BRSVD_CHECK_LAUNCH();
 }
 

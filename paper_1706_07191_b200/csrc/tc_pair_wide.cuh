@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(kThreadsW, 1)
   uint64_t* accfree = accready + 2;            // [2], per region
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accfree + 2);
 
+  if (p.run_flag != nullptr && *p.run_flag == 0) return;   // uniform: the whole grid
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cta_rank();
   const bool leader = crank == 0;
@@ -191,6 +192,8 @@ __global__ void __launch_bounds__(kThreadsW, 1)
     const int64_t grow = m0 + r;
     const float rscale =
         (p.row_max != nullptr && grow < p.M) ? h16_scale(p.row_max[grow]) : 1.f;
+    const bool want_max = p.amax_out != nullptr;
+    float amax = 0.f;
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % kStages;
       const uint32_t ph = (kb / kStages) & 1;
@@ -215,6 +218,10 @@ __global__ void __launch_bounds__(kThreadsW, 1)
 #pragma unroll
           for (int k = 0; k < 16; ++k) v[k] = lds32(box + (16 * qtr + k) * 128);
         }
+        if (want_max) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) amax = fmaxf(amax, fabsf(v[k]));
+        }
         uint32_t hi[8], lo[8];
 #pragma unroll
         for (int i2 = 0; i2 < 8; ++i2) {
@@ -231,6 +238,7 @@ __global__ void __launch_bounds__(kThreadsW, 1)
       __syncwarp();
       if (lane == 0) arrive_remote(tfull_l + 8u * s);
     }
+    if (want_max && grow < p.M) atomicMax(p.amax_out + grow, __float_as_uint(amax));
   } else if (warp >= 4 + kConvW) {  // ---------------- flushes + epilogue
     const int idx = warp - 4 - kConvW;          // 0..23
     const int wq = warp & 3;
@@ -297,14 +305,45 @@ __global__ void __launch_bounds__(kThreadsW, 1)
 
 // C = sum of the K-split partials in split order (deterministic), fp32
 __global__ void splitk_sum_f32_kernel(const float* __restrict__ part, int64_t M, int n,
-                                      int splits, float* __restrict__ C, int64_t ldc) {
+                                      int splits, float* __restrict__ C, int64_t ldc,
+                                      const int* __restrict__ run_flag) {
+  if (run_flag != nullptr && *run_flag == 0) return;
   const int64_t total = M * n;
+  if ((M & 3) == 0 && (ldc & 3) == 0 && ((reinterpret_cast<uintptr_t>(C) & 15) == 0)) {
+    // float4 along the columns (M % 4 == 0: a quad never straddles two)
+    const int64_t mq = M >> 2;
+    const float4* p4 = reinterpret_cast<const float4*>(part);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (total >> 2);
+         e += (int64_t)gridDim.x * blockDim.x) {
+      float4 v = p4[e];
+      for (int z = 1; z < splits; ++z) {
+        const float4 w = p4[(int64_t)z * (total >> 2) + e];
+        v.x += w.x;
+        v.y += w.y;
+        v.z += w.z;
+        v.w += w.w;
+      }
+      const int64_t col = e / mq, r4 = e - col * mq;
+      *reinterpret_cast<float4*>(C + col * ldc + 4 * r4) = v;
+    }
+    return;
+  }
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     float v = 0.f;
     for (int z = 0; z < splits; ++z) v += part[(int64_t)z * total + e];
     C[(e % M) + (e / M) * ldc] = v;
   }
+}
+
+// C (M x n) = 0 unless run_flag reads 0 (the two-split accumulator of a
+// launch that may be skipped)
+__global__ void zero_if_kernel(float* __restrict__ C, int64_t M, int n, int64_t ldc,
+                               const int* __restrict__ run_flag) {
+  if (run_flag != nullptr && *run_flag == 0) return;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M * n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    C[(e % M) + (e / M) * ldc] = 0.f;
 }
 
 // The single-chunk pair kernel for 160 < l <= 288 unless BRSVD_TCW=0.
@@ -319,7 +358,8 @@ inline bool fits(int l) { return l > 160 && l <= 288; }
 
 inline void tcw_gemm_launch(Ctx& c, const float* A, int64_t m, int64_t n, int64_t lda,
                             bool row_major, bool trans, const float* X, int64_t ldx, int l,
-                            float* C, int64_t ldc, const float* opa_max, double out_scale) {
+                            float* C, int64_t ldc, const float* opa_max, double out_scale,
+                            unsigned* amax_out = nullptr, const int* run_flag = nullptr) {
   using namespace tc;
   const int64_t M = trans ? n : m, K = trans ? m : n;
   const bool kmajor = row_major != trans;
@@ -344,6 +384,8 @@ inline void tcw_gemm_launch(Ctx& c, const float* A, int64_t m, int64_t n, int64_
   p.keep_scaled = 0;
   p.out_scale = out_scale;
   p.b_terms = 3;
+  p.amax_out = amax_out;
+  p.run_flag = run_flag;
   DBuf<float> hi, lo, opmax, cinv;
   const int64_t kld = ceil_div(K, 8) * 8;
   if (opa_max == nullptr) {
@@ -357,7 +399,7 @@ inline void tcw_gemm_launch(Ctx& c, const float* A, int64_t m, int64_t n, int64_
   lo.alloc(c, (size_t)npad * kld / 2 + 8);
   tc_split16_col_kernel<<<(unsigned)npad, 512, 0, c.stream>>>(
       X, K, l, ldx, kld, reinterpret_cast<uint16_t*>(hi.p), reinterpret_cast<uint16_t*>(lo.p),
-      cinv.p);
+      cinv.p, 0, run_flag);
   BRSVD_CHECK_LAUNCH();
   const CUtensorMap mapBhi =
       make_map(hi.p, (uint64_t)kld, (uint64_t)npad, (uint64_t)kld * 2, BK_H16,
@@ -384,14 +426,20 @@ inline void tcw_gemm_launch(Ctx& c, const float* A, int64_t m, int64_t n, int64_
       best = ks;
     }
   }
+  if (const char* f = std::getenv("BRSVD_TCW_KSPLIT")) best = std::max(1, std::min(8, atoi(f)));
   p.ksplit = best;
   DBuf<float> part;
   if (p.ksplit > 2) {
     part.alloc(c, (size_t)p.ksplit * M * l);
     p.part = part.p;
   } else if (p.ksplit == 2) {
-    BRSVD_CUDA(cudaMemset2DAsync(C, (size_t)ldc * sizeof(float), 0, (size_t)M * sizeof(float),
-                                 (size_t)l, c.stream));
+    if (run_flag != nullptr) {
+      tcw::zero_if_kernel<<<grid_for(M * l), 256, 0, c.stream>>>(C, M, l, ldc, run_flag);
+      BRSVD_CHECK_LAUNCH();
+    } else {
+      BRSVD_CUDA(cudaMemset2DAsync(C, (size_t)ldc * sizeof(float), 0,
+                                   (size_t)M * sizeof(float), (size_t)l, c.stream));
+    }
   }
   const size_t smem = tcw::smem_bytes(nc);
   cudaLaunchConfig_t cfg = {};
@@ -424,7 +472,7 @@ inline void tcw_gemm_launch(Ctx& c, const float* A, int64_t m, int64_t n, int64_
   ++g_brsvd_launches;
   if (p.part != nullptr) {
     tcw::splitk_sum_f32_kernel<<<grid_for(M * l), 256, 0, c.stream>>>(part.p, M, l, p.ksplit, C,
-                                                                  ldc);
+                                                                  ldc, run_flag);
     BRSVD_CHECK_LAUNCH();
   }
 }

@@ -824,9 +824,26 @@ inline bool tcs_gemm_launch(Ctx& c, const float* A, int64_t m, int64_t n, int64_
 
 // The fp32 A-streaming product: the persistent cluster kernel when the shape
 // allows, else the per-tile tc3 kernel.
+// The product dispatch below picks the single-chunk pair kernel for this l
+// (the only one that can run on sampled scales, LazyScales in pipeline.cuh).
+inline bool tcw_selected(Ctx& c, int l) {
+  return !tcs::env_enabled() && tcw::enabled() && tcp::enabled() && tc::h16_enabled() &&
+         tcw::fits(l) && !c.b_hi_only;
+}
+
+// amax_out / run_flag: see Params (single-chunk pair kernel only; the caller
+// checks tcw_selected first).
 inline void tc_product(Ctx& c, const float* A, int64_t m, int64_t n, int64_t lda,
                        bool row_major, bool trans, const float* X, int64_t ldx, int l, float* C,
-                       int64_t ldc, const float* opa_max = nullptr, double out_scale = 1.0) {
+                       int64_t ldc, const float* opa_max = nullptr, double out_scale = 1.0,
+                       unsigned* amax_out = nullptr, const int* run_flag = nullptr) {
+  if (amax_out != nullptr || run_flag != nullptr) {
+    if (!tcw_selected(c, l))
+      throw Error(kErrArg, "tc_product: sampled scales need the single-chunk pair kernel");
+    tcw_gemm_launch(c, A, m, n, lda, row_major, trans, X, ldx, l, C, ldc, opa_max, out_scale,
+                    amax_out, run_flag);
+    return;
+  }
   if (tcs_gemm_launch(c, A, m, n, lda, row_major, trans, X, ldx, l, C, ldc, opa_max,
                       out_scale))
     return;
