@@ -146,38 +146,55 @@ __global__ void __launch_bounds__(kCiThreads, 1)
     }
     __syncthreads();
     if (pi == 0) CI_T(2);
-    // factor the diagonal block right-looking with all threads: per column a
-    // pivot (rsqrt, no divisions -- piv/dg is only recorded for info[0]), a
-    // column scale and a rank-1 update of the trailing block, three barriers
+    // factor the diagonal block in ONE warp, rows in registers: lane i holds
+    // row i of the block, shifted so that the current column is always a[0]
+    // (the column loop is not unrolled: straight-line code for 32 columns does
+    // not fit the instruction cache).  Per column the pivot comes from lane c
+    // by a shuffle, rsqrt (no divisions -- piv/dg is only recorded for
+    // info[0]), and the rank-1 update broadcasts every lane's scaled entry by
+    // branch-free shuffles (all in flight before the FMAs); no barriers.
     double* rinv = Di + kCiNB * kCiLd - kCiNB;   // 1 / L11[c][c] for the TRSM
-    for (int c = 0; c < nb; ++c) {
-      const double piv = Lp[c * kCiLd + c];
-      const double dg = d0[p0 + c];
-      const bool drop = !(piv > 0.0) ||
-                        (drop_ratio > 0.0 && (!(dg > 0.0) || !(piv > drop_ratio * dg)));
-      const double inv = drop ? 0.0 : rsqrt(piv);
-      __syncthreads();
-      if (tid == 0) {
-        const double dsq = piv * inv;
-        Lp[c * kCiLd + c] = drop ? 1.0 : dsq;
-        rinv[c] = drop ? 1.0 : inv;
-        dropped[p0 + c] = drop ? 1 : 0;
-        dL[p0 + c] = drop ? 0.0 : dsq;
-        Rat[p0 + c] = piv;
+    if (warp == 0) {
+      const int i = lane;
+      double a[kCiNB];
+#pragma unroll
+      for (int jj = 0; jj < kCiNB; ++jj)
+        a[jj] = (i < nb && jj <= i) ? Lp[i * kCiLd + jj] : 0.0;
+#pragma unroll 1
+      for (int c = 0; c < nb; ++c) {
+        const double piv = __shfl_sync(0xffffffffu, a[0], c);
+        const double dg = d0[p0 + c];
+        const bool drop = !(piv > 0.0) ||
+                          (drop_ratio > 0.0 && (!(dg > 0.0) || !(piv > drop_ratio * dg)));
+        const double inv = drop ? 0.0 : rsqrt(piv);
+        const double lc = (i > c && i < nb) ? a[0] * inv : 0.0;
+        if (i == c) {
+          const double dsq = piv * inv;
+          Lp[c * kCiLd + c] = drop ? 1.0 : dsq;
+          rinv[c] = drop ? 1.0 : inv;
+          dropped[p0 + c] = drop ? 1 : 0;
+          dL[p0 + c] = drop ? 0.0 : dsq;
+          Rat[p0 + c] = piv;
+        } else if (i < nb) {
+          Lp[i * kCiLd + c] = lc;   // 0 above the diagonal
+        }
+        // lanes beyond the block hold lc = 0, so a[jj] of lanes i < c + jj
+        // only ever gets lc_i * lc_j with one factor zero or is unused
+        // two batches of 16 shuffles (register budget: the row takes 64)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double lj[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            lj[q] = __shfl_sync(0xffffffffu, lc, (c + 16 * h + q + 1) & 31);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int jj = 16 * h + q + 1;
+            if (jj < kCiNB) a[jj - 1] = fma(-lc, lj[q], a[jj]);
+          }
+        }
+        a[kCiNB - 1] = 0.0;
       }
-      const int rest = nb - c - 1;
-      if (tid < rest) Lp[(c + 1 + tid) * kCiLd + c] *= inv;
-      __syncthreads();
-      for (int e = tid; e < rest * rest; e += nt) {
-        const int i = c + 1 + e % rest, j = c + 1 + e / rest;
-        if (i >= j) Lp[i * kCiLd + j] = fma(-Lp[i * kCiLd + c], Lp[j * kCiLd + c], Lp[i * kCiLd + j]);
-      }
-    }
-    __syncthreads();
-    // zero the strict upper triangle of the block
-    for (int e = tid; e < nb * nb; e += nt) {
-      const int i = e % nb, j = e / nb;
-      if (i < j) Lp[i * kCiLd + j] = 0.0;
     }
     __syncthreads();
     if (pi == 0) CI_T(3);
@@ -207,13 +224,12 @@ __global__ void __launch_bounds__(kCiThreads, 1)
       }
     }
     __syncthreads();
-    if (leader) {
-      // write the panel (L) and the diagonal-block inverse (X) back
-      for (int e = tid; e < rows * nb; e += nt) {
-        const int i = e % rows, c = e / rows;
-        if (i >= c)
-          A[(int64_t)(p0 + c) * ld + (p0 + i)] = i < nb ? Lp[i * kCiLd + c] : PT[c * ldp + i];
-      }
+    // write the panel (L) back, its columns split over the cluster (every
+    // CTA holds the same panel; the leader alone writing it held up the
+    // cluster barrier below)
+    for (int c = me; c < nb; c += C) {
+      double* dst = A + (int64_t)(p0 + c) * ld + p0;
+      for (int i = c + tid; i < rows; i += nt) dst[i] = i < nb ? Lp[i * kCiLd + c] : PT[c * ldp + i];
     }
     if (pi == 0) CI_T(4);
     // trailing update: A22 -= L21 L21^T (lower), 4x4 register tiles, split
