@@ -132,3 +132,28 @@ def test_fp64_product_edges(m, n, l, layout, trans):
     bound = (A.abs().t() if trans else A.abs()) @ X.abs()
     err = ((C - ref).abs() / bound.clamp_min(1e-300)).max().item()
     assert err <= 1e-14, err
+
+
+@pytest.mark.parametrize("ksplit", ["1", "2", "3", "4"])
+@pytest.mark.parametrize("l", [200, 288])
+@pytest.mark.parametrize("layout,trans", [("row", False), ("col", True), ("col", False)])
+def test_single_chunk_pair_ksplits(ksplit, l, layout, trans, monkeypatch):
+    """The single-chunk CTA-pair product (160 < l <= 288) with 1-4 K-splits
+    forced (BRSVD_TCW_KSPLIT): every split count meets the fp32-level bound,
+    and a split count > 1 (partials summed in split order) is deterministic."""
+    import torch
+    from paper_1706_07191_b200.rsvd import sketch_product
+    monkeypatch.setenv("BRSVD_TCW_KSPLIT", ksplit)
+    m, n = (16384, 1000) if trans else (1000, 16384)
+    g = torch.Generator(device="cuda").manual_seed(l + 11 * int(ksplit))
+    A = torch.randn(m, n, generator=g, device="cuda", dtype=torch.float32)
+    if layout == "col":
+        A = A.t().contiguous().t()
+    X = torch.randn(m if trans else n, l, generator=g, device="cuda", dtype=torch.float32)
+    C = sketch_product(A, X, trans=trans)
+    A64 = A.double()
+    ref = (A64.t() if trans else A64) @ X.double()
+    bound = (A64.abs().t() if trans else A64.abs()) @ X.double().abs()
+    err = ((C.double() - ref).abs() / bound.clamp_min(1e-30)).max().item()
+    assert err <= 2e-6, err
+    assert torch.equal(C, sketch_product(A, X, trans=trans))
