@@ -50,18 +50,27 @@ __global__ void compact_cols_kernel(const double* __restrict__ T, int l,
 constexpr int kCiNB = 32;
 constexpr int kCiLd = 33;       // padded row stride of the shared panel
 constexpr int kCiThreads = 512;
+constexpr int kCiMaxBlk = 10;   // block rows of the largest order (kCholMaxL = 320)
 __device__ long long g_ci_t[64];
 #define CI_T(k) do { if (me == 0 && tid == 0) g_ci_t[(k)] = clock64(); } while (0)
 
 __host__ __device__ inline int cholinv_ldp(int n) { return (n + 3) & ~3; }
+// Columns of each block column of X = L^-1 owned by one CTA in phase 2 (the
+// launch uses an 8-CTA cluster for n > 96, one CTA otherwise).
+__host__ __device__ inline int cholinv_cpc(int n) { return n > 96 ? kCiNB / 8 : kCiNB; }
 __host__ __device__ inline size_t cholinv_big(int n) {
   const size_t p1 = (size_t)n * kCiLd + (size_t)kCiNB * cholinv_ldp(n);  // phase 1 panels
   const size_t nblk = (size_t)(n + kCiNB - 1) / kCiNB;
-  const size_t p2 = (2 * nblk + 2) * kCiNB * kCiLd;                     // phase 2
+  const size_t ldxm = nblk * cholinv_cpc(n);
+  const size_t xm = nblk * kCiNB * ldxm;
+  // phase 2: Dinv blocks, X columns (also the staging area of the diagonal
+  // blocks), one staged L block, the block-row sums
+  const size_t p2 = nblk * kCiNB * kCiLd + (xm > nblk * kCiNB * kCiLd ? xm : nblk * kCiNB * kCiLd) +
+                    (size_t)kCiNB * kCiNB + kCiNB * ldxm;
   return p1 > p2 ? p1 : p2;
 }
 inline size_t cholinv_smem(int n) {
-  return (cholinv_big(n) + (size_t)kCiNB * kCiLd + 4 * (size_t)n) * sizeof(double) +
+  return (cholinv_big(n) + (size_t)kCiNB * kCiLd + 4 * (size_t)n + 130) * sizeof(double) +
          (size_t)n * sizeof(int);
 }
 
@@ -83,7 +92,9 @@ __global__ void __launch_bounds__(kCiThreads, 1)
   double* d0 = sc + n;                    // scaled diagonal + shift
   double* dL = d0 + n;                    // diagonal of L
   double* Rat = dL + n;                   // pivots (for info[0] = min pivot / diagonal)
-  int* dropped = reinterpret_cast<int*>(Rat + n);
+  // column broadcast of the diagonal factor (128, 16-byte aligned)
+  double* bcst = Rat + n + ((reinterpret_cast<uintptr_t>(Rat + n) & 15) ? 1 : 0);
+  int* dropped = reinterpret_cast<int*>(Rat + n + 130);
   __shared__ double s_red[32];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
@@ -151,8 +162,11 @@ __global__ void __launch_bounds__(kCiThreads, 1)
     // (the column loop is not unrolled: straight-line code for 32 columns does
     // not fit the instruction cache).  Per column the pivot comes from lane c
     // by a shuffle, rsqrt (no divisions -- piv/dg is only recorded for
-    // info[0]), and the rank-1 update broadcasts every lane's scaled entry by
-    // branch-free shuffles (all in flight before the FMAs); no barriers.
+    // info[0]), and the rank-1 update reads the scaled column back from a
+    // shared broadcast buffer: lane i stores l_i at slot 32 + i - c - 1 (and a
+    // zero 32 slots further, so slots past the block read 0), every lane then
+    // loads slots 32..63 with 16-byte broadcast loads -- 16 loads per column
+    // instead of 64 fp64 shuffle halves; no block barriers.
     double* rinv = Di + kCiNB * kCiLd - kCiNB;   // 1 / L11[c][c] for the TRSM
     if (warp == 0) {
       const int i = lane;
@@ -160,6 +174,7 @@ __global__ void __launch_bounds__(kCiThreads, 1)
 #pragma unroll
       for (int jj = 0; jj < kCiNB; ++jj)
         a[jj] = (i < nb && jj <= i) ? Lp[i * kCiLd + jj] : 0.0;
+      const double2* b2 = reinterpret_cast<const double2*>(bcst + 32);
 #pragma unroll 1
       for (int c = 0; c < nb; ++c) {
         const double piv = __shfl_sync(0xffffffffu, a[0], c);
@@ -168,6 +183,10 @@ __global__ void __launch_bounds__(kCiThreads, 1)
                           (drop_ratio > 0.0 && (!(dg > 0.0) || !(piv > drop_ratio * dg)));
         const double inv = drop ? 0.0 : rsqrt(piv);
         const double lc = (i > c && i < nb) ? a[0] * inv : 0.0;
+        __syncwarp();   // the previous column's broadcast loads are done
+        bcst[32 + i - c - 1] = lc;
+        bcst[64 + i - c - 1] = 0.0;
+        __syncwarp();
         if (i == c) {
           const double dsq = piv * inv;
           Lp[c * kCiLd + c] = drop ? 1.0 : dsq;
@@ -178,19 +197,18 @@ __global__ void __launch_bounds__(kCiThreads, 1)
         } else if (i < nb) {
           Lp[i * kCiLd + c] = lc;   // 0 above the diagonal
         }
-        // lanes beyond the block hold lc = 0, so a[jj] of lanes i < c + jj
-        // only ever gets lc_i * lc_j with one factor zero or is unused
-        // two batches of 16 shuffles (register budget: the row takes 64)
+        // lanes i <= c hold lc = 0, so a[jj] of lanes i < c + jj only ever
+        // gets lc_i * lc_j with one factor zero or is unused
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          double lj[16];
+          double2 lj[8];
 #pragma unroll
-          for (int q = 0; q < 16; ++q)
-            lj[q] = __shfl_sync(0xffffffffu, lc, (c + 16 * h + q + 1) & 31);
+          for (int q = 0; q < 8; ++q) lj[q] = b2[8 * h + q];
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int jj = 16 * h + q + 1;
-            if (jj < kCiNB) a[jj - 1] = fma(-lc, lj[q], a[jj]);
+          for (int q = 0; q < 8; ++q) {
+            const int jj = 16 * h + 2 * q + 1;
+            a[jj - 1] = fma(-lc, lj[q].x, a[jj]);
+            if (jj + 1 < kCiNB) a[jj] = fma(-lc, lj[q].y, a[jj + 1]);
           }
         }
         a[kCiNB - 1] = 0.0;
@@ -297,24 +315,33 @@ __global__ void __launch_bounds__(kCiThreads, 1)
   }
 
   CI_T(6);
-  // ---- phase 2: T = S L^-T by block columns of X = L^-1 -----------------
-  // Block column J of X depends only on L: X_JJ = L_JJ^-1 and, for I > J,
-  // X_IJ = -L_II^-1 sum_{K=J..I-1} L_IK X_KJ.  Every CTA inverts the diagonal
-  // blocks (one warp each), then builds its own block columns J = me, me+C, ..
-  // in shared memory and writes rows J of T (T[k][j] = s_k X[j][k]) directly;
-  // no cluster barrier.
+  // ---- phase 2: T = S L^-T from X = L^-1, columns split over the cluster --
+  // Every block column J of X obeys X_JJ = L_JJ^-1 and, for I > J,
+  // X_IJ = -L_II^-1 sum_{K=J..I-1} L_IK X_KJ, and the columns of X are
+  // independent: CTA me owns columns me*cpc .. me*cpc+cpc-1 of EVERY block
+  // column (cpc = 32 / cluster size), so the work is balanced and the chain
+  // is one block row per step.  Every CTA inverts the diagonal blocks (one
+  // warp each), then walks the block rows I = 1..: the sums over K are
+  // accumulated with 2 x 2 register tiles against L_IK staged k-major in
+  // shared memory, then multiplied by -L_II^-1.  Rows k of T (k one of this
+  // CTA's columns) are written directly: T[k][j] = s_k X[j][k]; no cluster
+  // barrier.
   const int nblk = (n + kCiNB - 1) / kCiNB;
+  const int cpc = kCiNB / C;                             // == cholinv_cpc(n)
+  const int ldxm = nblk * cpc;                           // this CTA's columns
   constexpr int BB = kCiNB * kCiLd;                      // one 32 x 33 block
   double* Dinv = cism;                                   // nblk blocks: L_II^-1
-  double* Xc = cism + (size_t)nblk * BB;                 // nblk blocks: column J of X
-  double* Rb = Xc + (size_t)nblk * BB;                   // scratch block
-  double* Lt = Rb + BB;                                  // staged L_IK block
-  // diagonal blocks of L -> Xc (scratch), inverted by one warp each into Dinv
+  double* XM = cism + (size_t)nblk * BB;                 // X rows x this CTA's columns
+  const size_t xm_sz = (size_t)nblk * kCiNB * ldxm;
+  double* Lt = XM + (xm_sz > (size_t)nblk * BB ? xm_sz : (size_t)nblk * BB);  // L_IK, k-major
+  double* Rb = Lt + kCiNB * kCiNB;                       // 32 x ldxm block-row sums
+  // diagonal blocks of L -> XM (scratch), inverted by one warp each into Dinv
+  double* Xs = XM;
   for (int e = tid; e < nblk * kCiNB * kCiNB; e += nt) {
     const int bI = e / (kCiNB * kCiNB), rc = e % (kCiNB * kCiNB);
     const int r = rc % kCiNB, cc = rc / kCiNB, i0 = bI * kCiNB;
     const bool ok = i0 + r < n && i0 + cc < n && r >= cc;
-    Xc[(size_t)bI * BB + r * kCiLd + cc] = ok ? A[(int64_t)(i0 + cc) * ld + (i0 + r)] : 0.0;
+    Xs[(size_t)bI * BB + r * kCiLd + cc] = ok ? A[(int64_t)(i0 + cc) * ld + (i0 + r)] : 0.0;
   }
   __syncthreads();
   // Each diagonal block inverted by one warp, right-looking: lane c owns
@@ -325,7 +352,7 @@ __global__ void __launch_bounds__(kCiThreads, 1)
   // The dependent chain per row is one multiply and one FMA.
   for (int bI = warp; bI < nblk; bI += nw) {
     const int nbI = min(kCiNB, n - bI * kCiNB);
-    const double* Lb = Xc + (size_t)bI * BB;
+    const double* Lb = Xs + (size_t)bI * BB;
     double* Dv = Dinv + (size_t)bI * BB;
     const int c = lane;
     const double dgl = Lb[c * kCiLd + c];
@@ -349,91 +376,89 @@ __global__ void __launch_bounds__(kCiThreads, 1)
     }
   }
   __syncthreads();
-  for (int bJ = me; bJ < nblk; bJ += C) {
-    const int j0 = bJ * kCiNB, nbJ = min(kCiNB, n - j0);
-    for (int e = tid; e < BB; e += nt) Xc[(size_t)bJ * BB + e] = Dinv[(size_t)bJ * BB + e];
-    __syncthreads();
-    for (int bI = bJ + 1; bI < nblk; ++bI) {
-      const int i0 = bI * kCiNB, nbI = min(kCiNB, n - i0);
-      // Rb = sum_{K=J..I-1} L_IK X_KJ, L_IK staged block by block
-      double acc4[4] = {0.0, 0.0, 0.0, 0.0};
-      // the next L_IK block is loaded into registers while the current one
-      // is consumed (global latency off the critical path)
-      double nxt[2];
-      auto fetch = [&](int bK) {
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int e = tid + q * nt;
-          const int r = e % kCiNB, kk = e / kCiNB;
-          nxt[q] = (r < nbI) ? A[(int64_t)(bK * kCiNB + kk) * ld + (i0 + r)] : 0.0;
-        }
-      };
-      fetch(bJ);
-      for (int bK = bJ; bK < bI; ++bK) {
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int e = tid + q * nt;
-          Lt[(e % kCiNB) * kCiLd + e / kCiNB] = nxt[q];
-        }
-        __syncthreads();
-        if (bK + 1 < bI) fetch(bK + 1);
-        const double* xk = Xc + (size_t)bK * BB;
-        // 256 threads: row r, columns 4 cg .. 4 cg + 3 (the L_IK value is
-        // reused from a register, the X_KJ values are warp broadcasts)
-        if (tid < 256) {
-          const int r = tid % kCiNB, c0 = 4 * (tid / kCiNB);
-#pragma unroll 8
-          for (int kk = 0; kk < kCiNB; ++kk) {
-            const double lv = Lt[r * kCiLd + kk];
-            acc4[0] = fma(lv, xk[kk * kCiLd + c0], acc4[0]);
-            acc4[1] = fma(lv, xk[kk * kCiLd + c0 + 1], acc4[1]);
-            acc4[2] = fma(lv, xk[kk * kCiLd + c0 + 2], acc4[2]);
-            acc4[3] = fma(lv, xk[kk * kCiLd + c0 + 3], acc4[3]);
-          }
-        }
-        __syncthreads();
-      }
-      if (tid < 256) {
-        const int r = tid % kCiNB, c0 = 4 * (tid / kCiNB);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) Rb[r * kCiLd + c0 + q] = acc4[q];
-      }
-      __syncthreads();
-      // X_IJ = -L_II^-1 Rb
-      const double* Dv = Dinv + (size_t)bI * BB;
-      double* xo = Xc + (size_t)bI * BB;
-      for (int e = tid; e < kCiNB * kCiNB; e += nt) {
-        const int r = e % kCiNB, cc = e / kCiNB;
-        double v = 0.0;
-        for (int j = 0; j <= r; ++j) v = fma(Dv[r * kCiLd + j], Rb[j * kCiLd + cc], v);
-        xo[r * kCiLd + cc] = -v;
-      }
-      __syncthreads();
-    }
-    // rows k in block J of T: T[k][j] = s_k X[j][k] for j >= k (X row j lives
-    // in block I(j) >= J of this column), 0 below the diagonal; zero the
-    // strict upper triangle of A (L) in these columns
-    for (int e = tid; e < kCiNB * n; e += nt) {
-      const int kk = e % kCiNB, j = e / kCiNB;
-      const int k = j0 + kk;
-      if (kk >= nbJ) continue;
-      double v = 0.0;
-      if (j >= k) {
-        const int bI = j / kCiNB;
-        v = sc[k] * Xc[(size_t)bI * BB + (j - bI * kCiNB) * kCiLd + kk];
-      }
-      T[(int64_t)j * n + k] = v;
-    }
-    for (int e = tid; e < nbJ * j0; e += nt) {
-      const int i = e % j0, cc = e / j0;
-      A[(int64_t)(j0 + cc) * ld + i] = 0.0;
-    }
-    for (int e = tid; e < nbJ * nbJ; e += nt) {
-      const int i = e % nbJ, cc = e / nbJ;
-      if (i < cc) A[(int64_t)(j0 + cc) * ld + (j0 + i)] = 0.0;
-    }
-    __syncthreads();
+  CI_T(9);
+  // block row 0: X_00 restricted to this CTA's columns
+  for (int e = tid; e < kCiNB * cpc; e += nt) {
+    const int r = e / cpc, u = e % cpc;
+    XM[r * ldxm + u] = Dinv[r * kCiLd + me * cpc + u];
   }
+  for (int bI = 1; bI < nblk; ++bI) {
+    const int i0 = bI * kCiNB, nbI = min(kCiNB, n - i0);
+    const int na = bI * cpc;            // active columns: blocks J < I
+    // work item: rows 2 rp, 2 rp + 1 and local columns 2 cp, 2 cp + 1 (same J)
+    const int rp = tid & 15, cp = tid >> 4;
+    const bool act = 2 * cp < na;
+    const int jcol = act ? (2 * cp) / cpc : 0;
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    // the whole block row L_I,0..I-1 is loaded into registers up front (one
+    // global latency per block row instead of one per block)
+    double pre[kCiMaxBlk][2];
+#pragma unroll
+    for (int bK = 0; bK < kCiMaxBlk; ++bK)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int e = tid + q * nt;
+        const int r = e % kCiNB, kk = e / kCiNB;
+        pre[bK][q] = (bK < bI && r < nbI) ? A[(int64_t)(bK * kCiNB + kk) * ld + (i0 + r)] : 0.0;
+      }
+#pragma unroll
+    for (int bK = 0; bK < kCiMaxBlk; ++bK) {
+      if (bK >= bI) break;
+      __syncthreads();   // previous Lt consumed (and XM rows of block bK written)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) Lt[tid + q * nt] = pre[bK][q];   // Lt[kk][r]
+      __syncthreads();
+      if (act && jcol <= bK) {
+        const double* xr = XM + (size_t)bK * kCiNB * ldxm + 2 * cp;
+#pragma unroll 8
+        for (int kk = 0; kk < kCiNB; ++kk) {
+          const double2 lv = *reinterpret_cast<const double2*>(Lt + kk * kCiNB + 2 * rp);
+          const double2 xv = *reinterpret_cast<const double2*>(xr + (size_t)kk * ldxm);
+          acc[0][0] = fma(lv.x, xv.x, acc[0][0]);
+          acc[0][1] = fma(lv.x, xv.y, acc[0][1]);
+          acc[1][0] = fma(lv.y, xv.x, acc[1][0]);
+          acc[1][1] = fma(lv.y, xv.y, acc[1][1]);
+        }
+      }
+    }
+    if (act) {
+      *reinterpret_cast<double2*>(Rb + (2 * rp) * ldxm + 2 * cp) = make_double2(acc[0][0], acc[0][1]);
+      *reinterpret_cast<double2*>(Rb + (2 * rp + 1) * ldxm + 2 * cp) =
+          make_double2(acc[1][0], acc[1][1]);
+    }
+    __syncthreads();
+    // X_IJ = -L_II^-1 Rb (J < I); X_II = L_II^-1 restricted to our columns
+    const double* Dv = Dinv + (size_t)bI * BB;
+    double* xo = XM + (size_t)i0 * ldxm;
+    for (int e = tid; e < kCiNB * na; e += nt) {
+      const int r = e % kCiNB, cc = e / kCiNB;
+      double v = 0.0;   // Dv is zero above the diagonal: fixed trip count
+#pragma unroll 8
+      for (int j = 0; j < kCiNB; ++j) v = fma(Dv[r * kCiLd + j], Rb[j * ldxm + cc], v);
+      xo[r * ldxm + cc] = -v;
+    }
+    for (int e = tid; e < kCiNB * cpc; e += nt) {
+      const int r = e / cpc, u = e % cpc;
+      xo[r * ldxm + na + u] = Dv[r * kCiLd + me * cpc + u];
+    }
+  }
+  __syncthreads();
+  CI_T(10);
+  // rows k of T for this CTA's columns k: T[k][j] = s_k X[j][k] for j >= k, 0
+  // below the diagonal; zero the strict upper triangle of A (L) in these
+  // columns
+  for (int e = tid; e < ldxm * n; e += nt) {
+    const int lc = e % ldxm, j = e / ldxm;
+    const int k = (lc / cpc) * kCiNB + me * cpc + lc % cpc;
+    if (k >= n) continue;
+    T[(int64_t)j * n + k] = j >= k ? sc[k] * XM[(size_t)j * ldxm + lc] : 0.0;
+  }
+  for (int e = tid; e < ldxm * n; e += nt) {
+    const int lc = e / n, i = e % n;
+    const int k = (lc / cpc) * kCiNB + me * cpc + lc % cpc;
+    if (k < n && i < k) A[(int64_t)k * ld + i] = 0.0;
+  }
+  __syncthreads();
   CI_T(7);
   if (leader && info) {
     // info[0] = min pivot / diagonal, info[1] = reference rank, info[2] =
@@ -532,12 +557,13 @@ inline void cholinv_launch(cudaStream_t st, size_t smem_limit, double* A, int n,
   if (e != cudaSuccess)
     throw Error(kErrCuda, std::string("cholinv launch: ") + cudaGetErrorString(e));
   if (std::getenv("BRSVD_CI_TIMING")) {
-    long long t[9];
+    long long t[11];
     cudaStreamSynchronize(st);
     cudaMemcpyFromSymbol(t, g_ci_t, sizeof(t));
     std::fprintf(stderr, "[cholinv n=%d] scale %lld | p0: load %lld diag %lld trsm %lld trail %lld | "
-                 "panels %lld | inverse %lld | out %lld (cycles)\n", n, t[1] - t[0], t[2] - t[1],
-                 t[3] - t[2], t[4] - t[3], t[5] - t[4], t[6] - t[1], t[7] - t[6], t[8] - t[7]);
+                 "panels %lld | inverse %lld (diag blocks %lld, block rows %lld) | out %lld (cycles)\n", n,
+                 t[1] - t[0], t[2] - t[1], t[3] - t[2], t[4] - t[3], t[5] - t[4], t[6] - t[1],
+                 t[7] - t[6], t[9] - t[6], t[10] - t[9], t[8] - t[7]);
   }
 }
 
