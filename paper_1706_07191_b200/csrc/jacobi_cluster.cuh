@@ -249,6 +249,7 @@ __host__ __device__ inline size_t jacobi_cluster_smem(int l, int bw) {
 // Cycle split of the last launch (CTA 0, thread 0): rotations, cluster
 // barriers, block pulls, rounds (BRSVD_JC_TIMING=1 prints it).
 __device__ long long g_jc_t[4];
+__device__ float g_jc_c2[64];   // largest rotated cos^2 of each sweep (last launch)
 
 template <typename R, int NP2>
 __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
@@ -410,6 +411,7 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
           tot += *cluster.map_shared_rank(&s_cnt[sweep & 1], q);
           c2 = fmaxf(c2, *cluster.map_shared_rank(&s_c2[sweep & 1], q));
         }
+        if (me == 0 && sweep < 64) g_jc_c2[sweep] = c2;
         s_stop = (tot == 0) || (sweep + 1 >= a.max_sweeps) ||
                  (a.stop_cos > 0.0 && (double)c2 < a.stop_cos * a.stop_cos);
         s_cnt[(sweep + 1) & 1] = 0;

@@ -388,6 +388,10 @@ inline int jacobi(Ctx& c, R* G, int nrow, int ncol, int64_t ldg, R* V, int64_t l
           std::fprintf(stderr,
                        "[brsvd]   cycles: rotations %lld  cluster barriers %lld  pulls %lld"
                        "  (%lld rounds)\n", t[0], t[1], t[2], t[3]);
+          float c2[64];
+          BRSVD_CUDA(cudaMemcpyFromSymbol(c2, g_jc_c2, sizeof(c2)));
+          for (int s = 0; s < nsw && s < 64; ++s)
+            std::fprintf(stderr, "[brsvd]   sweep %d: max |cos| %.3e\n", s, std::sqrt((double)c2[s]));
         }
       }
       return 0;
