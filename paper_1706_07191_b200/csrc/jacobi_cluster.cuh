@@ -20,18 +20,35 @@
 // A column rotation is one warp: the two columns stay in registers from the
 // dot products to the update (NP2 row pairs per lane, 8/16-byte shared-memory
 // accesses), the three reductions share one butterfly.
+// The accumulated rotation V is NOT carried through the tournament: every
+// scheduled pair logs its rotation (c, s, columns) and jacobi_vreplay_kernel
+// applies the log to V afterwards, one row of V per CTA (the rows are
+// independent under column rotations).  The cluster kernel then moves and
+// rotates G columns only -- half the DSMEM pull bytes and no V update on the
+// chain of every step.
 #pragma once
 #include <cooperative_groups.h>
 #include "common.cuh"
 
 namespace brsvd {
 
+template <typename R> struct Vec2;
+template <> struct Vec2<float> { using type = float2; };
+template <> struct Vec2<double> { using type = double2; };
+
+// One logged rotation (c, s): the scheduled pair (x, y) of V columns becomes
+// (c x - s y, s x + c y); (1, 0) for a pair that was not rotated (exact
+// identity).  The columns follow from the tournament schedule.
+template <typename R>
+using JcRot = typename Vec2<R>::type;
+
 template <typename R>
 struct JacobiClusterArgs {
   R* G;          // l x l, column-major, ld ldg  (overwritten by G V)
   int64_t ldg;
-  R* V;          // l x l, column-major, ld ldv  (accumulated rotations; identity on entry)
-  int64_t ldv;
+  JcRot<R>* log;     // rotation log: step t, slot (CTA, warp) at t * C * bw + slot
+  int64_t log_steps; // capacity in steps
+  int* prog;         // [0] steps logged so far, [1] 1 when final (read by the replay)
   int l;         // matrix order
   int bw;        // block width
   int max_sweeps;
@@ -59,18 +76,15 @@ __device__ __forceinline__ float jc_rsqrt<float>(float x) { return rsqrtf(x); }
 template <>
 __device__ __forceinline__ double jc_rsqrt<double>(double x) { return rsqrt(x); }  // 1 ulp
 
-template <typename R> struct Vec2;
-template <> struct Vec2<float> { using type = float2; };
-template <> struct Vec2<double> { using type = double2; };
 
-// Rotate columns (x, y) of G and (vx, vy) of V so that the G columns become
-// orthogonal.  One warp; columns are zero-padded to lp (a multiple of 4) and
+// Rotate columns (x, y) of G so that they become orthogonal; (c, s) of the
+// rotation are returned in cr, sr.  One warp; columns are zero-padded to lp (a multiple of 4) and
 // each lane owns row pairs (2 lane + 64 k, +1), k < NP2, kept in registers
 // from the dot products to the update.  Returns true if rotated.
 template <typename R, int NP2>
-__device__ __forceinline__ bool jc_rotate(R* __restrict__ x, R* __restrict__ y,
-                                          R* __restrict__ vx, R* __restrict__ vy, int lp,
-                                          R tol2, R floor2, int lane, R& c2max) {
+__device__ __forceinline__ bool jc_rotate(R* __restrict__ x, R* __restrict__ y, int lp,
+                                          R tol2, R floor2, int lane, R& c2max, R& cr,
+                                          R& sr) {
   using V2 = typename Vec2<R>::type;
   V2 xr[NP2], yr[NP2];
   R a = 0, b = 0, g = 0;
@@ -136,28 +150,20 @@ __device__ __forceinline__ bool jc_rotate(R* __restrict__ x, R* __restrict__ y,
       ny.y = s * xr[k].y + c * yr[k].y;
       *reinterpret_cast<V2*>(x + i) = nx;
       *reinterpret_cast<V2*>(y + i) = ny;
-      xr[k] = *reinterpret_cast<const V2*>(vx + i);
-      yr[k] = *reinterpret_cast<const V2*>(vy + i);
-      nx.x = c * xr[k].x - s * yr[k].x;
-      nx.y = c * xr[k].y - s * yr[k].y;
-      ny.x = s * xr[k].x + c * yr[k].x;
-      ny.y = s * xr[k].y + c * yr[k].y;
-      *reinterpret_cast<V2*>(vx + i) = nx;
-      *reinterpret_cast<V2*>(vy + i) = ny;
     }
   }
+  cr = c;
+  sr = s;
   return true;
 }
 
 // Cross-round rotation with the block-a column x held in registers for the
-// whole round (xr: G part, xv: V part) and the partner y in shared memory:
-// the x loads and stores of jc_rotate disappear from every step.  Returns
-// true if rotated.
+// whole round and the partner y in shared memory: the x loads and stores of
+// jc_rotate disappear from every step.  Returns true if rotated.
 template <typename R, int NP2>
 __device__ __forceinline__ bool jc_rotate_x(typename Vec2<R>::type (&xr)[NP2],
-                                            typename Vec2<R>::type (&xv)[NP2],
-                                            R* __restrict__ y, R* __restrict__ vy, int lp,
-                                            R tol2, R floor2, int lane, R& c2max) {
+                                            R* __restrict__ y, int lp, R tol2, R floor2,
+                                            int lane, R& c2max, R& cr, R& sr) {
   using V2 = typename Vec2<R>::type;
   V2 yr[NP2];
   R g = 0, aa = 0, b = 0;
@@ -218,32 +224,36 @@ __device__ __forceinline__ bool jc_rotate_x(typename Vec2<R>::type (&xr)[NP2],
     ny.y = s * x0.y + c * yr[k].y;
     if (i < lp) *reinterpret_cast<V2*>(y + i) = ny;
   }
-#pragma unroll
-  for (int k = 0; k < NP2; ++k) {
-    const int i = 2 * lane + 64 * k;
-    V2 yv;
-    if (i < lp) {
-      yv = *reinterpret_cast<const V2*>(vy + i);
-    } else {
-      yv.x = yv.y = R(0);
-    }
-    const V2 x0 = xv[k];
-    xv[k].x = c * x0.x - s * yv.x;
-    xv[k].y = c * x0.y - s * yv.y;
-    V2 ny;
-    ny.x = s * x0.x + c * yv.x;
-    ny.y = s * x0.y + c * yv.y;
-    if (i < lp) *reinterpret_cast<V2*>(vy + i) = ny;
-  }
+  cr = c;
+  sr = s;
   return true;
 }
 
-// Shared memory: buf[2][2 slots][bw columns][2 * lp] of R, where a column is
-// its G part (lp entries, lp = l rounded up to 4) followed by its V part.
+// Shared memory: buf[2][2 slots][bw columns][lp] of R (lp = l rounded up to 4).
 template <typename R>
 __host__ __device__ inline size_t jacobi_cluster_smem(int l, int bw) {
   const int lp = (l + 3) & ~3;
-  return (size_t)2 * 2 * bw * 2 * lp * sizeof(R);
+  return (size_t)2 * 2 * bw * lp * sizeof(R);
+}
+
+// Logged steps per sweep: the first round orthogonalises the 2 bw columns of
+// every block pair (2 bw - 1 steps), the nb - 2 other rounds the cross pairs
+// (bw steps).  Step index of round r, step st: jc_step(r, ..) + st.
+__host__ __device__ inline int64_t jc_sweep_steps(int bw, int nb) {
+  return (int64_t)(2 * bw - 1) + (int64_t)(nb - 2) * bw;
+}
+__device__ __forceinline__ void jc_st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int jc_ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int64_t jc_step(int r, int bw, int nb) {
+  const int tr = r % (nb - 1);
+  return (int64_t)(r / (nb - 1)) * jc_sweep_steps(bw, nb) +
+         (tr == 0 ? 0 : (int64_t)(2 * bw - 1) + (int64_t)(tr - 1) * bw);
 }
 
 // Cycle split of the last launch (CTA 0, thread 0): rotations, cluster
@@ -264,7 +274,7 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
 
   const int l = a.l, bw = a.bw;
   const int lp = (l + 3) & ~3;
-  const int colsz = 2 * lp;                    // G part + V part
+  const int colsz = lp;                        // G columns only
   const size_t slotsz = (size_t)bw * colsz;    // one block
   const size_t bufsz = 2 * slotsz;             // two blocks
   const int C = (int)cluster.num_blocks();
@@ -273,6 +283,9 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
   const int tid = threadIdx.x, nt = blockDim.x;
+  // the V replay (launched programmatically dependent on this kernel) may
+  // start now: this grid is resident, so its spinning cannot block us
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // ||G||_F^2 is invariant under the rotations: fix the null floor once.
   {
@@ -310,7 +323,6 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
       R* col = dst + slot * slotsz + (size_t)j * colsz;
       const bool ok = gc < l && i < l;
       col[i] = ok ? a.G[(int64_t)gc * a.ldg + i] : R(0);
-      col[lp + i] = ok ? a.V[(int64_t)gc * a.ldv + i] : R(0);
     }
   }
   cluster.sync();
@@ -326,6 +338,7 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
     const int ba = tourn_pos(me, tr, nb), bb = tourn_pos(nb - 1 - me, tr, nb);
     // valid column counts of the two blocks (ragged last block)
     const int va = max(0, min(bw, l - ba * bw)), vb = max(0, min(bw, l - bb * bw));
+    JcRot<R>* lg = a.log + jc_step(r, bw, nb) * (C * bw) + me * bw;
     __syncthreads();
     if (tr == 0) {
       // all pairs of the 2bw columns: inner circle tournament over W = 2bw
@@ -336,10 +349,15 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
           const int ja = ca % bw, jb = cb % bw;
           const bool oka = ca < bw ? ja < va : ja < vb;
           const bool okb = cb < bw ? jb < va : jb < vb;
-          if (!oka || !okb) continue;
-          R* x = cur + (size_t)(ca / bw) * slotsz + (size_t)ja * colsz;
-          R* y = cur + (size_t)(cb / bw) * slotsz + (size_t)jb * colsz;
-          if (jc_rotate<R, NP2>(x, y, x + lp, y + lp, lp, tol2, floor2, lane, my_c2)) ++my_rot;
+          JcRot<R> e;
+          e.x = R(1);
+          e.y = R(0);
+          if (oka && okb) {
+            R* x = cur + (size_t)(ca / bw) * slotsz + (size_t)ja * colsz;
+            R* y = cur + (size_t)(cb / bw) * slotsz + (size_t)jb * colsz;
+            if (jc_rotate<R, NP2>(x, y, lp, tol2, floor2, lane, my_c2, e.x, e.y)) ++my_rot;
+          }
+          if (lane == 0) lg[(int64_t)st * (C * bw) + p] = e;
         }
         __syncthreads();
       }
@@ -350,7 +368,7 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
       using V2 = typename Vec2<R>::type;
       const int p = warp;
       const bool own = p < bw && p < va;
-      V2 xr[NP2], xv[NP2];
+      V2 xr[NP2];
       R* xcol = cur + (size_t)p * colsz;
       if (own) {
 #pragma unroll
@@ -358,31 +376,28 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
           const int i = 2 * lane + 64 * k;
           if (i < lp) {
             xr[k] = *reinterpret_cast<const V2*>(xcol + i);
-            xv[k] = *reinterpret_cast<const V2*>(xcol + lp + i);
           } else {
-            xr[k].x = xr[k].y = xv[k].x = xv[k].y = R(0);
+            xr[k].x = xr[k].y = R(0);
           }
         }
       }
       for (int st = 0; st < bw; ++st) {
-        if (own) {
-          const int jb = p + st < bw ? p + st : p + st - bw;
-          if (jb < vb) {
-            R* y = cur + slotsz + (size_t)jb * colsz;
-            if (jc_rotate_x<R, NP2>(xr, xv, y, y + lp, lp, tol2, floor2, lane, my_c2))
-              ++my_rot;
-          }
+        const int jb = p + st < bw ? p + st : p + st - bw;
+        JcRot<R> e;
+        e.x = R(1);
+        e.y = R(0);
+        if (own && jb < vb) {
+          R* y = cur + slotsz + (size_t)jb * colsz;
+          if (jc_rotate_x<R, NP2>(xr, y, lp, tol2, floor2, lane, my_c2, e.x, e.y)) ++my_rot;
         }
+        if (p < bw && lane == 0) lg[(int64_t)st * (C * bw) + p] = e;
         __syncthreads();
       }
       if (own) {
 #pragma unroll
         for (int k = 0; k < NP2; ++k) {
           const int i = 2 * lane + 64 * k;
-          if (i < lp) {
-            *reinterpret_cast<V2*>(xcol + i) = xr[k];
-            *reinterpret_cast<V2*>(xcol + lp + i) = xv[k];
-          }
+          if (i < lp) *reinterpret_cast<V2*>(xcol + i) = xr[k];
         }
       }
     }
@@ -403,6 +418,12 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
     cluster.sync();
     t0 = clock64();
     t_sync += t0 - t1;
+    // rounds 0..r are logged by every CTA (ordered by the cluster barrier):
+    // publish them to the replay
+    if (me == 0 && tid == 0) {
+      __threadfence();
+      jc_st_release(a.prog, (int)jc_step(r + 1, bw, nb));
+    }
     if (sweep_end) {
       if (tid == 0) {
         int tot = 0;
@@ -475,12 +496,140 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
       if (gc >= l) continue;
       const R* col = cur + slot * slotsz + (size_t)j * colsz;
       a.G[(int64_t)gc * a.ldg + i] = col[i];
-      a.V[(int64_t)gc * a.ldv + i] = col[lp + i];
     }
   }
   if (me == 0 && tid == 0 && a.sweeps_done) *a.sweeps_done = sweep + 1;
   // keep the cluster alive until every peer finished reading our counters
   cluster.sync();
+  if (me == 0 && tid == 0) {   // G written back by every CTA: final
+    __threadfence();
+    jc_st_release(a.prog + 1, 1);
+  }
+}
+
+// V <- V * (the logged rotations, in order).  The rows of V are independent
+// under column rotations and, within a tournament round, so are the block
+// pairs: warp j of a CTA replays block pair (slot) j of every round on the
+// rows of V held in shared memory, lane = (row, pair index p), one __syncwarp
+// per step and one block barrier per round.  rows_per_warp = 32 / bw rows of
+// V per CTA.  The replay is launched programmatically dependent on the
+// tournament and runs concurrently with it on the idle SMs: it consumes the
+// log in chunks of kJrK steps as the tournament publishes whole rounds
+// (prog[0], release / acquire), so only the last round's replay is left when
+// the tournament ends.  The columns of an entry follow from the schedule;
+// same arithmetic per element as an in-place update of V in the tournament.
+constexpr int kJrK = 16;
+__host__ __device__ inline size_t jacobi_vreplay_smem(int l, int bw, int C, size_t rsz) {
+  const int rpw = 32 / bw, LP = (2 * C * bw) | 1;
+  return (size_t)rpw * LP * rsz + 16 + (size_t)(2 * bw - 1) * bw * 4 +
+         (size_t)kJrK * C * bw * 2 * rsz + 16;
+}
+template <typename R>
+__global__ void __launch_bounds__(512) jacobi_vreplay_kernel(R* __restrict__ V, int64_t ldv,
+                                                             int l, int bw, int C,
+                                                             const JcRot<R>* __restrict__ log,
+                                                             const int* __restrict__ prog) {
+  extern __shared__ __align__(16) unsigned char jr_raw[];
+  // LP odd: the rows of a warp's lanes sit in different banks
+  const int nb = 2 * C, S = 2 * bw - 1, P = C * bw, LP = (nb * bw) | 1;
+  const int rpw = 32 / bw;                       // rows of V per CTA
+  JcRot<R>* ebuf = reinterpret_cast<JcRot<R>*>(jr_raw);            // [warp][kJrK][bw]
+  R* rows = reinterpret_cast<R*>(ebuf + (size_t)kJrK * P);         // rpw x LP
+  short2* tab = reinterpret_cast<short2*>(
+      (reinterpret_cast<uintptr_t>(rows + (size_t)rpw * LP) + 15) & ~uintptr_t(15));  // S x bw
+  const int i0 = blockIdx.x * rpw;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, j = tid >> 5;
+  for (int e = tid; e < rpw * LP; e += nt) {
+    const int rr = e / LP, col = e % LP;
+    rows[e] = (col < l && i0 + rr < l) ? V[(int64_t)col * ldv + i0 + rr] : R(0);
+  }
+  for (int e = tid; e < S * bw; e += nt) {
+    const int st = e / bw, p = e % bw, W = 2 * bw;
+    tab[e] = make_short2((short)tourn_pos(p, st, W), (short)tourn_pos(W - 1 - p, st, W));
+  }
+  const int rr = lane / bw, p = lane % bw;
+  const bool act = rr < rpw && i0 + rr < l;
+  const bool loader = lane < bw;                 // lane p fetches slot (j, p)
+  R* row = rows + (size_t)(rr < rpw ? rr : 0) * LP;
+  JcRot<R>* ew = ebuf + (size_t)j * kJrK * bw;   // this warp's chunk
+  __syncthreads();
+  // per-round state: round 0 is a full round (schedule table), the others
+  // are cross rounds (block a column p fixed, block b column jb advancing)
+  int r = 0, st = 0, steps = S, ti = p, jb = p;
+  bool full = true;
+  int ba = tourn_pos(j, 0, nb), bb = tourn_pos(nb - 1 - j, 0, nb);
+  int gxa = ba * bw + p, gyb = bb * bw;
+  for (int c = 0;; ++c) {
+    // wait until the chunk is published (or the tournament is over)
+    int avail = 0, dn = 0;
+    for (long long spin = 0;; ++spin) {
+      if (spin > (1ll << 26)) __trap();           // ~20 s: never hang the device
+      if (lane == 0) {
+        dn = jc_ld_acquire(prog + 1);
+        avail = jc_ld_acquire(prog);   // final once dn was seen
+      }
+      dn = __shfl_sync(0xffffffffu, dn, 0);
+      avail = __shfl_sync(0xffffffffu, avail, 0);
+      if (dn || avail >= (c + 1) * kJrK) break;
+      __nanosleep(256);
+    }
+    const int n = min(kJrK, avail - c * kJrK);
+    if (n <= 0) break;                            // dn: every step replayed
+    if (loader) {
+      JcRot<R> v[kJrK];
+      const JcRot<R>* src = log + (int64_t)c * kJrK * P + (size_t)j * bw + lane;
+#pragma unroll
+      for (int k = 0; k < kJrK; ++k) {
+        v[k].x = R(1);
+        v[k].y = R(0);
+        if (k < n) v[k] = __ldcg(src + (int64_t)k * P);
+      }
+#pragma unroll
+      for (int k = 0; k < kJrK; ++k) ew[k * bw + lane] = v[k];
+    }
+    __syncwarp();
+    for (int k = 0; k < n; ++k) {
+      const JcRot<R> e = ew[k * bw + p];
+      int gx, gy;
+      if (full) {
+        const short2 cc = tab[ti];
+        ti += bw;
+        gx = cc.x < bw ? ba * bw + cc.x : bb * bw + cc.x - bw;
+        gy = cc.y < bw ? ba * bw + cc.y : bb * bw + cc.y - bw;
+      } else {
+        gx = gxa;
+        gy = gyb + jb;
+        jb = (jb + 1 == bw) ? 0 : jb + 1;
+      }
+      if (act) {
+        const R x = row[gx], y = row[gy];
+        row[gx] = e.x * x - e.y * y;
+        row[gy] = e.y * x + e.x * y;
+      }
+      __syncwarp();
+      if (++st == steps) {   // end of round (uniform over the CTA)
+        ++r;
+        const int tr = r % (nb - 1);
+        ba = tourn_pos(j, tr, nb);
+        bb = tourn_pos(nb - 1 - j, tr, nb);
+        full = tr == 0;
+        steps = full ? S : bw;
+        st = 0;
+        ti = p;
+        jb = p;
+        gxa = ba * bw + p;
+        gyb = bb * bw;
+        __syncthreads();
+      }
+    }
+    __syncwarp();                                 // the chunk buffer is reused
+    if (n < kJrK) break;                          // that was the final chunk
+  }
+  __syncthreads();
+  for (int e = tid; e < rpw * LP; e += nt) {
+    const int q = e / LP, col = e % LP;
+    if (col < l && i0 + q < l) V[(int64_t)col * ldv + i0 + q] = rows[e];
+  }
 }
 
 }  // namespace brsvd

@@ -336,11 +336,17 @@ bool jacobi_cluster(Ctx& c, R* G, int l, int64_t ldg, R* V, int64_t ldv, double 
     const int bw = (int)ceil_div(l, 2 * csize);
     const size_t smem = jacobi_cluster_smem<R>(l, bw);
     if (smem > lim) continue;
+    const int P = csize * bw;   // logged rotations per step
+    const int64_t steps = (int64_t)max_sweeps * jc_sweep_steps(bw, 2 * csize);
+    DBuf<JcRot<R>> log(c, (size_t)steps * P);
+    DBuf<int> prog(c, 2);
+    BRSVD_CUDA(cudaMemsetAsync(prog.p, 0, 2 * sizeof(int), c.stream));
     JacobiClusterArgs<R> a;
     a.G = G;
     a.ldg = ldg;
-    a.V = V;
-    a.ldv = ldv;
+    a.log = log.p;
+    a.log_steps = steps;
+    a.prog = prog.p;
     a.l = l;
     a.bw = bw;
     a.max_sweeps = max_sweeps;
@@ -357,7 +363,30 @@ bool jacobi_cluster(Ctx& c, R* G, int l, int64_t ldg, R* V, int64_t ldv, double 
     else if (np2 <= 5) ok = jacobi_cluster_launch<R, 5>(c, a, csize, smem, threads);
     else if (np2 <= 6) ok = jacobi_cluster_launch<R, 6>(c, a, csize, smem, threads);
     else ok = jacobi_cluster_launch<R, 8>(c, a, csize, smem, threads);
-    if (ok) return true;
+    if (ok) {
+      // V <- V * the logged rotations, one CTA per row
+      // V <- V * the logged rotations: launched programmatically dependent
+      // on the tournament, so it streams the log while the tournament runs
+      const int rpw = 32 / bw;
+      const size_t rs = jacobi_vreplay_smem(l, bw, csize, sizeof(R));
+      auto rk = jacobi_vreplay_kernel<R>;
+      BRSVD_CUDA(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs));
+      cudaLaunchConfig_t rc = {};
+      rc.gridDim = dim3((unsigned)ceil_div(l, rpw));
+      rc.blockDim = dim3(32 * csize);
+      rc.dynamicSmemBytes = rs;
+      rc.stream = c.stream;
+      cudaLaunchAttribute ra[1];
+      ra[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      ra[0].val.programmaticStreamSerializationAllowed = 1;
+      rc.attrs = ra;
+      rc.numAttrs = 1;
+      const JcRot<R>* lp = log.p;
+      const int* pp = prog.p;
+      BRSVD_CUDA(cudaLaunchKernelEx(&rc, rk, V, ldv, l, bw, csize, lp, pp));
+      BRSVD_CHECK_LAUNCH();
+      return true;
+    }
   }
   return false;
 }
