@@ -368,7 +368,10 @@ bool jacobi_cluster(Ctx& c, R* G, int l, int64_t ldg, R* V, int64_t ldv, double 
       // V <- V * the logged rotations: launched programmatically dependent
       // on the tournament, so it streams the log while the tournament runs
       const int rpw = 32 / bw;
-      const size_t rs = jacobi_vreplay_smem(l, bw, csize, sizeof(R));
+      // shared memory sized so a replay CTA never shares an SM with a
+      // tournament CTA (the latency-bound tournament would lose issue slots)
+      const size_t rs = std::max(jacobi_vreplay_smem(l, bw, csize, sizeof(R)),
+                                 std::min(lim, (size_t)c.max_smem_optin + 1024 - smem));
       auto rk = jacobi_vreplay_kernel<R>;
       BRSVD_CUDA(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs));
       cudaLaunchConfig_t rc = {};
