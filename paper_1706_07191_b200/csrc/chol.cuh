@@ -55,11 +55,14 @@ __device__ long long g_ci_t[64];
 #define CI_T(k) do { if (me == 0 && tid == 0) g_ci_t[(k)] = clock64(); } while (0)
 
 __host__ __device__ inline int cholinv_ldp(int n) { return (n + 3) & ~3; }
+// offset of the k-major L21 copy PT after the n x 33 panel: even, so that its
+// 16-byte (double2) reads stay aligned for odd n
+__host__ __device__ inline size_t cholinv_pt_off(int n) { return ((size_t)n * kCiLd + 1) & ~size_t(1); }
 // Columns of each block column of X = L^-1 owned by one CTA in phase 2 (the
 // launch uses an 8-CTA cluster for n > 96, one CTA otherwise).
 __host__ __device__ inline int cholinv_cpc(int n) { return n > 96 ? kCiNB / 8 : kCiNB; }
 __host__ __device__ inline size_t cholinv_big(int n) {
-  const size_t p1 = (size_t)n * kCiLd + (size_t)kCiNB * cholinv_ldp(n);  // phase 1 panels
+  const size_t p1 = cholinv_pt_off(n) + (size_t)kCiNB * cholinv_ldp(n);  // phase 1 panels
   const size_t nblk = (size_t)(n + kCiNB - 1) / kCiNB;
   const size_t ldxm = nblk * cholinv_cpc(n);
   const size_t xm = nblk * kCiNB * ldxm;
@@ -86,7 +89,7 @@ __global__ void __launch_bounds__(kCiThreads, 1)
   const size_t big = cholinv_big(n);
   const int ldp = cholinv_ldp(n);
   double* Lp = cism;                      // phase 1: panel, row-major rows x 33
-  double* PT = cism + (size_t)n * kCiLd;  // phase 1: L21 k-major, 32 x ldp
+  double* PT = cism + cholinv_pt_off(n);  // phase 1: L21 k-major, 32 x ldp
   double* Di = cism + big;                // 32 x 33: inverse of the diagonal block
   double* sc = Di + kCiNB * kCiLd;        // column scaling
   double* d0 = sc + n;                    // scaled diagonal + shift
