@@ -15,15 +15,24 @@ namespace brsvd {
 
 constexpr int kCholNB = 32;
 
-// Tc[:, c] = T[:, keep[c]] for the kept columns (count from info[2]).
+// Tc[:, c] = T[:, keep[c]] for the kept columns (count from info[2]); with
+// zero_rest the columns k .. l-1 of Tc are zeroed (device-driven callers that
+// apply all l columns without reading k on the host).
 __global__ void compact_cols_kernel(const double* __restrict__ T, int l,
                                     const int* __restrict__ keep,
-                                    const double* __restrict__ info, double* __restrict__ Tc) {
+                                    const double* __restrict__ info, double* __restrict__ Tc,
+                                    int zero_rest = 0) {
   const int k = (int)info[2];
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < l * k; e += gridDim.x * blockDim.x) {
+  const int nc = zero_rest ? l : k;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < l * nc; e += gridDim.x * blockDim.x) {
     const int i = e % l, c = e / l;
-    Tc[(int64_t)c * l + i] = T[(int64_t)keep[c] * l + i];
+    Tc[(int64_t)c * l + i] = c < k ? T[(int64_t)keep[c] * l + i] : 0.0;
   }
+}
+
+// rank = min(reference rank cut, kept count) of a Cholesky pass, on the device
+__global__ void chol_rank_kernel(const double* __restrict__ info, int* __restrict__ rank) {
+  rank[0] = min((int)info[1], (int)info[2]);
 }
 
 // ---------------------------------------------------------------------------

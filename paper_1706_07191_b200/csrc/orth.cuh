@@ -348,14 +348,34 @@ int orth_full_f64(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, double* Q,
 // returns l orthonormal columns whose first k1 span the kept part of range(X)
 // (kernels.py:142-144, "columns of Q remain orthonormal").  Q is fp32; the
 // Grams and factors are fp64, the basis changes tcgen05 products.
+// rank_dev: the rank is written to the device (read by the caller's final
+// synchronisation) and -1 returned -- no host read in the middle of the
+// pipeline: the kept columns are applied as l columns with the dropped ones
+// zeroed and the Gaussian completion starts at the device-side kept count.
 inline int orth_full_f32(Ctx& c, const float* X, int64_t r, int l, int64_t ldx, float* Q,
-                         uint64_t seed) {
+                         uint64_t seed, int* rank_dev = nullptr) {
   const double eps_data = 1.1920928955078125e-07;
   const double drop = 4.0 * l * eps_data;  // the reference's rank cut, kernels.py:155-157
   DBuf<int> keep(c, l);
   DBuf<double> info(c, 3), Tm(c, (size_t)l * l), Tc(c, (size_t)l * l);
-  const CholInfo ci = chol_basis<float>(c, X, r, l, ldx, 0.0, Tm.p, true, drop, l * eps_data,
-                                        1e-12, keep.p, info.p);
+  const CholInfo ci = chol_basis<float>(c, X, r, l, ldx, 0.0, Tm.p, rank_dev == nullptr, drop,
+                                        l * eps_data, 1e-12, keep.p, info.p);
+  if (rank_dev) {
+    DBuf<float> Q1(c, (size_t)r * l);
+    compact_cols_kernel<<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(Tm.p, l, keep.p,
+                                                                        info.p, Tc.p, 1);
+    BRSVD_CHECK_LAUNCH();
+    apply_basis<float>(c, X, r, l, ldx, Tc.p, l, l, Q1.p, r);
+    gaussian_tail_kernel<float><<<grid_for(r * ((l + 1) / 2)), 256, 0, c.stream>>>(
+        Q1.p, r, l, r, info.p, seed, 0x636f6d706c657465ull);
+    BRSVD_CHECK_LAUNCH();
+    chol_basis<float>(c, Q1.p, r, l, r, 0.0, Tm.p, false, 0.0, 0.0, 0.0, nullptr, nullptr,
+                      /*tc_gram_ok=*/true);
+    apply_basis<float>(c, Q1.p, r, l, r, Tm.p, l, l, Q, r);
+    chol_rank_kernel<<<1, 1, 0, c.stream>>>(info.p, rank_dev);
+    BRSVD_CHECK_LAUNCH();
+    return -1;
+  }
   const int k1 = ci.kept;
   DBuf<float> Q1(c, (size_t)r * l);
   if (k1 > 0) {
@@ -383,7 +403,7 @@ inline int orth_full_f32(Ctx& c, const float* X, int64_t r, int l, int64_t ldx, 
 
 template <typename T>
 int orth_full(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, T* Q, uint64_t seed,
-              int ns_iters, bool scale_check = true) {
+              int ns_iters, bool scale_check = true, int* rank_dev = nullptr) {
   if (sizeof(T) == 8) {
     const int e = scale_check ? unit_exponent<T>(c, X, r, l, ldx) : 0;
     if (e != 0) {
@@ -398,7 +418,7 @@ int orth_full(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, T* Q, uint64_t 
   }
   if (l <= kCholMaxL)
     return orth_full_f32(c, reinterpret_cast<const float*>(X), r, l, ldx,
-                         reinterpret_cast<float*>(Q), seed);
+                         reinterpret_cast<float*>(Q), seed, rank_dev);
   DBuf<double> Qw(c, (size_t)r * l);
   const int rank = orth_full_f64<T>(c, X, r, l, ldx, Qw.p, seed, ns_iters);
   copy2d_kernel<double, T><<<grid_for(r * l), 256, 0, c.stream>>>(Qw.p, r, l, r, Q, r);
@@ -412,7 +432,8 @@ int orth_full(Ctx& c, const T* X, int64_t r, int l, int64_t ldx, T* Q, uint64_t 
 // Outputs: W (l x l fp64, ld l), sigma (fp64), Vout (n x l, T, ld ldv).
 template <typename T>
 int small_svd_device(Ctx& c, const T* Bt, int64_t n, int l, int64_t ldb, double* W,
-                     double* sigma, T* Vout, int64_t ldv, int ns_iters) {
+                     double* sigma, T* Vout, int64_t ldv, int ns_iters,
+                     int* rank_dev = nullptr) {
   // fp64 B near the range limits: factor 2^-e B, scale sigma back at the end
   const int e = unit_exponent<T>(c, Bt, n, l, ldb);
   DBuf<T> Bs;
@@ -426,7 +447,8 @@ int small_svd_device(Ctx& c, const T* Bt, int64_t n, int l, int64_t ldb, double*
   }
   DBuf<T> Qb(c, (size_t)n * l);
   DBuf<double> M(c, (size_t)l * l), Vj(c, (size_t)l * l), Zj(c, (size_t)l * l);
-  const int rank = orth_full<T>(c, Bt, n, l, ldb, Qb.p, 0x5eedb5ull, ns_iters, false);
+  // rank_dev: rank deferred to the caller's final read (-1 returned)
+  const int rank = orth_full<T>(c, Bt, n, l, ldb, Qb.p, 0x5eedb5ull, ns_iters, false, rank_dev);
   // M = Bt^T Qb = R^T
   gemm_tn_cm<T, T, double>(c, l, l, n, Bt, ldb, Qb.p, n, M.p, l);
   if (l > 64) {

@@ -399,7 +399,11 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
   const int ns = sizeof(T) == 8 ? 2 : 1;
   DBuf<T> Qw(c, (size_t)m * l);
   const bool y_extreme = ypeak > 0x1p400 || (ypeak > 0.0 && ypeak < 0x1p-400);
-  info.rank_y = orth_full<T>(c, Y.p, m, l, m, Qw.p, seed ^ 0x7153ull, ns, y_extreme);
+  // ranks of the fp32 path are read at the final synchronisation (no host
+  // read in the middle of the pipeline); -1 until then
+  DBuf<int> ranks(c, 2);
+  info.rank_y = orth_full<T>(c, Y.p, m, l, m, Qw.p, seed ^ 0x7153ull, ns, y_extreme,
+                             range_only ? nullptr : ranks.p);
   const double lim = 0.01 * finfo_max<T>();
   if (range_only) {
     BRSVD_CUDA(cudaMemcpyAsync(U, Qw.p, sizeof(T) * m * l, cudaMemcpyDeviceToDevice,
@@ -421,7 +425,7 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
   info.block_reads += 1;
   ev.rec(3, c.stream);
   DBuf<double> W(c, (size_t)l * l), sig(c, l);
-  info.rank_b = small_svd_device<T>(c, Bt.p, n, l, n, W.p, sig.p, V, n, ns);
+  info.rank_b = small_svd_device<T>(c, Bt.p, n, l, n, W.p, sig.p, V, n, ns, ranks.p + 1);
   apply_basis<T>(c, Qw.p, m, l, m, W.p, l, l, U, m);
   fix_signs<T>(c, U, m, l, m, V, n, n);
   copy2d_kernel<double, T><<<1, 256, 0, c.stream>>>(sig.p, l, 1, l, sigma, l);
@@ -430,8 +434,16 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
   double s0 = 0.0;
   BRSVD_CUDA(cudaMemcpyAsync(c.h_pinned, sig.p, sizeof(double),
                              cudaMemcpyDeviceToHost, c.stream));
+  BRSVD_CUDA(cudaMemcpyAsync(c.h_pinned + 1, ranks.p, 2 * sizeof(int), cudaMemcpyDeviceToHost,
+                             c.stream));
   BRSVD_CUDA(cudaStreamSynchronize(c.stream));
   std::memcpy(&s0, c.h_pinned, sizeof(double));
+  {
+    int rk[2];
+    std::memcpy(rk, c.h_pinned + 1, sizeof(rk));
+    if (info.rank_y < 0) info.rank_y = rk[0];
+    if (info.rank_b < 0) info.rank_b = rk[1];
+  }
   info.ms_sketch = ev.ms(0, 1);
   info.ms_orth = ev.ms(1, 2);
   info.ms_core = ev.ms(2, 3);

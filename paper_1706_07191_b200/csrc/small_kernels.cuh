@@ -350,32 +350,61 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
   return c;
 }
 
+// Two normals of the sketch stream for (global row, column pair pj): Philox
+// counter (pj, row, stream), Box-Muller on two 53-bit uniforms.
+__device__ __forceinline__ void gaussian_pair(uint64_t seed, uint64_t stream, uint64_t grow,
+                                              int64_t pj, double& v0, double& v1) {
+  const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  const uint4 ctr = make_uint4((uint32_t)pj, (uint32_t)grow, (uint32_t)(grow >> 32),
+                               (uint32_t)stream ^ ((uint32_t)(stream >> 32) * 0x85EBCA6Bu));
+  const uint4 x = philox4x32_10(ctr, key);
+  // two 53-bit uniforms in (0, 1]
+  const uint64_t a = ((uint64_t)x.x << 32) | x.y;
+  const uint64_t b = ((uint64_t)x.z << 32) | x.w;
+  const double u1 = ((a >> 11) + 1) * (1.0 / 9007199254740992.0);
+  const double u2 = (b >> 11) * (1.0 / 9007199254740992.0);
+  const double rad = sqrt(-2.0 * log(u1));
+  double sn, cs;
+  sincospi(2.0 * u2, &sn, &cs);
+  v0 = rad * cs;
+  v1 = rad * sn;
+}
+
 template <typename T>
 __global__ void gaussian_kernel(T* __restrict__ out, int64_t rows, int64_t cols,
                                 int64_t ld, uint64_t seed, uint64_t stream,
                                 int64_t row_offset) {
   const int64_t half = (cols + 1) / 2;
   const int64_t total = rows * half;
-  const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
        idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = idx % rows, pj = idx / rows;
-    const uint64_t grow = (uint64_t)(row_offset + r);
-    const uint4 ctr = make_uint4((uint32_t)pj, (uint32_t)grow,
-                                 (uint32_t)(grow >> 32),
-                                 (uint32_t)stream ^ ((uint32_t)(stream >> 32) * 0x85EBCA6Bu));
-    const uint4 x = philox4x32_10(ctr, key);
-    // two 53-bit uniforms in (0, 1]
-    const uint64_t a = ((uint64_t)x.x << 32) | x.y;
-    const uint64_t b = ((uint64_t)x.z << 32) | x.w;
-    const double u1 = ((a >> 11) + 1) * (1.0 / 9007199254740992.0);
-    const double u2 = (b >> 11) * (1.0 / 9007199254740992.0);
-    const double rad = sqrt(-2.0 * log(u1));
-    double sn, cs;
-    sincospi(2.0 * u2, &sn, &cs);
+    double v0, v1;
+    gaussian_pair(seed, stream, (uint64_t)(row_offset + r), pj, v0, v1);
     const int64_t c0 = 2 * pj;
-    out[r + c0 * ld] = (T)(rad * cs);
-    if (c0 + 1 < cols) out[r + (c0 + 1) * ld] = (T)(rad * sn);
+    out[r + c0 * ld] = (T)v0;
+    if (c0 + 1 < cols) out[r + (c0 + 1) * ld] = (T)v1;
+  }
+}
+
+// The same stream as gaussian_kernel(out + k0 * ld, rows, l - k0, ...) with
+// k0 = (int)info[2] read on the device (the kept count of a rank-revealing
+// Cholesky pass): the completion columns k0 .. l-1, without a host read.
+template <typename T>
+__global__ void gaussian_tail_kernel(T* __restrict__ out, int64_t rows, int l, int64_t ld,
+                                     const double* __restrict__ info, uint64_t seed,
+                                     uint64_t stream) {
+  const int k0 = (int)info[2];
+  const int64_t cols = l - k0;
+  const int64_t total = rows * ((cols + 1) / 2);
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+       idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx % rows, pj = idx / rows;
+    double v0, v1;
+    gaussian_pair(seed, stream, (uint64_t)r, pj, v0, v1);
+    const int64_t c0 = k0 + 2 * pj;
+    out[r + c0 * ld] = (T)v0;
+    if (2 * pj + 1 < cols) out[r + (c0 + 1) * ld] = (T)v1;
   }
 }
 
