@@ -381,7 +381,16 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
   info.words_read += (int64_t)(2 * q + 1) * m * n;
   info.block_reads += 2 * q + 1;
   double ypeak = p0.peak;   // max |Y| of the sample being orthonormalised
-  if (q > 0) {
+  // fp32 (the peak only steers fp64 scaling): the non-finite check of the
+  // powered sample is read at the final synchronisation instead of here
+  DBuf<unsigned long long> yq_chk;
+  const bool yq_defer = sizeof(T) == 4 && q > 0 && !range_only && !std::getenv("BRSVD_DEBUG");
+  if (yq_defer) {
+    yq_chk.alloc(c, 2);
+    BRSVD_CUDA(cudaMemsetAsync(yq_chk.p, 0, 2 * sizeof(unsigned long long), c.stream));
+    maxabs_kernel<T><<<grid_for(m * l), 256, 0, c.stream>>>(Y.p, m, l, m, yq_chk.p);
+    BRSVD_CHECK_LAUNCH();
+  } else if (q > 0) {
     const MaxAbs pq = maxabs<T>(c, Y.p, m, l, m);
     ypeak = pq.peak;
     if (std::getenv("BRSVD_DEBUG"))
@@ -436,6 +445,10 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
                              cudaMemcpyDeviceToHost, c.stream));
   BRSVD_CUDA(cudaMemcpyAsync(c.h_pinned + 1, ranks.p, 2 * sizeof(int), cudaMemcpyDeviceToHost,
                              c.stream));
+  c.h_pinned[2] = 0;
+  if (yq_defer)
+    BRSVD_CUDA(cudaMemcpyAsync(c.h_pinned + 2, yq_chk.p + 1, sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, c.stream));
   BRSVD_CUDA(cudaStreamSynchronize(c.stream));
   std::memcpy(&s0, c.h_pinned, sizeof(double));
   {
@@ -443,6 +456,11 @@ RsvdInfo rsvd_device(Ctx& c, const T* A, int64_t m, int64_t n, int64_t lda,
     std::memcpy(rk, c.h_pinned + 1, sizeof(rk));
     if (info.rank_y < 0) info.rank_y = rk[0];
     if (info.rank_b < 0) info.rank_b = rk[1];
+  }
+  if (c.h_pinned[2] != 0) {   // the powered sample was non-finite (deferred check)
+    info.overflow = true;
+    info.log10_peak = INFINITY;
+    return info;
   }
   info.ms_sketch = ev.ms(0, 1);
   info.ms_orth = ev.ms(1, 2);
