@@ -381,7 +381,8 @@ bool jacobi_cluster(Ctx& c, R* G, int l, int64_t ldg, R* V, int64_t ldv, double 
       rc.stream = c.stream;
       cudaLaunchAttribute ra[1];
       ra[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      ra[0].val.programmaticStreamSerializationAllowed = 1;
+      // BRSVD_NO_PDL=1: plain stream order (the replay after the tournament)
+      ra[0].val.programmaticStreamSerializationAllowed = std::getenv("BRSVD_NO_PDL") ? 0 : 1;
       rc.attrs = ra;
       rc.numAttrs = 1;
       const JcRot<R>* lp = log.p;
