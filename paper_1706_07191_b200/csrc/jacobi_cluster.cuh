@@ -46,8 +46,8 @@ template <typename R>
 struct JacobiClusterArgs {
   R* G;          // l x l, column-major, ld ldg  (overwritten by G V)
   int64_t ldg;
-  JcRot<R>* log;     // rotation log: step t, slot (CTA, warp) at t * C * bw + slot
-  int64_t log_steps; // capacity in steps
+  JcRot<R>* log;     // rotation log: step t, slot (CTA, warp) at t * C * bw + slot;
+                     // max_sweeps * jc_sweep_steps steps (the sweep cap bounds it)
   int* prog;         // [0] steps logged so far, [1] 1 when final (read by the replay)
   int l;         // matrix order
   int bw;        // block width

@@ -345,7 +345,6 @@ bool jacobi_cluster(Ctx& c, R* G, int l, int64_t ldg, R* V, int64_t ldv, double 
     a.G = G;
     a.ldg = ldg;
     a.log = log.p;
-    a.log_steps = steps;
     a.prog = prog.p;
     a.l = l;
     a.bw = bw;
