@@ -519,13 +519,18 @@ __global__ void jacobi_cluster_kernel(JacobiClusterArgs<R> a) {
 // the tournament ends.  The columns of an entry follow from the schedule;
 // same arithmetic per element as an in-place update of V in the tournament.
 constexpr int kJrK = 16;
-__host__ __device__ inline size_t jacobi_vreplay_smem(int l, int bw, int C, size_t rsz) {
+// vsz: bytes of a V element, rsz: of a logged rotation component.
+__host__ __device__ inline size_t jacobi_vreplay_smem(int l, int bw, int C, size_t vsz,
+                                                      size_t rsz) {
   const int rpw = 32 / bw, LP = (2 * C * bw) | 1;
-  return (size_t)rpw * LP * rsz + 16 + (size_t)(2 * bw - 1) * bw * 4 +
+  return (size_t)rpw * LP * vsz + 16 + (size_t)(2 * bw - 1) * bw * 4 +
          (size_t)kJrK * C * bw * 2 * rsz + 16;
 }
-template <typename R>
-__global__ void __launch_bounds__(512) jacobi_vreplay_kernel(R* __restrict__ V, int64_t ldv,
+// RV: the element type of V.  A wider V than the log (fp64 V of the fp32
+// tournament) takes each rotation renormalised in RV, so V stays orthogonal
+// to RV's rounding however many fp32 rotations it absorbs.
+template <typename R, typename RV>
+__global__ void __launch_bounds__(512) jacobi_vreplay_kernel(RV* __restrict__ V, int64_t ldv,
                                                              int l, int bw, int C,
                                                              const JcRot<R>* __restrict__ log,
                                                              const int* __restrict__ prog) {
@@ -534,14 +539,14 @@ __global__ void __launch_bounds__(512) jacobi_vreplay_kernel(R* __restrict__ V, 
   const int nb = 2 * C, S = 2 * bw - 1, P = C * bw, LP = (nb * bw) | 1;
   const int rpw = 32 / bw;                       // rows of V per CTA
   JcRot<R>* ebuf = reinterpret_cast<JcRot<R>*>(jr_raw);            // [warp][kJrK][bw]
-  R* rows = reinterpret_cast<R*>(ebuf + (size_t)kJrK * P);         // rpw x LP
+  RV* rows = reinterpret_cast<RV*>(ebuf + (size_t)kJrK * P);       // rpw x LP
   short2* tab = reinterpret_cast<short2*>(
       (reinterpret_cast<uintptr_t>(rows + (size_t)rpw * LP) + 15) & ~uintptr_t(15));  // S x bw
   const int i0 = blockIdx.x * rpw;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, j = tid >> 5;
   for (int e = tid; e < rpw * LP; e += nt) {
     const int rr = e / LP, col = e % LP;
-    rows[e] = (col < l && i0 + rr < l) ? V[(int64_t)col * ldv + i0 + rr] : R(0);
+    rows[e] = (col < l && i0 + rr < l) ? V[(int64_t)col * ldv + i0 + rr] : RV(0);
   }
   for (int e = tid; e < S * bw; e += nt) {
     const int st = e / bw, p = e % bw, W = 2 * bw;
@@ -550,7 +555,7 @@ __global__ void __launch_bounds__(512) jacobi_vreplay_kernel(R* __restrict__ V, 
   const int rr = lane / bw, p = lane % bw;
   const bool act = rr < rpw && i0 + rr < l;
   const bool loader = lane < bw;                 // lane p fetches slot (j, p)
-  R* row = rows + (size_t)(rr < rpw ? rr : 0) * LP;
+  RV* row = rows + (size_t)(rr < rpw ? rr : 0) * LP;
   JcRot<R>* ew = ebuf + (size_t)j * kJrK * bw;   // this warp's chunk
   __syncthreads();
   // per-round state: round 0 is a full round (schedule table), the others
@@ -602,9 +607,15 @@ __global__ void __launch_bounds__(512) jacobi_vreplay_kernel(R* __restrict__ V, 
         jb = (jb + 1 == bw) ? 0 : jb + 1;
       }
       if (act) {
-        const R x = row[gx], y = row[gy];
-        row[gx] = e.x * x - e.y * y;
-        row[gy] = e.y * x + e.x * y;
+        RV cr = (RV)e.x, sr = (RV)e.y;
+        if (sizeof(RV) > sizeof(R)) {
+          const RV nr = rsqrt(cr * cr + sr * sr);
+          cr *= nr;
+          sr *= nr;
+        }
+        const RV x = row[gx], y = row[gy];
+        row[gx] = cr * x - sr * y;
+        row[gy] = sr * x + cr * y;
       }
       __syncwarp();
       if (++st == steps) {   // end of round (uniform over the CTA)

@@ -456,18 +456,29 @@ int small_svd_device(Ctx& c, const T* Bt, int64_t n, int l, int64_t ldb, double*
     // and shared memory) down to ~1e-5 orthogonality, then the fp64 sweeps
     // start from M V0 with V0 polished to an fp64-orthogonal matrix; the
     // quadratic convergence leaves only ~2 fp64 sweeps.
-    DBuf<float> M32(c, (size_t)l * l), V32(c, (size_t)l * l);
+    DBuf<float> M32(c, (size_t)l * l), V32;
     copy2d_kernel<double, float><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(M.p, l, l, l,
                                                                                 M32.p, l);
-    eye_kernel<float><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(V32.p, l);
     BRSVD_CHECK_LAUNCH();
     // predicted stop at sqrt(tol): this phase only preconditions the fp64 one
-    jacobi<float>(c, M32.p, l, l, l, V32.p, l, 1e-5, 40, 16.0 * l * 2.220446049250313e-16,
-                  /*stop_cos=*/std::sqrt(1.6e-5));
-    copy2d_kernel<float, double><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(V32.p, l, l, l,
-                                                                                Vj.p, l);
+    const double tol32 = std::max(1e-5, 8.0 * std::sqrt((double)l) * 1.1920928955078125e-07);
+    const double floor32 = 16.0 * l * 2.220446049250313e-16, stop32 = std::sqrt(1.6e-5);
+    eye_kernel<double><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(Vj.p, l);
     BRSVD_CHECK_LAUNCH();
-    ns_refine(c, Vj.p, l, l, 2);
+    // cluster tournament: its rotations are replayed on an fp64 V0, each
+    // renormalised in fp64, so V0 is orthogonal to fp64 rounding and needs
+    // no polish; otherwise fp32 V0, then two Newton-Schulz steps in fp64
+    if (!jacobi_cluster<float, double>(c, M32.p, l, l, Vj.p, l, tol32, floor32, 40, nullptr,
+                                       stop32)) {
+      V32.alloc(c, (size_t)l * l);
+      eye_kernel<float><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(V32.p, l);
+      BRSVD_CHECK_LAUNCH();
+      jacobi<float>(c, M32.p, l, l, l, V32.p, l, 1e-5, 40, floor32, stop32);
+      copy2d_kernel<float, double><<<grid_for((int64_t)l * l), 256, 0, c.stream>>>(
+          V32.p, l, l, l, Vj.p, l);
+      BRSVD_CHECK_LAUNCH();
+      ns_refine(c, Vj.p, l, l, 2);
+    }
     DBuf<double> M1(c, (size_t)l * l);
     gemm_nn_cm<double, double, double>(c, l, l, l, M.p, l, Vj.p, l, M1.p, l);
     BRSVD_CUDA(cudaMemcpyAsync(M.p, M1.p, sizeof(double) * l * l, cudaMemcpyDeviceToDevice,

@@ -327,8 +327,9 @@ bool jacobi_cluster_launch(Ctx& c, const JacobiClusterArgs<R>& args, int csize,
   return true;
 }
 
-template <typename R>
-bool jacobi_cluster(Ctx& c, R* G, int l, int64_t ldg, R* V, int64_t ldv, double tol,
+// RV: V's element type (fp64 V for the fp32 tournament: see jacobi_vreplay_kernel)
+template <typename R, typename RV = R>
+bool jacobi_cluster(Ctx& c, R* G, int l, int64_t ldg, RV* V, int64_t ldv, double tol,
                     double floor_rel, int max_sweeps, int* sweeps_done, double stop_cos = 0.0) {
   if (l > 512 || l < 64 || std::getenv("BRSVD_NO_CLUSTER_JACOBI")) return false;
   const size_t lim = c.max_smem_optin > 4096 ? c.max_smem_optin - 4096 : 0;
@@ -369,9 +370,9 @@ bool jacobi_cluster(Ctx& c, R* G, int l, int64_t ldg, R* V, int64_t ldv, double 
       const int rpw = 32 / bw;
       // shared memory sized so a replay CTA never shares an SM with a
       // tournament CTA (the latency-bound tournament would lose issue slots)
-      const size_t rs = std::max(jacobi_vreplay_smem(l, bw, csize, sizeof(R)),
+      const size_t rs = std::max(jacobi_vreplay_smem(l, bw, csize, sizeof(RV), sizeof(R)),
                                  std::min(lim, (size_t)c.max_smem_optin + 1024 - smem));
-      auto rk = jacobi_vreplay_kernel<R>;
+      auto rk = jacobi_vreplay_kernel<R, RV>;
       BRSVD_CUDA(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs));
       cudaLaunchConfig_t rc = {};
       rc.gridDim = dim3((unsigned)ceil_div(l, rpw));
