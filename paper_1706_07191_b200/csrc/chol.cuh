@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <cooperative_groups.h>
 #include "common.cuh"
 
@@ -187,8 +188,11 @@ __global__ void __launch_bounds__(kCiThreads, 1)
       for (int jj = 0; jj < kCiNB; ++jj)
         a[jj] = (i < nb && jj <= i) ? Lp[i * kCiLd + jj] : 0.0;
       const double2* b2 = reinterpret_cast<const double2*>(bcst + 32);
-#pragma unroll 1
-      for (int c = 0; c < nb; ++c) {
+      // one column; J = live row length bound for this column (32 - 8 g in
+      // phase g, columns 8 g .. 8 g + 7): entries a[J..] are zero and stay
+      // zero, so the rank-1 update and the broadcast loads stop at J
+      auto column = [&](auto Jc, int c) {
+        constexpr int J = decltype(Jc)::value;
         const double piv = __shfl_sync(0xffffffffu, a[0], c);
         const double dg = d0[p0 + c];
         const bool drop = !(piv > 0.0) ||
@@ -211,20 +215,25 @@ __global__ void __launch_bounds__(kCiThreads, 1)
         }
         // lanes i <= c hold lc = 0, so a[jj] of lanes i < c + jj only ever
         // gets lc_i * lc_j with one factor zero or is unused
+        double2 lj[J / 2];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          double2 lj[8];
+        for (int q = 0; q < J / 2; ++q) lj[q] = b2[q];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) lj[q] = b2[8 * h + q];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int jj = 16 * h + 2 * q + 1;
-            a[jj - 1] = fma(-lc, lj[q].x, a[jj]);
-            if (jj + 1 < kCiNB) a[jj] = fma(-lc, lj[q].y, a[jj + 1]);
-          }
+        for (int q = 0; q < J / 2; ++q) {
+          const int jj = 2 * q + 1;
+          a[jj - 1] = fma(-lc, lj[q].x, a[jj]);
+          if (jj + 1 < J) a[jj] = fma(-lc, lj[q].y, a[jj + 1]);
         }
-        a[kCiNB - 1] = 0.0;
-      }
+        a[J - 1] = 0.0;
+      };
+#pragma unroll 1
+      for (int c = 0; c < min(nb, 8); ++c) column(std::integral_constant<int, 32>{}, c);
+#pragma unroll 1
+      for (int c = 8; c < min(nb, 16); ++c) column(std::integral_constant<int, 24>{}, c);
+#pragma unroll 1
+      for (int c = 16; c < min(nb, 24); ++c) column(std::integral_constant<int, 16>{}, c);
+#pragma unroll 1
+      for (int c = 24; c < nb; ++c) column(std::integral_constant<int, 8>{}, c);
     }
     __syncthreads();
     if (pi == 0) CI_T(3);
